@@ -1,0 +1,757 @@
+// extern "C" surface (include/symsplit_b200.h). Each function validates like
+// the reference function it replaces, runs on the device, and converts
+// exceptions to status codes + a thread-local message.
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SS_OK;
+  } catch (const ssb::Failure& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SS_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SS_ERR_INVALID;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) ssb::fail(std::string(what) + " must not be null");
+}
+
+// The opaque ABI handles are the internal objects themselves.
+ssb::Matrix* M(ss_matrix_t a) {
+  need(a, "matrix");
+  return reinterpret_cast<ssb::Matrix*>(a);
+}
+ssb::Context* CX(ss_ctx_t c) {
+  need(c, "ctx");
+  return reinterpret_cast<ssb::Context*>(c);
+}
+ssb::Plan* PL(ss_plan_t p) {
+  need(p, "plan");
+  return reinterpret_cast<ssb::Plan*>(p);
+}
+ss_matrix_t wrap(ssb::Matrix* a) { return reinterpret_cast<ss_matrix_t>(a); }
+ss_plan_t wrap(ssb::Plan* p) { return reinterpret_cast<ss_plan_t>(p); }
+
+void use_device(ssb::Context* c) { SSB_CUDA(cudaSetDevice(c->device)); }
+
+template <class T>
+ssb::DBuf<T> to_device(ssb::Context* c, const T* h, std::int64_t n) {
+  ssb::DBuf<T> d(n);
+  if (n) {
+    need(h, "host buffer");
+    SSB_CUDA(cudaMemcpyAsync(d.get(), h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  }
+  return d;
+}
+
+template <class T>
+void to_host(ssb::Context* c, T* h, const T* d, std::int64_t n) {
+  if (n) {
+    need(h, "host buffer");
+    SSB_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  }
+  c->sync();
+}
+
+// reference solvers.cpp:28-36
+void check_system(std::int64_t rows, const double* p, std::int64_t m, const char* op) {
+  if (m != rows) {
+    std::ostringstream msg;
+    msg << op << ": rhs length " << m << " does not match rows " << rows;
+    ssb::fail(msg.str());
+  }
+  for (std::int64_t i = 0; i < m; ++i) {
+    if (!std::isfinite(p[i])) ssb::fail(std::string(op) + ": non-finite rhs");
+  }
+}
+
+void check_options(const ss_solve_options& o) {
+  if (o.relaxation <= 0 || o.relaxation > 2) ssb::fail("sart_solve: relaxation must be in (0, 2]");
+  if (o.max_iters < 1) ssb::fail("sart_solve: max_iters must be >= 1");
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ||A f - p|| and ||f|| on the device in fp64, after the timed loop like the
+// reference (solvers.cpp:194-197, :266-267).
+void fill_report(ssb::Matrix& a, const double* f_dev, const double* p_dev, ss_solve_report* rep) {
+  ssb::DBuf<double> r(a.rows);
+  ssb::residual_dev(a, f_dev, p_dev, r.get());
+  rep->residual_norm = std::sqrt(ssb::norm2_dev(a.ctx, r.get(), a.rows));
+  rep->solution_norm = std::sqrt(ssb::norm2_dev(a.ctx, f_dev, a.cols));
+}
+
+// reference centro.cpp:27-42 message
+std::string symmetry_message(const char* op, const ss_symmetry_report& r, double tol) {
+  std::ostringstream msg;
+  msg << op << ": matrix is not centrosymmetric";
+  if (r.status == 1) {
+    msg << " (odd row count)";
+  } else if (r.status == 2) {
+    msg << " (odd column count)";
+  } else {
+    msg << " (max violation " << r.max_violation << " at (" << r.worst_row << ","
+        << r.worst_col << "), tol " << tol << ")";
+  }
+  return msg.str();
+}
+
+struct SplitOut {
+  std::unique_ptr<ssb::Matrix> a1, a2;
+  ssb::DBuf<double> p1, p2;
+  double fills[3] = {0, 0, 0};
+};
+
+// reference split_system (centro.cpp:144-156) on the device
+void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double tol, SplitOut& o,
+                  ss_symmetry_report* rep) {
+  if (m != a.rows) ssb::fail("split_system: right-hand side length does not match rows");
+  const ss_symmetry_report r = ssb::verify_symmetry(a, tol);
+  if (!r.holds) {
+    if (rep) *rep = r;
+    throw ssb::Failure(SS_ERR_SYMMETRY, symmetry_message("split_system", r, tol));
+  }
+  ssb::Matrix *x = nullptr, *y = nullptr;
+  ssb::fold(a, x, y);
+  o.a1.reset(x);
+  o.a2.reset(y);
+  o.p1.alloc(m / 2);
+  o.p2.alloc(m / 2);
+  ssb::split_rhs_dev(a.ctx, p_dev, o.p1.get(), o.p2.get(), m / 2);
+  const double parent = static_cast<double>(a.rows) * static_cast<double>(a.cols);
+  const double half = static_cast<double>(o.a1->rows) * static_cast<double>(o.a1->cols);
+  o.fills[0] = parent > 0 ? static_cast<double>(ssb::nonzeros(a)) / parent : 0.0;
+  o.fills[1] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a1)) / half : 0.0;
+  o.fills[2] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a2)) / half : 0.0;
+}
+
+ssb::Grid to_grid(const ss_grid_spec* g) {
+  need(g, "grid");
+  ssb::Grid o;
+  o.n_x = g->n_x;
+  o.n_y = g->n_y;
+  o.voxel_size = g->voxel_size;
+  o.center_x = g->center_x;
+  o.y_bottom = g->y_bottom;
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ss_last_error(void) { return g_err.c_str(); }
+
+int ss_version(void) { return 1; }
+
+void ss_default_options(ss_solve_options* o) {
+  o->max_iters = 200;
+  o->tol = 1e-10;
+  o->relaxation = 1.0;
+  o->parallelism = 0;
+  o->dtype = SS_F64;
+}
+
+int ss_device_count(int* out) {
+  return guarded([&] { SSB_CUDA(cudaGetDeviceCount(out)); });
+}
+
+int ss_ctx_create(int device, ss_ctx_t* out) {
+  return guarded([&] {
+    need(out, "out");
+    SSB_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<ssb::Context>();
+    c->device = device;
+    SSB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    SSB_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    int l2 = 0;
+    SSB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+    c->l2_bytes = static_cast<std::size_t>(l2);
+    *out = reinterpret_cast<ss_ctx_t>(c.release());
+  });
+}
+
+int ss_ctx_destroy(ss_ctx_t h) {
+  return guarded([&] {
+    if (!h) return;
+    ssb::Context* ctx = CX(h);
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->comm));
+    ctx->scratch.release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int ss_ctx_synchronize(ss_ctx_t h) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    use_device(ctx);
+    ctx->sync();
+  });
+}
+
+void* ss_ctx_stream(ss_ctx_t h) {
+  return h ? static_cast<void*>(reinterpret_cast<ssb::Context*>(h)->stream) : nullptr;
+}
+
+int64_t ss_ctx_launch_count(ss_ctx_t h) {
+  return h ? reinterpret_cast<ssb::Context*>(h)->launches : 0;
+}
+
+// ------------------------------------------------------------ matrices
+int ss_matrix_from_csc(ss_ctx_t h, int64_t rows, int64_t cols, int64_t nnz, const int32_t* outer,
+                       const int32_t* inner, const double* values, ss_matrix_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(out, "out");
+    need(outer, "outer");
+    use_device(ctx);
+    *out = wrap(ssb::matrix_from_csc_host(ctx, rows, cols, nnz, outer, inner, values));
+  });
+}
+
+int ss_matrix_from_triplets(ss_ctx_t h, int64_t rows, int64_t cols, int64_t count,
+                            const int32_t* row, const int32_t* col, const double* values,
+                            ss_matrix_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::matrix_from_triplets_host(ctx, rows, cols, count, row, col, values));
+  });
+}
+
+int ss_matrix_destroy(ss_matrix_t a) {
+  return guarded([&] {
+    if (!a) return;
+    ssb::Matrix* m = M(a);
+    cudaSetDevice(m->ctx->device);
+    m->ctx->sync();
+    delete m;
+  });
+}
+
+int ss_matrix_shape(ss_matrix_t a, int64_t* rows, int64_t* cols, int64_t* stored) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    if (rows) *rows = m->rows;
+    if (cols) *cols = m->cols;
+    if (stored) *stored = m->nnz;
+  });
+}
+
+int ss_matrix_nonzeros(ss_matrix_t a, int64_t* out) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    *out = ssb::nonzeros(*m);
+  });
+}
+
+int ss_matrix_fill_ratio(ss_matrix_t a, double* out) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    const double size = static_cast<double>(m->rows) * static_cast<double>(m->cols);
+    *out = size > 0 ? static_cast<double>(ssb::nonzeros(*m)) / size : 0.0;
+  });
+}
+
+int ss_matrix_download_csr(ss_matrix_t a, int32_t* ptr, int32_t* idx, double* values) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    if (ptr) to_host(m->ctx, ptr, m->rowptr.get(), m->rows + 1);
+    if (idx) to_host(m->ctx, idx, m->colidx.get(), m->nnz);
+    if (values) to_host(m->ctx, values, m->val.get(), m->nnz);
+  });
+}
+
+int ss_matrix_download_csc(ss_matrix_t a, int32_t* outer, int32_t* inner, double* values) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    m->ensure_csc();
+    if (outer) to_host(m->ctx, outer, m->colptr.get(), m->cols + 1);
+    if (inner) to_host(m->ctx, inner, m->rowidx.get(), m->nnz);
+    if (values) to_host(m->ctx, values, m->cval.get(), m->nnz);
+  });
+}
+
+int ss_matrix_apply(ss_matrix_t a, const double* x, double* y) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    ssb::Context* c = m->ctx;
+    use_device(c);
+    auto dx = to_device(c, x, m->cols);
+    ssb::DBuf<double> dy(m->rows);
+    ssb::apply_dev(*m, dx.get(), dy.get());
+    to_host(c, y, dy.get(), m->rows);
+  });
+}
+
+int ss_matrix_apply_transpose(ss_matrix_t a, const double* y, double* x) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    ssb::Context* c = m->ctx;
+    use_device(c);
+    auto dy = to_device(c, y, m->rows);
+    ssb::DBuf<double> dx(m->cols);
+    ssb::apply_transpose_dev(*m, dy.get(), dx.get());
+    to_host(c, x, dx.get(), m->cols);
+  });
+}
+
+// ------------------------------------------------------------ geometry
+int ss_parse_scan_config(const char* text, ss_scan_config* out) {
+  return guarded([&] {
+    need(text, "text");
+    need(out, "out");
+    *out = ssb::parse_scan_config(text);
+  });
+}
+
+int ss_make_grid(const ss_scan_config* cfg, ss_grid_spec* out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    const ssb::Grid g = ssb::make_grid(*cfg);
+    *out = ss_grid_spec{g.n_x, g.n_y, g.voxel_size, g.center_x, g.y_bottom};
+  });
+}
+
+int ss_snake_index(int c, int r, const ss_grid_spec* grid, int* j) {
+  return guarded([&] { *j = ssb::snake_index(c, r, to_grid(grid)); });
+}
+
+int ss_snake_inverse(int j, const ss_grid_spec* grid, int* c, int* r) {
+  return guarded([&] {
+    auto [a, b] = ssb::snake_inverse(j, to_grid(grid));
+    *c = a;
+    *r = b;
+  });
+}
+
+int ss_enumerate_rays(const ss_scan_config* cfg, double* rays4, int64_t* count, int* samples,
+                      double* pitch) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    const ssb::Grid g = ssb::make_grid(*cfg);
+    const ssb::RayTable t = ssb::enumerate_rays(*cfg, g, rays4 != nullptr);
+    *count = t.m;
+    if (samples) *samples = t.samples;
+    if (pitch) *pitch = t.pitch;
+    if (rays4) std::memcpy(rays4, t.all4.data(), t.all4.size() * sizeof(double));
+  });
+}
+
+int ss_build_system(ss_ctx_t h, const ss_scan_config* cfg, int parallelism, ss_matrix_t* out) {
+  (void)parallelism;  // the device build is identical for any worker count
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(cfg, "cfg");
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::build_system(ctx, *cfg));
+  });
+}
+
+// ------------------------------------------------------------ centro
+int ss_verify_symmetry(ss_matrix_t a, double tol, ss_symmetry_report* out) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    *out = ssb::verify_symmetry(*m, tol);
+  });
+}
+
+int ss_split_rhs(ss_ctx_t h, const double* p, int64_t m, double* p1, double* p2) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    if (m % 2 != 0) ssb::fail("split_rhs: vector length must be even");
+    use_device(ctx);
+    auto dp = to_device(ctx, p, m);
+    ssb::DBuf<double> d1(m / 2), d2(m / 2);
+    ssb::split_rhs_dev(ctx, dp.get(), d1.get(), d2.get(), m / 2);
+    to_host(ctx, p1, d1.get(), m / 2);
+    to_host(ctx, p2, d2.get(), m / 2);
+  });
+}
+
+int ss_split_system(ss_matrix_t a, const double* p, int64_t m, double symmetry_tol,
+                    ss_matrix_t* a1, ss_matrix_t* a2, double* p1, double* p2, double* fills,
+                    ss_symmetry_report* report) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    need(a1, "a1");
+    need(a2, "a2");
+    auto dp = to_device(c, p, m);
+    SplitOut o;
+    split_device(*A, dp.get(), m, symmetry_tol, o, report);
+    to_host(c, p1, o.p1.get(), m / 2);
+    to_host(c, p2, o.p2.get(), m / 2);
+    if (fills) std::memcpy(fills, o.fills, sizeof o.fills);
+    *a1 = wrap(o.a1.release());
+    *a2 = wrap(o.a2.release());
+  });
+}
+
+int ss_decompose_solution(ss_ctx_t h, const double* f, int64_t n, double* f1, double* f2) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    if (n % 2 != 0) ssb::fail("decompose_solution: vector length must be even");
+    use_device(ctx);
+    auto df = to_device(ctx, f, n);
+    ssb::DBuf<double> d1(n / 2), d2(n / 2);
+    ssb::decompose_dev(ctx, df.get(), d1.get(), d2.get(), n / 2);
+    to_host(ctx, f1, d1.get(), n / 2);
+    to_host(ctx, f2, d2.get(), n / 2);
+  });
+}
+
+int ss_recombine_solution(ss_ctx_t h, const double* f1, const double* f2, int64_t nh,
+                          double* f) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    use_device(ctx);
+    auto d1 = to_device(ctx, f1, nh);
+    auto d2 = to_device(ctx, f2, nh);
+    if (!ssb::all_finite_dev(ctx, d1.get(), nh) || !ssb::all_finite_dev(ctx, d2.get(), nh)) {
+      ssb::fail("recombine_solution: non-finite component");
+    }
+    ssb::DBuf<double> df(2 * nh);
+    ssb::recombine_dev(ctx, d1.get(), d2.get(), df.get(), nh, 1);
+    to_host(ctx, f, df.get(), 2 * nh);
+  });
+}
+
+// ------------------------------------------------------------ solvers
+int ss_sart_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
+                  double* f, int64_t n, ss_solve_report* report, double* history) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    need(opts, "opts");
+    check_system(A->rows, p, m, "sart_solve");
+    check_options(*opts);
+    if (n != A->cols) ssb::fail("sart_solve: solution length does not match columns");
+    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, A, nullptr, *opts, 1));
+    P->set_rhs_host(0, p);
+    P->launch();
+    ss_solve_report rep{};
+    P->finish(&rep);
+    P->get_solution(0, f);
+    auto fd = to_device(c, f, n);
+    auto dp = to_device(c, p, m);
+    fill_report(*A, fd.get(), dp.get(), &rep);
+    int len = 0;
+    P->get_history(0, 0, history, &len);
+    rep.history_len = len;
+    if (report) *report = rep;
+  });
+}
+
+int ss_solve_direct(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
+                    double* f, int64_t n, ss_solve_report* report) {
+  return ss_sart_solve(a, p, m, opts, f, n, report, nullptr);
+}
+
+int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_tol,
+                   const ss_solve_options* opts, double* f, int64_t n, ss_solve_report* report) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    need(opts, "opts");
+    const double t0 = now();
+    auto dp = to_device(c, p, m);
+    SplitOut o;
+    split_device(*A, dp.get(), m, symmetry_tol, o, nullptr);
+    c->sync();
+    const double split_seconds = now() - t0;
+    if (n != A->cols) ssb::fail("solve_split: solution length does not match columns");
+    // Branch validation in the reference's order; failures of both branches
+    // aggregate into one message (solvers.cpp:235-247).
+    std::string errs[2];
+    auto raise_if_failed = [&](int code) {
+      if (errs[0].empty() && errs[1].empty()) return;
+      std::ostringstream msg;
+      msg << "solve_split: branch failure:";
+      for (int s = 0; s < 2; ++s) {
+        if (!errs[s].empty()) msg << " [system " << s + 1 << "] " << errs[s];
+      }
+      throw ssb::Failure(code, msg.str());
+    };
+    const std::int64_t mh = m / 2;
+    std::vector<double> hp(static_cast<std::size_t>(mh));
+    for (int s = 0; s < 2; ++s) {
+      to_host(c, hp.data(), (s ? o.p2 : o.p1).get(), mh);
+      try {
+        check_system(o.a1->rows, hp.data(), mh, "sart_solve");
+        check_options(*opts);
+      } catch (const ssb::Failure& e) {
+        errs[s] = e.what();
+      }
+    }
+    raise_if_failed(SS_ERR_INVALID);
+    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1));
+    for (int s = 0; s < 2; ++s) {
+      if (P->empty_rows[s]) errs[s] = "sart_solve: matrix has no nonzero rows";
+    }
+    raise_if_failed(SS_ERR_INVALID);
+    P->set_rhs_device_f64(0, o.p1.get());
+    P->set_rhs_device_f64(1, o.p2.get());
+    P->launch();
+    ss_solve_report rep{};
+    try {
+      P->finish(&rep);
+    } catch (const ssb::Failure& e) {
+      if (e.code != SS_ERR_DIVERGED) throw;
+      for (int s = 0; s < 2; ++s) {
+        const int at = P->diverged_at(s);
+        if (at) {
+          errs[s] = "sart_solve: diverged (non-finite iterate at iteration " +
+                    std::to_string(at) + ")";
+        }
+      }
+      raise_if_failed(SS_ERR_DIVERGED);
+    }
+    const double t_rec0 = now();
+    ssb::DBuf<double> fd(n);
+    P->recombine_device(fd.get());
+    to_host(c, f, fd.get(), n);
+    const double recombine_seconds = now() - t_rec0;
+    fill_report(*A, fd.get(), dp.get(), &rep);
+    rep.split_seconds = split_seconds;
+    rep.recombine_seconds = recombine_seconds;
+    rep.wall_time_seconds = split_seconds + rep.branch1_seconds + recombine_seconds;
+    rep.history_len = 0;  // solve_split's report carries no history
+    if (report) *report = rep;
+  });
+}
+
+// ------------------------------------------------------------ phantom
+int ss_random_ellipses(uint64_t seed, int count, double* out6) {
+  return guarded([&] {
+    if (count < 0) ssb::fail("random_ellipses: count must be >= 0");
+    ssb::random_ellipses(seed, count, out6);
+  });
+}
+
+int ss_rasterize(ss_ctx_t h, const double* ellipses6, int count, const ss_grid_spec* grid,
+                 double* values) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    use_device(ctx);
+    const ssb::Grid g = to_grid(grid);
+    g.validate();
+    const std::int64_t n = static_cast<std::int64_t>(g.n_x) * g.n_y;
+    ssb::DBuf<double> out(n);
+    ssb::rasterize_dev(ctx, ellipses6, count, g, out.get());
+    to_host(ctx, values, out.get(), n);
+  });
+}
+
+int ss_forward_project(ss_matrix_t a, const double* f, double* p) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    for (std::int64_t j = 0; j < A->cols; ++j) {
+      if (!std::isfinite(f[j])) ssb::fail("forward_project: non-finite image");
+    }
+    auto df = to_device(c, f, A->cols);
+    ssb::DBuf<double> dp(A->rows);
+    ssb::forward_project_dev(*A, df.get(), dp.get());
+    to_host(c, p, dp.get(), A->rows);
+  });
+}
+
+int ss_add_noise(double* p, int64_t m, double sigma, uint64_t seed) {
+  return guarded([&] { ssb::add_noise(p, m, sigma, seed); });
+}
+
+// ------------------------------------------------------------ plans
+int ss_plan_create(ss_ctx_t h, ss_matrix_t a1, ss_matrix_t a2, const ss_solve_options* opts,
+                   int nrhs, ss_plan_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(out, "out");
+    use_device(ctx);
+    check_options(*opts);
+    *out = wrap(ssb::make_plan(ctx, M(a1), a2 ? M(a2) : nullptr, *opts, nrhs));
+  });
+}
+
+int ss_plan_destroy(ss_plan_t plan) {
+  return guarded([&] {
+    if (!plan) return;
+    ssb::Plan* P = PL(plan);
+    cudaSetDevice(P->ctx->device);
+    P->ctx->sync();
+    delete P;
+  });
+}
+
+int ss_plan_set_rhs(ss_plan_t plan, int which, const double* p) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(p, "p");
+    P->set_rhs_host(which, p);
+  });
+}
+
+int ss_plan_set_rhs_device(ss_plan_t plan, int which, const void* p_dev) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(p_dev, "p_dev");
+    P->set_rhs_device(which, p_dev);
+  });
+}
+
+int ss_plan_launch(ss_plan_t plan) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    P->launch();
+  });
+}
+
+int ss_plan_finish(ss_plan_t plan, ss_solve_report* report) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    P->finish(report);
+  });
+}
+
+int ss_plan_get_solution(ss_plan_t plan, int which, double* f) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(f, "f");
+    P->get_solution(which, f);
+  });
+}
+
+int ss_plan_get_history(ss_plan_t plan, int which, int slice, double* hist, int* len) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(len, "len");
+    P->get_history(which, slice, hist, len);
+  });
+}
+
+int ss_plan_recombine(ss_plan_t plan, double* f) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(f, "f");
+    P->recombine(f);
+  });
+}
+
+void* ss_plan_solution_device(ss_plan_t plan, int which) {
+  if (!plan) return nullptr;
+  ssb::Plan* P = reinterpret_cast<ssb::Plan*>(plan);
+  if (which < 0 || which >= P->nsys) return nullptr;
+  return P->x[which].get();
+}
+
+int ss_plan_stats(ss_plan_t plan, int64_t* mb, int64_t* vb, int* kernels) {
+  return guarded([&] { PL(plan)->stats(mb, vb, kernels); });
+}
+
+int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(fwd_ms, "fwd_ms");
+    need(back_ms, "back_ms");
+    P->profile(iters, fwd_ms, back_ms);
+  });
+}
+
+// ------------------------------------------------------------ multi-GPU
+int ss_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    need(out128, "out");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+      ssb::fail(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r), SS_ERR_NCCL);
+    }
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int ss_ctx_attach_nccl(ss_ctx_t h, const void* uid, int nranks, int rank) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(uid, "unique_id");
+    use_device(ctx);
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclComm_t comm;
+    const ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      ssb::fail(std::string("ncclCommInitRank: ") + ncclGetErrorString(r), SS_ERR_NCCL);
+    }
+    ctx->comm = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+int ss_partition_rows(const int32_t* rowptr, int64_t rows, int parts, int64_t* bounds) {
+  return guarded([&] {
+    need(rowptr, "rowptr");
+    need(bounds, "bounds");
+    ssb::partition_rows(rowptr, rows, parts, bounds);
+  });
+}
+
+int ss_plan_create_sharded(ss_ctx_t h, ss_matrix_t a, int64_t row_begin, int64_t row_end,
+                           const ss_solve_options* opts, ss_plan_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::make_sharded_plan(ctx, M(a), row_begin, row_end, *opts));
+  });
+}
+
+}  // extern "C"

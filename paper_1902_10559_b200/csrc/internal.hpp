@@ -1,0 +1,185 @@
+// Internal types of the symsplit_b200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/symsplit_b200.h"
+
+namespace ssb {
+
+// Status-carrying exception; the C ABI maps it to SS_ERR_* + message.
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(const std::string& msg, int code = SS_ERR_INVALID) {
+  throw Failure(code, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw Failure(SS_ERR_OOM, std::string(what) + ": out of device memory");
+  }
+  throw Failure(SS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define SSB_CUDA(x) ::ssb::cuda_check((x), #x)
+
+// Owning device buffer (cudaMalloc; 256-byte aligned, which the 128-bit
+// loads of the SpMV kernels rely on).
+template <class T>
+class DBuf {
+ public:
+  DBuf() = default;
+  explicit DBuf(std::size_t n) { alloc(n); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(std::size_t n) {
+    release();
+    if (n == 0) n = 1;  // keep a valid pointer for empty arrays
+    void* q = nullptr;
+    SSB_CUDA(cudaMalloc(&q, n * sizeof(T)));
+    p_ = static_cast<T*>(q);
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+  explicit operator bool() const { return p_ != nullptr; }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  std::size_t l2_bytes = 0;
+  std::int64_t launches = 0;
+  DBuf<char> scratch;  // CUB temporary storage, grown on demand
+  // NCCL (row-sharded plans); opaque to avoid the header here
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  void* temp(std::size_t bytes) {
+    if (scratch.size() < bytes) scratch.alloc(bytes + bytes / 4);
+    return scratch.get();
+  }
+  void launched(int n = 1) { launches += n; }
+  void sync() { SSB_CUDA(cudaStreamSynchronize(stream)); }
+  void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) cuda_check(e, what);
+    ++launches;
+  }
+};
+
+// Device sparse matrix: CSR master (fp64, int32 — Eigen's int StorageIndex),
+// CSC and fp32 copies built on demand. Rows/cols are 0-based.
+struct Matrix {
+  Context* ctx = nullptr;
+  std::int64_t rows = 0, cols = 0, nnz = 0;
+  DBuf<int> rowptr, colidx;
+  DBuf<double> val;
+  bool has_csc = false;
+  DBuf<int> colptr, rowidx;
+  DBuf<double> cval;
+  bool has_f32 = false;
+  DBuf<float> val32, cval32;
+
+  void ensure_csc();
+  void ensure_f32();
+};
+
+// ---------------------------------------------------------------- host geometry
+struct Grid {
+  int n_x = 32, n_y = 32;
+  double voxel_size = 0.1 / 32, center_x = 0.0, y_bottom = 0.25;
+  int cell_count() const { return n_x * n_y; }
+  double width() const { return n_x * voxel_size; }
+  double height() const { return n_y * voxel_size; }
+  double x_left() const { return center_x - 0.5 * width(); }
+  double x_right() const { return center_x + 0.5 * width(); }
+  double y_top() const { return y_bottom + height(); }
+  void validate() const;
+};
+
+struct RayTable {  // traced half, structure of arrays (host)
+  std::int64_t m = 0;  // total rays M (both halves)
+  int samples = 0;
+  double pitch = 0.0;
+  std::vector<double> sx, sy, dx, dy, seg_len, t_in, t_out;  // M/2 each
+  std::vector<double> all4;                                  // optional (sx,sy,dx,dy) x M
+};
+
+void validate_geometry(const ss_scan_config& c);
+Grid make_grid(const ss_scan_config& c);
+RayTable enumerate_rays(const ss_scan_config& c, const Grid& g, bool keep_all);
+ss_scan_config parse_scan_config(const std::string& text);
+int snake_index(int c, int r, const Grid& g);
+std::pair<int, int> snake_inverse(int j, const Grid& g);
+void random_ellipses(std::uint64_t seed, int count, double* out6);
+void add_noise(double* p, std::int64_t m, double sigma, std::uint64_t seed);
+
+// ---------------------------------------------------------------- device ops (ops.cu)
+Matrix* matrix_from_csr_device(Context* ctx, std::int64_t rows, std::int64_t cols,
+                               std::int64_t nnz, DBuf<int>&& rowptr, DBuf<int>&& colidx,
+                               DBuf<double>&& val);
+Matrix* matrix_from_sorted_triplets(Context* ctx, std::int64_t rows, std::int64_t cols,
+                                    std::int64_t count, unsigned long long* keys,
+                                    double* vals);
+Matrix* matrix_from_triplets_host(Context* ctx, std::int64_t rows, std::int64_t cols,
+                                  std::int64_t count, const int* r, const int* c,
+                                  const double* v);
+Matrix* matrix_from_csc_host(Context* ctx, std::int64_t rows, std::int64_t cols,
+                             std::int64_t nnz, const int* outer, const int* inner,
+                             const double* v);
+Matrix* build_system(Context* ctx, const ss_scan_config& cfg);
+void check_finite(Matrix& a);
+std::int64_t nonzeros(Matrix& a);
+ss_symmetry_report verify_symmetry(Matrix& a, double tol);
+void fold(Matrix& a, Matrix*& a1, Matrix*& a2);
+void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh);
+void recombine_dev(Context* ctx, const double* f1, const double* f2, double* f,
+                   std::int64_t nh, std::int64_t nrhs);
+void decompose_dev(Context* ctx, const double* f, double* f1, double* f2, std::int64_t nh);
+void abs_sums(Matrix& a, double* row_sums, double* col_sums);
+void apply_dev(Matrix& a, const double* x, double* y);            // y = A x
+void apply_transpose_dev(Matrix& a, const double* y, double* x);  // x = A^T y
+void residual_dev(Matrix& a, const double* x, const double* p, double* r);  // r = A x - p
+double norm2_dev(Context* ctx, const double* v, std::int64_t n);  // deterministic sum of squares
+double max_dev(Context* ctx, const double* v, std::int64_t n);
+bool all_finite_dev(Context* ctx, const double* v, std::int64_t n);
+void rasterize_dev(Context* ctx, const double* ell6, int count, const Grid& g, double* out);
+void forward_project_dev(Matrix& a, const double* f, double* p);
+
+template <class T>
+void cast_dev(Context* ctx, const double* src, T* dst, std::int64_t n);
+
+}  // namespace ssb

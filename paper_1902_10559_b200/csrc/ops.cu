@@ -1,0 +1,1081 @@
+// Device operations of the build side of the path: Siddon tracer, CSR/CSC
+// construction, centrosymmetric fold, symmetry check, normalisers, phantom
+// rasterisation and folded forward projection.
+//
+// Bit-exactness contract: every floating-point operation
+// here reproduces the reference's scalar expression with round-to-nearest
+// and no contraction. The file is compiled with -fmad=false and the
+// arithmetic is spelled with __d*_rn intrinsics so that a flag change cannot
+// silently introduce an FMA. Integer/index work is exact by construction.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.hpp"
+
+namespace ssb {
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+
+int grid_for(Context* ctx, std::int64_t n, int threads = kT) {
+  const std::int64_t want = (n + threads - 1) / threads;
+  const std::int64_t cap = static_cast<std::int64_t>(ctx->sm_count) * 16;
+  return static_cast<int>(std::max<std::int64_t>(1, std::min(want, cap)));
+}
+
+int bits_for(std::int64_t v) {  // bits needed to represent values in [0, v)
+  int b = 1;
+  while ((std::int64_t{1} << b) < v) ++b;
+  return b;
+}
+
+// ------------------------------------------------------------------ tracer
+struct TraceArgs {
+  const double *sx, *sy, *dx, *dy, *seg, *tin, *tout;
+  const double *xb, *yb;  // boundary abscissae k = 0..n_x, ordinates k = 0..n_y
+  int nx, ny;
+  double vs, x_left, y_bottom;
+  std::int64_t mh;
+};
+
+// Next parametric crossing of one axis strictly inside (t_in, t_out), or +inf.
+// The boundary sequence is monotone in k and so is (b_k - p0)/d, hence the
+// in-range candidates are one contiguous run that this cursor walks in
+// increasing t (reference collects all k and std::sorts; equal values are
+// bitwise identical so their relative order cannot matter).
+struct AxisCursor {
+  const double* b;
+  double p0, d, tin, tout;
+  int k, kend, step;
+  __device__ double next() {
+    while (k != kend) {
+      const double t = dvd(sub(b[k], p0), d);
+      k += step;
+      if (t > tin) {
+        if (t < tout) return t;
+        k = kend;
+        break;
+      }
+    }
+    return __longlong_as_double(0x7ff0000000000000LL);
+  }
+};
+
+// Walk of reference ray_weights (geometry.cpp:175-225) for traced ray i:
+// sorted crossings -> per-segment midpoint cell -> snake column, lengths
+// of consecutive equal cells merged with +=. emit(col0, len) per entry.
+template <class Emit>
+__device__ void walk_ray(const TraceArgs& a, std::int64_t i, Emit&& emit) {
+  const double sx = a.sx[i], sy = a.sy[i], dx = a.dx[i], dy = a.dy[i];
+  const double seg = a.seg[i], tin = a.tin[i], tout = a.tout[i];
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  AxisCursor cx{a.xb, sx, dx, tin, tout, 0, 0, 1};
+  if (dx > 0.0) {
+    cx.k = 0; cx.kend = a.nx + 1; cx.step = 1;
+  } else if (dx < 0.0) {
+    cx.k = a.nx; cx.kend = -1; cx.step = -1;
+  }
+  AxisCursor cy{a.yb, sy, dy, tin, tout, 0, 0, 1};
+  if (dy > 0.0) {
+    cy.k = 0; cy.kend = a.ny + 1; cy.step = 1;
+  } else if (dy < 0.0) {
+    cy.k = a.ny; cy.kend = -1; cy.step = -1;
+  }
+  double tx = cx.next(), ty = cy.next();
+  double ta = tin;
+  int pc = -1;
+  double plen = 0.0;
+  for (;;) {
+    double tb;
+    bool last = false;
+    if (tx <= ty) {
+      if (tx == INF) {
+        tb = tout;
+        last = true;
+      } else {
+        tb = tx;
+        tx = cx.next();
+      }
+    } else {
+      tb = ty;
+      ty = cy.next();
+    }
+    if (tb > ta) {
+      const double tm = mul(0.5, add(ta, tb));
+      const double xm = add(sx, mul(tm, dx));
+      const double ym = add(sy, mul(tm, dy));
+      int c = static_cast<int>(floor(dvd(sub(xm, a.x_left), a.vs)));
+      c = min(max(c, 0), a.nx - 1);
+      int fb = static_cast<int>(floor(dvd(sub(ym, a.y_bottom), a.vs)));
+      fb = min(max(fb, 0), a.ny - 1);
+      // snake_index(c+1, n_y-fb) - 1: odd 1-based columns run top->bottom
+      const int col = (c & 1) ? c * a.ny + fb : c * a.ny + (a.ny - 1 - fb);
+      const double len = mul(sub(tb, ta), seg);
+      if (col == pc) {
+        plen = add(plen, len);
+      } else {
+        if (pc >= 0) emit(pc, plen);
+        pc = col;
+        plen = len;
+      }
+    }
+    ta = tb;
+    if (last) break;
+  }
+  if (pc >= 0) emit(pc, plen);
+}
+
+__global__ void trace_count_kernel(TraceArgs a, int* counts) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < a.mh;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    int n = 0;
+    walk_ray(a, i, [&](int, double) { ++n; });
+    counts[i] = n;
+  }
+}
+
+__global__ void trace_fill_kernel(TraceArgs a, const std::int64_t* offsets,
+                                  unsigned long long* keys, double* vals) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < a.mh;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    std::int64_t o = offsets[i];
+    const unsigned long long rowkey = static_cast<unsigned long long>(i) << 32;
+    walk_ray(a, i, [&](int col, double len) {
+      keys[o] = rowkey | static_cast<unsigned int>(col);
+      vals[o] = len;
+      ++o;
+    });
+  }
+}
+
+// ------------------------------------------------------------------ sorted triplets -> CSR
+__global__ void head_flags_kernel(const unsigned long long* keys, std::int64_t n, int* head) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    head[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+  }
+}
+
+// Repeated (row,col) runs are summed left to right in stable (insertion)
+// order — Eigen collapseDuplicates: first slot kept, value = acc + next.
+__global__ void collapse_kernel(const unsigned long long* keys, const double* vals,
+                                const int* head, const std::int64_t* pos, std::int64_t n,
+                                int* col_out, int* row_out, double* val_out) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    if (!head[k]) continue;
+    double acc = vals[k];
+    std::int64_t e = k + 1;
+    while (e < n && keys[e] == keys[k]) {
+      acc = add(acc, vals[e]);
+      ++e;
+    }
+    const std::int64_t o = pos[k];
+    col_out[o] = static_cast<int>(keys[k] & 0xffffffffull);
+    row_out[o] = static_cast<int>(keys[k] >> 32);
+    val_out[o] = acc;
+  }
+}
+
+__global__ void split_keys_kernel(const unsigned long long* keys, std::int64_t n, int* col_out,
+                                  int* row_out) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    col_out[k] = static_cast<int>(keys[k] & 0xffffffffull);
+    row_out[k] = static_cast<int>(keys[k] >> 32);
+  }
+}
+
+// ptr[r] = first position whose (sorted) outer index is >= r.
+__global__ void ptr_from_sorted_kernel(const int* outer_of, std::int64_t n, std::int64_t outer,
+                                       int* ptr) {
+  for (std::int64_t u = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; u <= n;
+       u += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t prev = (u == 0) ? -1 : outer_of[u - 1];
+    const std::int64_t cur = (u == n) ? outer : outer_of[u];
+    for (std::int64_t r = prev + 1; r <= cur; ++r) ptr[r] = static_cast<int>(u);
+  }
+}
+
+__global__ void iota_kernel(int* v, std::int64_t n) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    v[k] = static_cast<int>(k);
+  }
+}
+
+__global__ void expand_ptr_kernel(const int* ptr, std::int64_t outer, int* outer_of) {
+  for (std::int64_t r = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; r < outer;
+       r += (std::int64_t)gridDim.x * blockDim.x) {
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) outer_of[k] = static_cast<int>(r);
+  }
+}
+
+__global__ void gather_kernel(const int* perm, const int* src_idx, const double* src_val,
+                              std::int64_t n, int* dst_idx, double* dst_val) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    const int s = perm[k];
+    dst_idx[k] = src_idx[s];
+    dst_val[k] = src_val[s];
+  }
+}
+
+// Full A from the traced half by the mirror rule (geometry.cpp:257-269):
+// row M-1-i holds (N-1-j, len) of row i, so the mirrored half of the CSR
+// arrays is the traced half reversed with columns reflected.
+__global__ void mirror_fill_kernel(int* col, double* val, std::int64_t half, std::int64_t n) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < half;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t d = 2 * half - 1 - k;
+    col[d] = static_cast<int>(n - 1 - col[k]);
+    val[d] = val[k];
+  }
+}
+
+__global__ void mirror_ptr_kernel(int* ptr, std::int64_t mh, std::int64_t half) {
+  // ptr[mh + t] = 2H - ptr[mh - t] for t = 1..mh
+  for (std::int64_t t = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x + 1; t <= mh;
+       t += (std::int64_t)gridDim.x * blockDim.x) {
+    ptr[mh + t] = static_cast<int>(2 * half - ptr[mh - t]);
+  }
+}
+
+template <class T>
+__global__ void cast_kernel(const double* s, T* d, std::int64_t n) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    d[k] = static_cast<T>(s[k]);
+  }
+}
+
+__global__ void finite_kernel(const double* v, std::int64_t n, int* bad) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    if (!isfinite(v[k])) atomicOr(bad, 1);
+  }
+}
+
+__global__ void count_nonzero_kernel(const double* v, std::int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    c += v[k] != 0.0 ? 1ull : 0ull;
+  }
+  using BR = cub::BlockReduce<unsigned long long, kT>;
+  __shared__ typename BR::TempStorage tmp;
+  c = BR(tmp).Sum(c);
+  if (threadIdx.x == 0 && c) atomicAdd(out, c);
+}
+
+// ------------------------------------------------------------------ symmetry
+// Row i against the reflected row M-1-i (centro.cpp:46-66): for every stored
+// (i,j,v), d = |v - a(M-1-i, N-1-j)| (0 if absent). Keeps the row maximum
+// and the smallest column reaching it (strict '>' in column-major order).
+__global__ void symmetry_rows_kernel(const int* ptr, const int* col, const double* val,
+                                     std::int64_t m, std::int64_t n, double* rmax, int* rarg) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t mi = m - 1 - i;
+    int q = ptr[mi + 1] - 1;
+    const int qb = ptr[mi];
+    double best = 0.0;
+    int arg = -1;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+      const int j = col[k];
+      while (q >= qb && (n - 1 - col[q]) < j) --q;
+      const double mv = (q >= qb && (n - 1 - col[q]) == j) ? val[q] : 0.0;
+      const double d = fabs(sub(val[k], mv));
+      if (d > best) {
+        best = d;
+        arg = j;
+      }
+    }
+    rmax[i] = best;
+    rarg[i] = arg;
+  }
+}
+
+struct Worst {
+  double d;
+  int j;
+  long long i;
+};
+
+__device__ __forceinline__ bool better(const Worst& a, const Worst& b) {
+  if (a.d != b.d) return a.d > b.d;
+  if (a.j != b.j) return a.j < b.j;
+  return a.i < b.i;
+}
+
+__global__ void symmetry_reduce_kernel(const double* rmax, const int* rarg, std::int64_t m,
+                                       Worst* out) {
+  __shared__ Worst sh[1024];
+  Worst w{0.0, 0x7fffffff, 0x7fffffffffffffffLL};
+  for (std::int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    if (rarg[i] >= 0) {
+      Worst c{rmax[i], rarg[i], i};
+      if (better(c, w)) w = c;
+    }
+  }
+  sh[threadIdx.x] = w;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s && better(sh[threadIdx.x + s], sh[threadIdx.x])) {
+      sh[threadIdx.x] = sh[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ------------------------------------------------------------------ fold
+struct FoldArgs {
+  const int* ptr;
+  const int* col;
+  const double* val;
+  std::int64_t m, n, mh, nh;
+  const int* ptr1;  // fill pass: output row pointers
+  const int* ptr2;
+  int* cnt1;        // count pass outputs
+  int* cnt2;
+  int* col1;
+  double* val1;
+  int* col2;
+  double* val2;
+};
+
+__device__ __forceinline__ int first_at_least(const int* col, int b, int e, std::int64_t v) {
+  while (b < e) {
+    const int mid = b + ((e - b) >> 1);
+    if (col[mid] < v) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+// Output row bi merges the four quadrant streams of buckets (bi, bj):
+// TL = a(bi,bj), BL = a(M-1-bi,bj), TR = a(bi,N-1-bj), BR = a(M-1-bi,N-1-bj)
+// (centro.cpp:109-128 visits them in this column-major triplet order). Each
+// term enters as h = 0.5*v (A1 signs +,-,-,+; A2 all +), summed left to right
+// from the first present term, then exact zeros (either sign) are pruned.
+template <bool FILL>
+__global__ void fold_kernel(FoldArgs a) {
+  for (std::int64_t bi = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; bi < a.mh;
+       bi += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t top = bi, bot = a.m - 1 - bi;
+    int tl = a.ptr[top];
+    const int tl_end = first_at_least(a.col, a.ptr[top], a.ptr[top + 1], a.nh);
+    int tr = a.ptr[top + 1] - 1;
+    int bl = a.ptr[bot];
+    const int bl_end = first_at_least(a.col, a.ptr[bot], a.ptr[bot + 1], a.nh);
+    int br = a.ptr[bot + 1] - 1;
+    int o1 = FILL ? a.ptr1[bi] : 0, o2 = FILL ? a.ptr2[bi] : 0;
+    int n1 = 0, n2 = 0;
+    const std::int64_t nm1 = a.n - 1;
+    for (;;) {
+      std::int64_t bj = a.nh;
+      if (tl < tl_end) bj = min(bj, (std::int64_t)a.col[tl]);
+      if (bl < bl_end) bj = min(bj, (std::int64_t)a.col[bl]);
+      if (tr >= tl_end) bj = min(bj, (std::int64_t)nm1 - a.col[tr]);
+      if (br >= bl_end) bj = min(bj, (std::int64_t)nm1 - a.col[br]);
+      if (bj == a.nh) break;
+      bool have = false;
+      double s1 = 0.0, s2 = 0.0;
+      auto term = [&](double v, bool neg) {
+        const double h = mul(0.5, v);
+        const double t1 = neg ? -h : h;
+        if (!have) {
+          s1 = t1;
+          s2 = h;
+          have = true;
+        } else {
+          s1 = add(s1, t1);
+          s2 = add(s2, h);
+        }
+      };
+      if (tl < tl_end && a.col[tl] == bj) term(a.val[tl++], false);
+      if (bl < bl_end && a.col[bl] == bj) term(a.val[bl++], true);
+      if (tr >= tl_end && nm1 - a.col[tr] == bj) term(a.val[tr--], true);
+      if (br >= bl_end && nm1 - a.col[br] == bj) term(a.val[br--], false);
+      if (s1 != 0.0) {
+        if (FILL) {
+          a.col1[o1] = static_cast<int>(bj);
+          a.val1[o1] = s1;
+          ++o1;
+        }
+        ++n1;
+      }
+      if (s2 != 0.0) {
+        if (FILL) {
+          a.col2[o2] = static_cast<int>(bj);
+          a.val2[o2] = s2;
+          ++o2;
+        }
+        ++n2;
+      }
+    }
+    if (!FILL) {
+      a.cnt1[bi] = n1;
+      a.cnt2[bi] = n2;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ small vectors
+__global__ void split_rhs_kernel(const double* p, double* p1, double* p2, std::int64_t mh) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < mh;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    const double a = p[i], b = p[2 * mh - 1 - i];
+    p1[i] = sub(a, b);
+    p2[i] = add(a, b);
+  }
+}
+
+// f[s*N + j] = (f2+f1)/2, f[s*N + N-1-j] = (f2-f1)/2 with f1/f2 laid out
+// [nh][nrhs] (centro.cpp:170-185).
+__global__ void recombine_kernel(const double* f1, const double* f2, double* f, std::int64_t nh,
+                                 std::int64_t nrhs) {
+  const std::int64_t total = nh * nrhs;
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t j = k / nrhs, s = k % nrhs;
+    const double a = f1[k], b = f2[k];
+    f[s * 2 * nh + j] = mul(0.5, add(b, a));
+    f[s * 2 * nh + 2 * nh - 1 - j] = mul(0.5, sub(b, a));
+  }
+}
+
+__global__ void decompose_kernel(const double* f, double* f1, double* f2, std::int64_t nh) {
+  for (std::int64_t j = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; j < nh;
+       j += (std::int64_t)gridDim.x * blockDim.x) {
+    const double a = f[j], b = f[2 * nh - 1 - j];
+    f1[j] = sub(a, b);
+    f2[j] = add(a, b);
+  }
+}
+
+// Sum of |v| over a compressed outer vector in stored (ascending) order —
+// the reference accumulates row_sums[i] and col_sums[j] in column-major
+// for_each order (solvers.cpp:156-160), i.e. ascending j per row and
+// ascending i per column, starting from 0.0.
+__global__ void abs_sum_kernel(const int* ptr, const double* val, std::int64_t outer, double* out) {
+  for (std::int64_t r = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; r < outer;
+       r += (std::int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) s = add(s, fabs(val[k]));
+    out[r] = s;
+  }
+}
+
+// y[i] (-= p[i]) = sum_k val*x over row i, warp per row (residual / apply).
+__global__ void csr_apply_kernel(const int* ptr, const int* col, const double* val,
+                                 const double* x, const double* p, std::int64_t m, double* y) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nw = ((std::int64_t)gridDim.x * blockDim.x) >> 5;
+  for (std::int64_t i = warp; i < m; i += nw) {
+    double s = 0.0;
+    for (int k = ptr[i] + lane; k < ptr[i + 1]; k += 32) s = add(s, mul(val[k], x[col[k]]));
+    for (int o = 16; o > 0; o >>= 1) s = add(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) y[i] = p ? sub(s, p[i]) : s;
+  }
+}
+
+__global__ void sq_partial_kernel(const double* v, std::int64_t n, double* part) {
+  double s = 0.0;
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    s = add(s, mul(v[k], v[k]));
+  }
+  using BR = cub::BlockReduce<double, kT, cub::BLOCK_REDUCE_RAKING_COMMUTATIVE_ONLY>;
+  __shared__ typename BR::TempStorage tmp;
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_partial_kernel(const double* v, std::int64_t n, double* part) {
+  double s = 0.0;
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    s = add(s, v[k]);
+  }
+  using BR = cub::BlockReduce<double, kT, cub::BLOCK_REDUCE_RAKING_COMMUTATIVE_ONLY>;
+  __shared__ typename BR::TempStorage tmp;
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void max_partial_kernel(const double* v, std::int64_t n, double* part) {
+  double s = -__longlong_as_double(0x7ff0000000000000LL);
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    s = fmax(s, v[k]);
+  }
+  using BR = cub::BlockReduce<double, kT>;
+  __shared__ typename BR::TempStorage tmp;
+  s = BR(tmp).Reduce(s, cub::Max());
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// ------------------------------------------------------------------ phantom
+struct EllipseDev {
+  double x0, y0, a, b, ca, sa, density;
+};
+
+struct RasterArgs {
+  const EllipseDev* e;
+  int count, nx, ny;
+  double vs, center_x, y_bottom, half_w, half_h, y_mid;
+  double* out;
+};
+
+// reference phantom.cpp:34-58 with Ellipse::contains (:8-16); cos/sin of the
+// ellipse angle come from the host libm.
+__global__ void rasterize_kernel(RasterArgs a) {
+  const std::int64_t total = static_cast<std::int64_t>(a.nx) * a.ny;
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(k / a.ny) + 1;  // 1-based column
+    const int r = static_cast<int>(k % a.ny) + 1;  // 1-based row
+    const double x = add(a.center_x, mul(sub(static_cast<double>(c) - 0.5, 0.5 * a.nx), a.vs));
+    const double y = add(a.y_bottom, mul(static_cast<double>(a.ny - r) + 0.5, a.vs));
+    const double u = dvd(sub(x, a.center_x), a.half_w);
+    const double v = dvd(sub(y, a.y_mid), a.half_h);
+    double value = 0.0;
+    for (int q = 0; q < a.count; ++q) {
+      const EllipseDev& e = a.e[q];
+      const double dx = sub(u, e.x0), dy = sub(v, e.y0);
+      const double uu = dvd(add(mul(dx, e.ca), mul(dy, e.sa)), e.a);
+      const double vv = dvd(add(mul(-dx, e.sa), mul(dy, e.ca)), e.b);
+      if (add(mul(uu, uu), mul(vv, vv)) <= 1.0) value = add(value, e.density);
+    }
+    const int base = (c - 1) * a.ny;
+    const int j = (c & 1) ? base + r : base + (a.ny - r + 1);
+    a.out[j - 1] = value;
+  }
+}
+
+// reference phantom.cpp:75-104: two-pointer walk pairing column j with its
+// mirror N-1-j so a centrosymmetric A maps mirror images to mirror data.
+__global__ void forward_project_kernel(const int* ptr, const int* col, const double* val,
+                                       const double* f, std::int64_t m, std::int64_t n,
+                                       double* p) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    const std::int64_t begin = ptr[i], end = ptr[i + 1];
+    double acc = 0.0;
+    std::int64_t l = begin, r = end - 1;
+    while (l <= r && l < end) {
+      const std::int64_t cl = col[l];
+      const std::int64_t crm = n - 1 - col[r];
+      if (l == r) {
+        acc = add(acc, mul(val[l], f[cl]));
+        break;
+      }
+      if (cl < crm) {
+        acc = add(acc, mul(val[l], f[cl]));
+        ++l;
+      } else if (cl > crm) {
+        acc = add(acc, mul(val[r], f[col[r]]));
+        --r;
+      } else {
+        acc = add(acc, add(mul(val[l], f[cl]), mul(val[r], f[col[r]])));
+        ++l;
+        --r;
+      }
+    }
+    p[i] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ host helpers
+template <class T>
+void upload(Context* ctx, T* dst, const T* src, std::size_t n) {
+  if (n) SSB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void exclusive_scan_int_to_i64(Context* ctx, const int* in, std::int64_t* out, std::int64_t n) {
+  std::size_t bytes = 0;
+  SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, static_cast<int>(n + 1),
+                                         ctx->stream));
+  void* t = ctx->temp(bytes);
+  SSB_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, static_cast<int>(n + 1), ctx->stream));
+  ctx->launched(1);
+}
+
+// counts[0..n) -> ptr[0..n] (int, exclusive scan incl. the total)
+void counts_to_ptr(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n) {
+  std::size_t bytes = 0;
+  SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts_np1, ptr, static_cast<int>(n + 1),
+                                         ctx->stream));
+  void* t = ctx->temp(bytes);
+  SSB_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, counts_np1, ptr, static_cast<int>(n + 1),
+                                         ctx->stream));
+  ctx->launched(1);
+}
+
+template <class T>
+T read_scalar(Context* ctx, const T* dev) {
+  T h{};
+  SSB_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  return h;
+}
+
+}  // namespace
+
+// ====================================================================== API
+template <class T>
+void cast_dev(Context* ctx, const double* src, T* dst, std::int64_t n) {
+  if (n <= 0) return;
+  cast_kernel<T><<<grid_for(ctx, n), kT, 0, ctx->stream>>>(src, dst, n);
+  ctx->check_launch("cast_kernel");
+}
+template void cast_dev<float>(Context*, const double*, float*, std::int64_t);
+template void cast_dev<double>(Context*, const double*, double*, std::int64_t);
+
+Matrix* matrix_from_csr_device(Context* ctx, std::int64_t rows, std::int64_t cols,
+                               std::int64_t nnz, DBuf<int>&& rowptr, DBuf<int>&& colidx,
+                               DBuf<double>&& val) {
+  auto* a = new Matrix();
+  a->ctx = ctx;
+  a->rows = rows;
+  a->cols = cols;
+  a->nnz = nnz;
+  a->rowptr = std::move(rowptr);
+  a->colidx = std::move(colidx);
+  a->val = std::move(val);
+  return a;
+}
+
+// Stable-sorted (row<<32|col) keys with values -> CSR; repeats collapse in
+// insertion order. keys/vals are consumed (device, `count` entries).
+Matrix* matrix_from_sorted_triplets(Context* ctx, std::int64_t rows, std::int64_t cols,
+                                    std::int64_t count, unsigned long long* keys, double* vals) {
+  DBuf<int> rowptr(rows + 1);
+  if (count == 0) {
+    SSB_CUDA(cudaMemsetAsync(rowptr.get(), 0, (rows + 1) * sizeof(int), ctx->stream));
+    return matrix_from_csr_device(ctx, rows, cols, 0, std::move(rowptr), DBuf<int>(1),
+                                  DBuf<double>(1));
+  }
+  DBuf<int> head(count + 1);
+  head_flags_kernel<<<grid_for(ctx, count), kT, 0, ctx->stream>>>(keys, count, head.get());
+  ctx->check_launch("head_flags_kernel");
+  SSB_CUDA(cudaMemsetAsync(head.get() + count, 0, sizeof(int), ctx->stream));
+  DBuf<std::int64_t> pos(count + 1);
+  exclusive_scan_int_to_i64(ctx, head.get(), pos.get(), count);
+  const std::int64_t uniq = read_scalar(ctx, pos.get() + count);
+  DBuf<int> col(uniq), row(uniq);
+  DBuf<double> val(uniq);
+  if (uniq == count) {
+    split_keys_kernel<<<grid_for(ctx, count), kT, 0, ctx->stream>>>(keys, count, col.get(),
+                                                                   row.get());
+    ctx->check_launch("split_keys_kernel");
+    SSB_CUDA(cudaMemcpyAsync(val.get(), vals, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  } else {
+    collapse_kernel<<<grid_for(ctx, count), kT, 0, ctx->stream>>>(
+        keys, vals, head.get(), pos.get(), count, col.get(), row.get(), val.get());
+    ctx->check_launch("collapse_kernel");
+  }
+  ptr_from_sorted_kernel<<<grid_for(ctx, uniq + 1), kT, 0, ctx->stream>>>(row.get(), uniq, rows,
+                                                                          rowptr.get());
+  ctx->check_launch("ptr_from_sorted_kernel");
+  return matrix_from_csr_device(ctx, rows, cols, uniq, std::move(rowptr), std::move(col),
+                                std::move(val));
+}
+
+namespace {
+void sort_pairs_u64(Context* ctx, unsigned long long* kin, unsigned long long* kout,
+                    double* vin, double* vout, std::int64_t n, int end_bit) {
+  std::size_t bytes = 0;
+  SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout,
+                                           static_cast<int>(n), 0, end_bit, ctx->stream));
+  void* t = ctx->temp(bytes);
+  SSB_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, static_cast<int>(n), 0,
+                                           end_bit, ctx->stream));
+  ctx->launched(1);
+}
+
+__global__ void make_keys_kernel(const int* r, const int* c, std::int64_t n,
+                                 unsigned long long* keys) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    keys[k] = (static_cast<unsigned long long>(r[k]) << 32) | static_cast<unsigned int>(c[k]);
+  }
+}
+}  // namespace
+
+Matrix* matrix_from_triplets_host(Context* ctx, std::int64_t rows, std::int64_t cols,
+                                  std::int64_t count, const int* r, const int* c,
+                                  const double* v) {
+  if (rows < 0 || cols < 0) fail("matrix shape must be non-negative");
+  for (std::int64_t k = 0; k < count; ++k) {
+    if (r[k] < 0 || r[k] >= rows || c[k] < 0 || c[k] >= cols) fail("triplet index out of range");
+  }
+  DBuf<int> dr(count), dc(count);
+  DBuf<double> dv(count), dv2(count);
+  DBuf<unsigned long long> k1(count), k2(count);
+  upload(ctx, dr.get(), r, count);
+  upload(ctx, dc.get(), c, count);
+  upload(ctx, dv.get(), v, count);
+  Matrix* a = nullptr;
+  if (count > 0) {
+    make_keys_kernel<<<grid_for(ctx, count), kT, 0, ctx->stream>>>(dr.get(), dc.get(), count,
+                                                                  k1.get());
+    ctx->check_launch("make_keys_kernel");
+    sort_pairs_u64(ctx, k1.get(), k2.get(), dv.get(), dv2.get(), count, 32 + bits_for(rows));
+    a = matrix_from_sorted_triplets(ctx, rows, cols, count, k2.get(), dv2.get());
+  } else {
+    a = matrix_from_sorted_triplets(ctx, rows, cols, 0, nullptr, nullptr);
+  }
+  ctx->sync();
+  check_finite(*a);
+  return a;
+}
+
+Matrix* matrix_from_csc_host(Context* ctx, std::int64_t rows, std::int64_t cols,
+                             std::int64_t nnz, const int* outer, const int* inner,
+                             const double* v) {
+  if (rows < 0 || cols < 0 || nnz < 0) fail("matrix shape must be non-negative");
+  if (outer[0] != 0 || outer[cols] != nnz) fail("invalid compressed column pointers");
+  for (std::int64_t j = 0; j < cols; ++j) {
+    if (outer[j + 1] < outer[j]) fail("invalid compressed column pointers");
+    for (int k = outer[j]; k < outer[j + 1]; ++k) {
+      if (inner[k] < 0 || inner[k] >= rows) fail("row index out of range");
+      if (k > outer[j] && inner[k] <= inner[k - 1]) fail("row indices must ascend within a column");
+    }
+  }
+  // Column-major triplets are already in (col,row) order; a stable sort by
+  // row gives the CSR with columns ascending.
+  std::vector<int> r(inner, inner + nnz), c(static_cast<std::size_t>(nnz));
+  for (std::int64_t j = 0; j < cols; ++j) {
+    for (int k = outer[j]; k < outer[j + 1]; ++k) c[k] = static_cast<int>(j);
+  }
+  Matrix* a = matrix_from_triplets_host(ctx, rows, cols, nnz, r.data(), c.data(), v);
+  a->colptr.alloc(cols + 1);
+  a->rowidx.alloc(nnz);
+  a->cval.alloc(nnz);
+  upload(ctx, a->colptr.get(), outer, cols + 1);
+  upload(ctx, a->rowidx.get(), inner, nnz);
+  upload(ctx, a->cval.get(), v, nnz);
+  a->has_csc = true;
+  ctx->sync();
+  return a;
+}
+
+void Matrix::ensure_csc() {
+  if (has_csc) return;
+  Context* c = ctx;
+  colptr.alloc(cols + 1);
+  rowidx.alloc(nnz);
+  cval.alloc(nnz);
+  if (nnz == 0) {
+    SSB_CUDA(cudaMemsetAsync(colptr.get(), 0, (cols + 1) * sizeof(int), c->stream));
+    has_csc = true;
+    return;
+  }
+  DBuf<int> rowof(nnz), keys_in(nnz), keys_out(nnz), perm_in(nnz), perm_out(nnz);
+  expand_ptr_kernel<<<grid_for(c, rows), kT, 0, c->stream>>>(rowptr.get(), rows, rowof.get());
+  c->check_launch("expand_ptr_kernel");
+  SSB_CUDA(cudaMemcpyAsync(keys_in.get(), colidx.get(), nnz * sizeof(int),
+                           cudaMemcpyDeviceToDevice, c->stream));
+  iota_kernel<<<grid_for(c, nnz), kT, 0, c->stream>>>(perm_in.get(), nnz);
+  c->check_launch("iota_kernel");
+  // Stable radix sort by column: CSR order has rows ascending, so rows stay
+  // ascending inside every column (Eigen's compressed CSC invariant).
+  std::size_t bytes = 0;
+  const int eb = bits_for(std::max<std::int64_t>(cols, 2));
+  SSB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in.get(), keys_out.get(),
+                                           perm_in.get(), perm_out.get(), static_cast<int>(nnz), 0,
+                                           eb, c->stream));
+  void* t = c->temp(bytes);
+  SSB_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, keys_in.get(), keys_out.get(), perm_in.get(),
+                                           perm_out.get(), static_cast<int>(nnz), 0, eb,
+                                           c->stream));
+  c->launched(1);
+  gather_kernel<<<grid_for(c, nnz), kT, 0, c->stream>>>(perm_out.get(), rowof.get(), val.get(),
+                                                        nnz, rowidx.get(), cval.get());
+  c->check_launch("gather_kernel");
+  ptr_from_sorted_kernel<<<grid_for(c, nnz + 1), kT, 0, c->stream>>>(keys_out.get(), nnz, cols,
+                                                                    colptr.get());
+  c->check_launch("ptr_from_sorted_kernel");
+  c->sync();
+  has_csc = true;
+}
+
+void Matrix::ensure_f32() {
+  if (has_f32) return;
+  ensure_csc();
+  val32.alloc(nnz);
+  cval32.alloc(nnz);
+  cast_dev<float>(ctx, val.get(), val32.get(), nnz);
+  cast_dev<float>(ctx, cval.get(), cval32.get(), nnz);
+  ctx->sync();
+  has_f32 = true;
+}
+
+void check_finite(Matrix& a) {
+  Context* ctx = a.ctx;
+  if (a.nnz == 0) return;
+  DBuf<int> bad(1);
+  SSB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx->stream));
+  finite_kernel<<<grid_for(ctx, a.nnz), kT, 0, ctx->stream>>>(a.val.get(), a.nnz, bad.get());
+  ctx->check_launch("finite_kernel");
+  if (read_scalar(ctx, bad.get())) fail("matrix contains non-finite values");
+}
+
+std::int64_t nonzeros(Matrix& a) {
+  Context* ctx = a.ctx;
+  if (a.nnz == 0) return 0;
+  DBuf<unsigned long long> out(1);
+  SSB_CUDA(cudaMemsetAsync(out.get(), 0, sizeof(unsigned long long), ctx->stream));
+  count_nonzero_kernel<<<grid_for(ctx, a.nnz), kT, 0, ctx->stream>>>(a.val.get(), a.nnz,
+                                                                    out.get());
+  ctx->check_launch("count_nonzero_kernel");
+  return static_cast<std::int64_t>(read_scalar(ctx, out.get()));
+}
+
+// GPU build_system (geometry.cpp:227-275): count -> scan -> fill of the
+// traced half, stable (row,col) radix sort (repeats collapse in traversal
+// order, as setFromTriplets would sum them), then the mirror half.
+Matrix* build_system(Context* ctx, const ss_scan_config& cfg) {
+  const Grid g = make_grid(cfg);
+  const RayTable rt = enumerate_rays(cfg, g, false);
+  const std::int64_t mh = rt.m / 2, m = rt.m, n = g.cell_count();
+  std::vector<double> xb(g.n_x + 1), yb(g.n_y + 1);
+  for (int k = 0; k <= g.n_x; ++k) xb[k] = g.center_x + (k - g.n_x / 2) * g.voxel_size;
+  for (int k = 0; k <= g.n_y; ++k) yb[k] = g.y_bottom + k * g.voxel_size;
+
+  DBuf<double> d_rays(7 * mh), d_xb(xb.size()), d_yb(yb.size());
+  const std::vector<double>* cols7[7] = {&rt.sx, &rt.sy, &rt.dx, &rt.dy,
+                                         &rt.seg_len, &rt.t_in, &rt.t_out};
+  for (int q = 0; q < 7; ++q) upload(ctx, d_rays.get() + q * mh, cols7[q]->data(), mh);
+  upload(ctx, d_xb.get(), xb.data(), xb.size());
+  upload(ctx, d_yb.get(), yb.data(), yb.size());
+  TraceArgs ta{d_rays.get(),          d_rays.get() + mh,     d_rays.get() + 2 * mh,
+               d_rays.get() + 3 * mh, d_rays.get() + 4 * mh, d_rays.get() + 5 * mh,
+               d_rays.get() + 6 * mh, d_xb.get(),            d_yb.get(),
+               g.n_x,                 g.n_y,                 g.voxel_size,
+               g.x_left(),            g.y_bottom,            mh};
+  DBuf<int> counts(mh + 1);
+  SSB_CUDA(cudaMemsetAsync(counts.get() + mh, 0, sizeof(int), ctx->stream));
+  trace_count_kernel<<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(ta, counts.get());
+  ctx->check_launch("trace_count_kernel");
+  DBuf<std::int64_t> offs(mh + 1);
+  exclusive_scan_int_to_i64(ctx, counts.get(), offs.get(), mh);
+  const std::int64_t half = read_scalar(ctx, offs.get() + mh);
+  if (2 * half >= (std::int64_t{1} << 31)) fail("build_system: nnz exceeds int32 storage");
+  Matrix* a = nullptr;
+  {
+    DBuf<unsigned long long> k1(half), k2(half);
+    DBuf<double> v1(half), v2(half);
+    trace_fill_kernel<<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(ta, offs.get(), k1.get(),
+                                                                      v1.get());
+    ctx->check_launch("trace_fill_kernel");
+    sort_pairs_u64(ctx, k1.get(), k2.get(), v1.get(), v2.get(), half, 32 + bits_for(mh));
+    a = matrix_from_sorted_triplets(ctx, mh, n, half, k2.get(), v2.get());
+  }
+  // Grow the traced-half CSR into the full M x N matrix.
+  const std::int64_t h = a->nnz;
+  DBuf<int> ptr(m + 1), col(2 * h);
+  DBuf<double> val(2 * h);
+  SSB_CUDA(cudaMemcpyAsync(ptr.get(), a->rowptr.get(), (mh + 1) * sizeof(int),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(col.get(), a->colidx.get(), h * sizeof(int), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(val.get(), a->val.get(), h * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  mirror_ptr_kernel<<<grid_for(ctx, mh), kT, 0, ctx->stream>>>(ptr.get(), mh, h);
+  ctx->check_launch("mirror_ptr_kernel");
+  mirror_fill_kernel<<<grid_for(ctx, h), kT, 0, ctx->stream>>>(col.get(), val.get(), h, n);
+  ctx->check_launch("mirror_fill_kernel");
+  ctx->sync();
+  delete a;
+  return matrix_from_csr_device(ctx, m, n, 2 * h, std::move(ptr), std::move(col), std::move(val));
+}
+
+ss_symmetry_report verify_symmetry(Matrix& a, double tol) {
+  if (tol < 0) fail("verify_symmetry: tol must be non-negative");
+  Context* ctx = a.ctx;
+  ss_symmetry_report rep{};
+  rep.status = a.rows % 2 != 0 ? 1 : (a.cols % 2 != 0 ? 2 : 0);
+  rep.max_violation = 0.0;
+  rep.worst_row = 1;
+  rep.worst_col = 1;
+  if (a.rows > 0 && a.nnz > 0) {
+    DBuf<double> rmax(a.rows);
+    DBuf<int> rarg(a.rows);
+    DBuf<Worst> w(1);
+    symmetry_rows_kernel<<<grid_for(ctx, a.rows), kT, 0, ctx->stream>>>(
+        a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, rmax.get(), rarg.get());
+    ctx->check_launch("symmetry_rows_kernel");
+    symmetry_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(rmax.get(), rarg.get(), a.rows, w.get());
+    ctx->check_launch("symmetry_reduce_kernel");
+    const Worst hw = read_scalar(ctx, w.get());
+    if (hw.j != 0x7fffffff && hw.d > 0.0) {
+      rep.max_violation = hw.d;
+      rep.worst_row = hw.i + 1;
+      rep.worst_col = hw.j + 1;
+    }
+  }
+  rep.holds = (rep.status == 0 && rep.max_violation <= tol) ? 1 : 0;
+  return rep;
+}
+
+void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
+  if (a.rows % 2 != 0 || a.cols % 2 != 0) fail("split_matrix: dimensions must be even");
+  Context* ctx = a.ctx;
+  const std::int64_t mh = a.rows / 2, nh = a.cols / 2;
+  DBuf<int> c1(mh + 1), c2(mh + 1);
+  SSB_CUDA(cudaMemsetAsync(c1.get() + mh, 0, sizeof(int), ctx->stream));
+  SSB_CUDA(cudaMemsetAsync(c2.get() + mh, 0, sizeof(int), ctx->stream));
+  FoldArgs fa{a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, mh, nh,
+              nullptr, nullptr, c1.get(), c2.get(), nullptr, nullptr, nullptr, nullptr};
+  if (mh > 0) {
+    fold_kernel<false><<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(fa);
+    ctx->check_launch("fold_kernel<count>");
+  }
+  DBuf<int> p1(mh + 1), p2(mh + 1);
+  counts_to_ptr(ctx, c1.get(), p1.get(), mh);
+  counts_to_ptr(ctx, c2.get(), p2.get(), mh);
+  const int n1 = read_scalar(ctx, p1.get() + mh);
+  const int n2 = read_scalar(ctx, p2.get() + mh);
+  DBuf<int> col1(n1), col2(n2);
+  DBuf<double> val1(n1), val2(n2);
+  fa.ptr1 = p1.get();
+  fa.ptr2 = p2.get();
+  fa.col1 = col1.get();
+  fa.val1 = val1.get();
+  fa.col2 = col2.get();
+  fa.val2 = val2.get();
+  if (mh > 0) {
+    fold_kernel<true><<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(fa);
+    ctx->check_launch("fold_kernel<fill>");
+  }
+  ctx->sync();
+  a1 = matrix_from_csr_device(ctx, mh, nh, n1, std::move(p1), std::move(col1), std::move(val1));
+  a2 = matrix_from_csr_device(ctx, mh, nh, n2, std::move(p2), std::move(col2), std::move(val2));
+}
+
+void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh) {
+  if (mh <= 0) return;
+  split_rhs_kernel<<<grid_for(ctx, mh), kT, 0, ctx->stream>>>(p, p1, p2, mh);
+  ctx->check_launch("split_rhs_kernel");
+}
+
+void recombine_dev(Context* ctx, const double* f1, const double* f2, double* f, std::int64_t nh,
+                   std::int64_t nrhs) {
+  if (nh * nrhs <= 0) return;
+  recombine_kernel<<<grid_for(ctx, nh * nrhs), kT, 0, ctx->stream>>>(f1, f2, f, nh, nrhs);
+  ctx->check_launch("recombine_kernel");
+}
+
+void decompose_dev(Context* ctx, const double* f, double* f1, double* f2, std::int64_t nh) {
+  if (nh <= 0) return;
+  decompose_kernel<<<grid_for(ctx, nh), kT, 0, ctx->stream>>>(f, f1, f2, nh);
+  ctx->check_launch("decompose_kernel");
+}
+
+void abs_sums(Matrix& a, double* row_sums, double* col_sums) {
+  Context* ctx = a.ctx;
+  a.ensure_csc();
+  if (a.rows > 0) {
+    abs_sum_kernel<<<grid_for(ctx, a.rows), kT, 0, ctx->stream>>>(a.rowptr.get(), a.val.get(),
+                                                                 a.rows, row_sums);
+    ctx->check_launch("abs_sum_kernel<rows>");
+  }
+  if (a.cols > 0) {
+    abs_sum_kernel<<<grid_for(ctx, a.cols), kT, 0, ctx->stream>>>(a.colptr.get(), a.cval.get(),
+                                                                 a.cols, col_sums);
+    ctx->check_launch("abs_sum_kernel<cols>");
+  }
+}
+
+void apply_dev(Matrix& a, const double* x, double* y) {
+  if (a.rows <= 0) return;
+  csr_apply_kernel<<<grid_for(a.ctx, a.rows * 32), kT, 0, a.ctx->stream>>>(
+      a.rowptr.get(), a.colidx.get(), a.val.get(), x, nullptr, a.rows, y);
+  a.ctx->check_launch("csr_apply_kernel");
+}
+
+void apply_transpose_dev(Matrix& a, const double* y, double* x) {
+  a.ensure_csc();
+  if (a.cols <= 0) return;
+  csr_apply_kernel<<<grid_for(a.ctx, a.cols * 32), kT, 0, a.ctx->stream>>>(
+      a.colptr.get(), a.rowidx.get(), a.cval.get(), y, nullptr, a.cols, x);
+  a.ctx->check_launch("csr_apply_kernel<T>");
+}
+
+void residual_dev(Matrix& a, const double* x, const double* p, double* r) {
+  if (a.rows <= 0) return;
+  csr_apply_kernel<<<grid_for(a.ctx, a.rows * 32), kT, 0, a.ctx->stream>>>(
+      a.rowptr.get(), a.colidx.get(), a.val.get(), x, p, a.rows, r);
+  a.ctx->check_launch("csr_apply_kernel<res>");
+}
+
+double norm2_dev(Context* ctx, const double* v, std::int64_t n) {
+  if (n <= 0) return 0.0;
+  const int blocks = 256;
+  DBuf<double> part(blocks), out(1);
+  sq_partial_kernel<<<blocks, kT, 0, ctx->stream>>>(v, n, part.get());
+  ctx->check_launch("sq_partial_kernel");
+  sum_partial_kernel<<<1, kT, 0, ctx->stream>>>(part.get(), blocks, out.get());
+  ctx->check_launch("sum_partial_kernel");
+  return read_scalar(ctx, out.get());
+}
+
+double max_dev(Context* ctx, const double* v, std::int64_t n) {
+  if (n <= 0) return 0.0;
+  const int blocks = 256;
+  DBuf<double> part(blocks), out(1);
+  max_partial_kernel<<<blocks, kT, 0, ctx->stream>>>(v, n, part.get());
+  ctx->check_launch("max_partial_kernel");
+  max_partial_kernel<<<1, kT, 0, ctx->stream>>>(part.get(), blocks, out.get());
+  ctx->check_launch("max_partial_kernel<final>");
+  return read_scalar(ctx, out.get());
+}
+
+bool all_finite_dev(Context* ctx, const double* v, std::int64_t n) {
+  if (n <= 0) return true;
+  DBuf<int> bad(1);
+  SSB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx->stream));
+  finite_kernel<<<grid_for(ctx, n), kT, 0, ctx->stream>>>(v, n, bad.get());
+  ctx->check_launch("finite_kernel");
+  return read_scalar(ctx, bad.get()) == 0;
+}
+
+void rasterize_dev(Context* ctx, const double* ell6, int count, const Grid& g, double* out) {
+  g.validate();
+  std::vector<EllipseDev> es(static_cast<std::size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const double* e = ell6 + 6 * q;
+    es[q] = EllipseDev{e[0], e[1], e[2], e[3], std::cos(e[4]), std::sin(e[4]), e[5]};
+  }
+  DBuf<EllipseDev> d(es.size());
+  upload(ctx, d.get(), es.data(), es.size());
+  const double half_w = 0.5 * g.width(), half_h = 0.5 * g.height();
+  RasterArgs ra{d.get(), count, g.n_x, g.n_y, g.voxel_size, g.center_x, g.y_bottom,
+                half_w, half_h, g.y_bottom + half_h, out};
+  const std::int64_t total = static_cast<std::int64_t>(g.n_x) * g.n_y;
+  rasterize_kernel<<<grid_for(ctx, total), kT, 0, ctx->stream>>>(ra);
+  ctx->check_launch("rasterize_kernel");
+  ctx->sync();
+}
+
+void forward_project_dev(Matrix& a, const double* f, double* p) {
+  if (a.rows <= 0) return;
+  forward_project_kernel<<<grid_for(a.ctx, a.rows), kT, 0, a.ctx->stream>>>(
+      a.rowptr.get(), a.colidx.get(), a.val.get(), f, a.rows, a.cols, p);
+  a.ctx->check_launch("forward_project_kernel");
+}
+
+}  // namespace ssb

@@ -1,0 +1,62 @@
+// SART plan: the device-resident iteration loop of reference sart_solve
+// (proj/src/solvers.cpp:148-199) over one system or the folded pair.
+#pragma once
+
+#include "internal.hpp"
+
+namespace ssb {
+
+struct Plan {
+  Context* ctx = nullptr;
+  int nsys = 1;
+  int nrhs = 1;
+  int dtype = SS_F64;
+  int vs_fwd = 32, vs_back = 8;
+  int fwd_blocks = 0, back_blocks = 0;
+  bool sharded = false;
+  std::int64_t row_begin = 0, row_end = 0;  // sharded: rows kept by this rank
+  ss_solve_options opts{};
+  Matrix* a[2] = {nullptr, nullptr};
+  // Row-sharded plans own a row-block copy of the (single) system.
+  Matrix* own = nullptr;
+  std::int64_t rows[2] = {0, 0}, cols[2] = {0, 0};
+  // per system, plan dtype (T) buffers in bytes
+  DBuf<char> x[2], w[2], p[2], rinv[2], cinv[2];
+  DBuf<double> partial;   // [nsys*nrhs][fwd_blocks]
+  DBuf<double> pnorm;     // [nsys*nrhs]
+  DBuf<double> history;   // [nsys*nrhs][max_iters+1]
+  DBuf<int> state;        // [nsys*nrhs][4] stopped, stop_it, diverged_at, -
+  DBuf<unsigned> ticket;  // last-block ticket of the forward kernel
+  DBuf<char> bp;          // sharded: back-projection + ||r||^2 slot (all-reduced)
+  cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.0f;
+  bool launched = false;
+  bool empty_rows[2] = {false, false};  // all row sums zero (reference throws)
+
+  ~Plan();
+  std::size_t tsize() const { return dtype == SS_F32 ? 4 : 8; }
+  void build_graph();
+  void enqueue_iterations(int first, int count);  // raw launches (no graph)
+  void enqueue_reset();
+  void set_rhs_host(int which, const double* p_slice_major);
+  void set_rhs_device(int which, const void* p_dev);
+  void set_rhs_device_f64(int which, const double* p_dev);  // [rows] fp64, nrhs == 1
+  void finish_rhs(int which);  // ||p|| (all-reduced for sharded plans)
+  int diverged_at(int which) const;
+  void recombine_device(double* f_dev);  // N = 2*cols fp64, nrhs == 1
+  void launch();
+  void finish(ss_solve_report* rep);
+  void get_solution(int which, double* f_slice_major);
+  void get_history(int which, int slice, double* h, int* len);
+  void recombine(double* f_slice_major);
+  void profile(int iters, float* fwd_ms, float* back_ms);
+  void stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const;
+};
+
+Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs);
+Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t row_begin, std::int64_t row_end,
+                        const ss_solve_options& o);
+void partition_rows(const int* rowptr, std::int64_t rows, int parts, std::int64_t* bounds);
+
+}  // namespace ssb

@@ -1,0 +1,38 @@
+"""Multi-GPU layouts of the folded-SART path, one process per GPU.
+
+world == 2: rank r solves folded system r; no data-path collective.
+world >= 4 (even): ranks [0, W/2) hold A1, ranks [W/2, W) hold A2; each
+group splits its system into nnz-balanced row blocks and all-reduces the
+N/2-length back-projection (+ the ||r||^2 slot) once per iteration over NCCL
+inside the C++ library. torch.distributed only carries the rendezvous (the
+128-byte NCCL unique id, over a gloo group) and the barrier.
+"""
+from __future__ import annotations
+
+
+def group_layout(rank: int, world: int):
+    """(system index, rank inside the group, group size, group ranks)."""
+    if world < 4 or world % 2:
+        raise ValueError("row sharding needs an even world size >= 4")
+    half = world // 2
+    sysid = rank // half
+    return sysid, rank % half, half, list(range(sysid * half, (sysid + 1) * half))
+
+
+def make_sharded_plan(P, ctx, split, opts, rank: int, world: int):
+    import torch.distributed as tdist
+
+    sysid, grank, half, members = group_layout(rank, world)
+    groups = [tdist.new_group(list(range(0, half)), backend="gloo"),
+              tdist.new_group(list(range(half, world)), backend="gloo")]
+    obj = [P.symsplit.nccl_unique_id() if grank == 0 else None]
+    tdist.broadcast_object_list(obj, src=members[0], group=groups[sysid])
+    P.symsplit.attach_nccl(ctx, obj[0], half, grank)
+    a = split.a1 if sysid == 0 else split.a2
+    p = split.p1 if sysid == 0 else split.p2
+    ptr = a.to_csr()[0]
+    bounds = P.symsplit.partition_rows(ptr, half)
+    rb, re = int(bounds[grank]), int(bounds[grank + 1])
+    plan = P.symsplit.ShardedSartPlan(ctx, a, rb, re, opts)
+    plan.set_rhs(0, p[rb:re])
+    return plan

@@ -1,0 +1,627 @@
+"""Python mirror of the reference `symsplit` API for the folded-SART path.
+
+Same names, argument meaning and error behaviour as the reference C++/pybind11
+surface (proj/include/symsplit/*.hpp, proj/python/bindings.cpp), backed by the
+sm_100a library through its C ABI (include/symsplit_b200.h). Matrices live on
+the GPU; vectors cross the boundary as numpy float64 arrays.
+
+Differences from the reference, all deliberate:
+  * only Method.sart exists here (dense min-norm / CGLS are out of scope);
+  * Matrix storage is always sparse on the device — `Matrix.dense(d)` stores
+    the nonzero entries, so its fold follows the sparse (4-term) semantics
+    (centro.cpp:109-130); for exactly centrosymmetric inputs both agree;
+  * SolveOptions.dtype selects fp64 (reference) or fp32 device arithmetic.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+
+kPi = 3.14159265358979323846
+
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """symsplit::Error (matrix.hpp:22-25); pybind name SymsplitError."""
+
+
+SymsplitError = Error
+
+
+class SymmetryError(Error):
+    """symsplit::SymmetryError carrying its SymmetryReport (centro.hpp:73-78)."""
+
+    def __init__(self, what, report):
+        super().__init__(what)
+        self.report = report
+
+
+class DeviceError(Error):
+    """CUDA / NCCL / out-of-memory failure inside the library."""
+
+
+def _lib():
+    return N.load()
+
+
+def _check(rc, report=None):
+    if rc == N.SS_OK:
+        return
+    msg = _lib().ss_last_error().decode()
+    if rc == N.SS_ERR_SYMMETRY:
+        raise SymmetryError(msg, report)
+    if rc in (N.SS_ERR_CUDA, N.SS_ERR_NCCL, N.SS_ERR_OOM):
+        raise DeviceError(msg)
+    raise Error(msg)
+
+
+def _f64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def _i32(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+def _dp(a):
+    return a.ctypes.data_as(N.dp)
+
+
+def _ip(a):
+    return a.ctypes.data_as(N.i32p)
+
+
+def degrees_to_radians(deg):
+    return deg * kPi / 180.0
+
+
+# ----------------------------------------------------------------- context
+class Context:
+    """One CUDA stream + workspace on one device (ss_ctx_t)."""
+
+    def __init__(self, device: int = 0):
+        h = N.vp()
+        _check(_lib().ss_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().ss_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(_lib().ss_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return _lib().ss_ctx_stream(self.h) or 0
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib().ss_ctx_launch_count(self.h))
+
+
+_ctx_lock = threading.Lock()
+_contexts: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    with _ctx_lock:
+        if device not in _contexts:
+            _contexts[device] = Context(device)
+        return _contexts[device]
+
+
+# ----------------------------------------------------------------- matrix
+class Matrix:
+    """Device sparse matrix (reference Matrix, matrix.hpp:34-87)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and N._lib is not None:
+                N._lib.ss_matrix_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # -- construction
+    @classmethod
+    def from_csc(cls, rows, cols, outer, inner, values, ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        outer, inner, values = _i32(outer), _i32(inner), _f64(values)
+        h = N.vp()
+        _check(_lib().ss_matrix_from_csc(ctx.h, rows, cols, len(values), _ip(outer), _ip(inner),
+                                         _dp(values), C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_triplets(cls, rows, cols, row, col, values, ctx: Optional[Context] = None):
+        """Matrix::from_triplets (matrix.cpp:12-18): repeats summed in order."""
+        ctx = ctx or default_context()
+        row, col, values = _i32(row), _i32(col), _f64(values)
+        h = N.vp()
+        _check(_lib().ss_matrix_from_triplets(ctx.h, rows, cols, len(values), _ip(row), _ip(col),
+                                              _dp(values), C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def dense(cls, d, ctx: Optional[Context] = None):
+        d = np.asarray(d, dtype=np.float64)
+        if not np.all(np.isfinite(d)):
+            raise Error("matrix contains non-finite values")
+        cols_, rows_ = np.nonzero(d.T)  # column-major order of the nonzeros
+        return cls.from_triplets(d.shape[0], d.shape[1], rows_, cols_, d[rows_, cols_], ctx)
+
+    # -- queries
+    @property
+    def shape(self):
+        r, c, s = N.i64(), N.i64(), N.i64()
+        _check(_lib().ss_matrix_shape(self.h, C.byref(r), C.byref(c), C.byref(s)))
+        return r.value, c.value
+
+    def rows(self):
+        return self.shape[0]
+
+    def cols(self):
+        return self.shape[1]
+
+    @property
+    def stored(self) -> int:
+        r, c, s = N.i64(), N.i64(), N.i64()
+        _check(_lib().ss_matrix_shape(self.h, C.byref(r), C.byref(c), C.byref(s)))
+        return s.value
+
+    def is_sparse(self):
+        return True
+
+    def nonzeros(self) -> int:
+        out = N.i64()
+        _check(_lib().ss_matrix_nonzeros(self.h, C.byref(out)))
+        return out.value
+
+    def fill_ratio(self) -> float:
+        out = C.c_double()
+        _check(_lib().ss_matrix_fill_ratio(self.h, C.byref(out)))
+        return out.value
+
+    def to_csr(self):
+        rows, cols = self.shape
+        nnz = self.stored
+        ptr = np.empty(rows + 1, np.int32)
+        idx = np.empty(nnz, np.int32)
+        val = np.empty(nnz, np.float64)
+        _check(_lib().ss_matrix_download_csr(self.h, _ip(ptr), _ip(idx), _dp(val)))
+        return ptr, idx, val
+
+    def to_csc(self):
+        rows, cols = self.shape
+        nnz = self.stored
+        outer = np.empty(cols + 1, np.int32)
+        inner = np.empty(nnz, np.int32)
+        val = np.empty(nnz, np.float64)
+        _check(_lib().ss_matrix_download_csc(self.h, _ip(outer), _ip(inner), _dp(val)))
+        return outer, inner, val
+
+    def to_dense(self):
+        rows, cols = self.shape
+        ptr, idx, val = self.to_csr()
+        d = np.zeros((rows, cols))
+        for i in range(rows):
+            d[i, idx[ptr[i]:ptr[i + 1]]] = val[ptr[i]:ptr[i + 1]]
+        return d
+
+    def coeff(self, i, j):
+        ptr, idx, val = self.to_csr()
+        seg = idx[ptr[i]:ptr[i + 1]]
+        k = np.searchsorted(seg, j)
+        return float(val[ptr[i] + k]) if k < len(seg) and seg[k] == j else 0.0
+
+    def apply(self, x):
+        x = _f64(x)
+        rows, cols = self.shape
+        if x.shape != (cols,):
+            raise Error("matrix-vector size mismatch")
+        y = np.empty(rows)
+        _check(_lib().ss_matrix_apply(self.h, _dp(x), _dp(y)))
+        return y
+
+    def apply_transpose(self, y):
+        y = _f64(y)
+        rows, cols = self.shape
+        if y.shape != (rows,):
+            raise Error("matrix-vector size mismatch")
+        x = np.empty(cols)
+        _check(_lib().ss_matrix_apply_transpose(self.h, _dp(y), _dp(x)))
+        return x
+
+
+# ----------------------------------------------------------------- value types
+@dataclass
+class SymmetryReport:
+    holds: bool = False
+    max_violation: float = 0.0
+    worst_row: int = 1
+    worst_col: int = 1
+    status: int = 0  # 0 ok, 1 odd_row_count, 2 odd_col_count
+
+    @classmethod
+    def _from(cls, r: N.SymmetryReportC):
+        return cls(bool(r.holds), r.max_violation, r.worst_row, r.worst_col, r.status)
+
+
+@dataclass
+class CentroSystem:
+    a: Matrix
+    p: np.ndarray
+    symmetry_tol: float = 1e-12
+
+
+@dataclass
+class SplitSystem:
+    a1: Matrix
+    p1: np.ndarray
+    a2: Matrix
+    p2: np.ndarray
+    parent_fill: float = 0.0
+    fill1: float = 0.0
+    fill2: float = 0.0
+
+
+@dataclass
+class SolutionPair:
+    f1: np.ndarray
+    f2: np.ndarray
+
+
+@dataclass
+class SolveOptions:
+    """reference SolveOptions (solvers.hpp:19-27); method is SART."""
+    max_iters: int = 200
+    tol: float = 1e-10
+    relaxation: float = 1.0
+    parallelism: int = 0
+    dtype: str = "f64"  # "f64" (reference arithmetic) or "f32"
+    method: str = "sart"
+
+    def _c(self):
+        if self.method != "sart":
+            raise Error(f"unknown method name: {self.method}" if self.method not in
+                        ("dense", "dense_minnorm", "cgls") else
+                        f"method {self.method} is not on the B200 path")
+        if self.dtype not in ("f64", "f32"):
+            raise Error("dtype must be 'f64' or 'f32'")
+        return N.SolveOptionsC(int(self.max_iters), float(self.tol), float(self.relaxation),
+                               int(self.parallelism), N.SS_F64 if self.dtype == "f64" else N.SS_F32)
+
+
+@dataclass
+class SolveReport:
+    f: np.ndarray
+    residual_norm: float = 0.0
+    solution_norm: float = 0.0
+    iterations: int = 0
+    wall_time_seconds: float = 0.0
+    method: str = "sart"
+    mode: str = "direct"
+    residual_history: list = field(default_factory=list)
+    split_seconds: float = 0.0
+    recombine_seconds: float = 0.0
+    branch1_seconds: float = 0.0
+    branch2_seconds: float = 0.0
+
+
+def _report(f, r: N.SolveReportC, mode, hist=()):
+    return SolveReport(f=f, residual_norm=r.residual_norm, solution_norm=r.solution_norm,
+                       iterations=r.iterations, wall_time_seconds=r.wall_time_seconds,
+                       mode=mode, residual_history=list(hist), split_seconds=r.split_seconds,
+                       recombine_seconds=r.recombine_seconds, branch1_seconds=r.branch1_seconds,
+                       branch2_seconds=r.branch2_seconds)
+
+
+# ----------------------------------------------------------------- centro
+def verify_symmetry(a: Matrix, tol: float) -> SymmetryReport:
+    """centro.cpp:46-66"""
+    r = N.SymmetryReportC()
+    _check(_lib().ss_verify_symmetry(a.h, C.c_double(tol), C.byref(r)))
+    return SymmetryReport._from(r)
+
+
+def split_rhs(p, ctx: Optional[Context] = None):
+    """centro.cpp:89-99"""
+    ctx = ctx or default_context()
+    p = _f64(p)
+    p1 = np.empty(len(p) // 2)
+    p2 = np.empty(len(p) // 2)
+    _check(_lib().ss_split_rhs(ctx.h, _dp(p), len(p), _dp(p1), _dp(p2)))
+    return p1, p2
+
+
+def split_system(sys: CentroSystem) -> SplitSystem:
+    """centro.cpp:144-156 (sparse fold :109-130), bit-exact on the device."""
+    a = sys.a
+    p = _f64(sys.p)
+    m = len(p)
+    a1, a2 = N.vp(), N.vp()
+    p1 = np.empty(m // 2)
+    p2 = np.empty(m // 2)
+    fills = np.empty(3)
+    rep = N.SymmetryReportC()
+    rc = _lib().ss_split_system(a.h, _dp(p), m, C.c_double(sys.symmetry_tol), C.byref(a1),
+                                C.byref(a2), _dp(p1), _dp(p2), _dp(fills), C.byref(rep))
+    _check(rc, SymmetryReport._from(rep))
+    return SplitSystem(Matrix(a1, a.ctx), p1, Matrix(a2, a.ctx), p2, *fills)
+
+
+def decompose_solution(f, ctx: Optional[Context] = None) -> SolutionPair:
+    ctx = ctx or default_context()
+    f = _f64(f)
+    f1 = np.empty(len(f) // 2)
+    f2 = np.empty(len(f) // 2)
+    _check(_lib().ss_decompose_solution(ctx.h, _dp(f), len(f), _dp(f1), _dp(f2)))
+    return SolutionPair(f1, f2)
+
+
+def recombine_solution(pair, f2=None, ctx: Optional[Context] = None):
+    """centro.cpp:170-185; accepts a SolutionPair or (f1, f2)."""
+    ctx = ctx or default_context()
+    f1 = pair.f1 if isinstance(pair, SolutionPair) else pair
+    f2 = pair.f2 if isinstance(pair, SolutionPair) else f2
+    f1, f2 = _f64(f1), _f64(f2)
+    if len(f1) != len(f2):
+        raise Error("recombine_solution: component lengths differ")
+    f = np.empty(2 * len(f1))
+    _check(_lib().ss_recombine_solution(ctx.h, _dp(f1), _dp(f2), len(f1), _dp(f)))
+    return f
+
+
+# ----------------------------------------------------------------- solvers
+def sart_solve(a: Matrix, p, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """solvers.cpp:148-199"""
+    opts = opts or SolveOptions()
+    p = _f64(p)
+    rows, cols = a.shape
+    f = np.empty(cols)
+    hist = np.empty(int(opts.max_iters) + 1)
+    r = N.SolveReportC()
+    o = opts._c()
+    _check(_lib().ss_sart_solve(a.h, _dp(p), len(p), C.byref(o), _dp(f), cols, C.byref(r),
+                                _dp(hist)))
+    return _report(f, r, "direct", hist[:r.history_len])
+
+
+def solve_direct(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """solvers.cpp:201-205 (method = sart)"""
+    return sart_solve(sys.a, sys.p, opts)
+
+
+def solve_split(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """solvers.cpp:207-269 (method = sart): fold, both branches, recombine."""
+    opts = opts or SolveOptions()
+    p = _f64(sys.p)
+    rows, cols = sys.a.shape
+    f = np.empty(cols)
+    r = N.SolveReportC()
+    o = opts._c()
+    _check(_lib().ss_solve_split(sys.a.h, _dp(p), len(p), C.c_double(sys.symmetry_tol),
+                                 C.byref(o), _dp(f), cols, C.byref(r)))
+    return _report(f, r, "split")
+
+
+# ----------------------------------------------------------------- geometry
+def scan_config(k=24, gamma=None, gamma_deg=30.0, h_e=1.0, h_m=0.25, l_m=0.43, n_p=1024,
+                a_e=7e-4, obj_size=0.1, grid_nx=32, grid_ny=32) -> N.ScanConfig:
+    g = degrees_to_radians(gamma_deg) if gamma is None else gamma
+    return N.ScanConfig(k, g, h_e, h_m, l_m, n_p, a_e, obj_size, grid_nx, grid_ny)
+
+
+def parse_scan_config(text: str) -> N.ScanConfig:
+    out = N.ScanConfig()
+    _check(_lib().ss_parse_scan_config(text.encode(), C.byref(out)))
+    return out
+
+
+def make_grid(cfg: N.ScanConfig) -> N.GridSpec:
+    g = N.GridSpec()
+    _check(_lib().ss_make_grid(C.byref(cfg), C.byref(g)))
+    return g
+
+
+def snake_index(c, r, grid: N.GridSpec) -> int:
+    j = C.c_int()
+    _check(_lib().ss_snake_index(c, r, C.byref(grid), C.byref(j)))
+    return j.value
+
+
+def snake_inverse(j, grid: N.GridSpec):
+    c, r = C.c_int(), C.c_int()
+    _check(_lib().ss_snake_inverse(j, C.byref(grid), C.byref(c), C.byref(r)))
+    return c.value, r.value
+
+
+def enumerate_rays(cfg: N.ScanConfig):
+    """geometry.cpp:132-173 -> (rays[M,4] as (sx,sy,dx,dy), samples, pitch)"""
+    cnt, samples, pitch = N.i64(), C.c_int(), C.c_double()
+    _check(_lib().ss_enumerate_rays(C.byref(cfg), None, C.byref(cnt), C.byref(samples),
+                                    C.byref(pitch)))
+    rays = np.empty((cnt.value, 4))
+    _check(_lib().ss_enumerate_rays(C.byref(cfg), _dp(rays), C.byref(cnt), C.byref(samples),
+                                    C.byref(pitch)))
+    return rays, samples.value, pitch.value
+
+
+def build_system(cfg: N.ScanConfig, parallelism: int = 0,
+                 ctx: Optional[Context] = None) -> CentroSystem:
+    """geometry.cpp:227-275 on the GPU: A with p = 0 and symmetry_tol = 0."""
+    ctx = ctx or default_context()
+    h = N.vp()
+    _check(_lib().ss_build_system(ctx.h, C.byref(cfg), parallelism, C.byref(h)))
+    a = Matrix(h, ctx)
+    return CentroSystem(a, np.zeros(a.shape[0]), 0.0)
+
+
+# ----------------------------------------------------------------- phantom
+def random_ellipses(seed: int, count: int = 8):
+    out = np.empty((count, 6))
+    _check(_lib().ss_random_ellipses(seed, count, _dp(out)))
+    return out
+
+
+def rasterize(ellipses, grid: N.GridSpec, ctx: Optional[Context] = None):
+    """phantom.cpp:34-58 on the GPU; ellipses rows (x0, y0, a, b, angle, density)."""
+    ctx = ctx or default_context()
+    e = _f64(np.asarray(ellipses, dtype=np.float64).reshape(-1, 6))
+    out = np.empty(grid.n_x * grid.n_y)
+    _check(_lib().ss_rasterize(ctx.h, _dp(e), len(e), C.byref(grid), _dp(out)))
+    return out
+
+
+def forward_project(a: Matrix, f, noise_sigma: float = 0.0, seed: int = 0):
+    """phantom.cpp:108-149: folded row sums on the GPU, seeded noise on the host."""
+    f = _f64(f)
+    rows, cols = a.shape
+    if f.shape != (cols,):
+        raise Error("forward_project: image length does not match columns")
+    p = np.empty(rows)
+    _check(_lib().ss_forward_project(a.h, _dp(f), _dp(p)))
+    if noise_sigma != 0.0 or noise_sigma < 0:
+        _check(_lib().ss_add_noise(_dp(p), rows, C.c_double(noise_sigma), C.c_uint64(seed)))
+    return p
+
+
+# ----------------------------------------------------------------- plans
+class SartPlan:
+    """Device-resident SART loop over one system or the folded pair (ss_plan_t).
+
+    Normalisers are computed at construction (the reference computes them
+    before its timer). `run()` = one full solve from x0 = 0.
+    """
+
+    def __init__(self, a1: Matrix, a2: Optional[Matrix] = None,
+                 opts: Optional[SolveOptions] = None, nrhs: int = 1):
+        self.opts = opts or SolveOptions()
+        self.ctx = a1.ctx
+        self.nsys = 2 if a2 is not None else 1
+        self.nrhs = nrhs
+        self.a = (a1, a2)  # keep the matrices alive
+        h = N.vp()
+        o = self.opts._c()
+        _check(_lib().ss_plan_create(self.ctx.h, a1.h, a2.h if a2 is not None else None,
+                                     C.byref(o), nrhs, C.byref(h)))
+        self.h = h
+        self.rows, self.cols = a1.shape
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and N._lib is not None:
+                N._lib.ss_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def set_rhs(self, which, p):
+        p = _f64(p)
+        if p.size != self.rows * self.nrhs:
+            raise Error("plan: rhs size mismatch")
+        _check(_lib().ss_plan_set_rhs(self.h, which, _dp(p)))
+
+    def set_rhs_device(self, which, ptr: int):
+        _check(_lib().ss_plan_set_rhs_device(self.h, which, N.vp(ptr)))
+
+    def launch(self):
+        _check(_lib().ss_plan_launch(self.h))
+
+    def finish(self) -> N.SolveReportC:
+        r = N.SolveReportC()
+        _check(_lib().ss_plan_finish(self.h, C.byref(r)))
+        return r
+
+    def run(self) -> N.SolveReportC:
+        self.launch()
+        return self.finish()
+
+    def solution(self, which=0):
+        f = np.empty(self.cols * self.nrhs)
+        _check(_lib().ss_plan_get_solution(self.h, which, _dp(f)))
+        return f if self.nrhs == 1 else f.reshape(self.nrhs, self.cols)
+
+    def history(self, which=0, slice_=0):
+        h = np.empty(int(self.opts.max_iters) + 1)
+        n = C.c_int()
+        _check(_lib().ss_plan_get_history(self.h, which, slice_, _dp(h), C.byref(n)))
+        return h[:n.value].copy()
+
+    def recombine(self):
+        f = np.empty(2 * self.cols * self.nrhs)
+        _check(_lib().ss_plan_recombine(self.h, _dp(f)))
+        return f if self.nrhs == 1 else f.reshape(self.nrhs, 2 * self.cols)
+
+    def solution_device_ptr(self, which=0) -> int:
+        return _lib().ss_plan_solution_device(self.h, which) or 0
+
+    def stats(self):
+        mb, vb, k = N.i64(), N.i64(), C.c_int()
+        _check(_lib().ss_plan_stats(self.h, C.byref(mb), C.byref(vb), C.byref(k)))
+        return mb.value, vb.value, k.value
+
+    def profile(self, iters):
+        a, b = C.c_float(), C.c_float()
+        _check(_lib().ss_plan_profile(self.h, iters, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+# ----------------------------------------------------------------- multi-GPU helpers
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib().ss_nccl_unique_id(C.cast(buf, N.vp)))
+    return buf.raw
+
+
+def attach_nccl(ctx: Context, unique_id: bytes, nranks: int, rank: int):
+    buf = C.create_string_buffer(bytes(unique_id), 128)
+    _check(_lib().ss_ctx_attach_nccl(ctx.h, C.cast(buf, N.vp), nranks, rank))
+
+
+def partition_rows(rowptr, parts: int):
+    """Balanced row blocks of a CSR row pointer by nnz (host logic, no GPU)."""
+    rowptr = _i32(rowptr)
+    bounds = np.empty(parts + 1, np.int64)
+    _check(_lib().ss_partition_rows(_ip(rowptr), len(rowptr) - 1, parts,
+                                    bounds.ctypes.data_as(N.i64p)))
+    return bounds
+
+
+class ShardedSartPlan(SartPlan):
+    """Rows [row_begin, row_end) of one folded system on this rank; the
+    back-projection is all-reduced over the context's NCCL communicator."""
+
+    def __init__(self, ctx: Context, a: Matrix, row_begin: int, row_end: int,
+                 opts: Optional[SolveOptions] = None):
+        self.opts = opts or SolveOptions()
+        self.ctx = ctx
+        self.nsys = 1
+        self.nrhs = 1
+        self.a = (a, None)
+        h = N.vp()
+        o = self.opts._c()
+        _check(_lib().ss_plan_create_sharded(ctx.h, a.h, row_begin, row_end, C.byref(o),
+                                             C.byref(h)))
+        self.h = h
+        self.rows = row_end - row_begin
+        self.cols = a.shape[1]

@@ -1,0 +1,305 @@
+"""GPU path vs the CPU oracle, through the C ABI. Bit-exact for the build,
+fold, split_rhs, recombine, rasterize and forward projection (fp64); f and
+||Af - p||/||p|| within 1e-10 relative (fp64) / 1e-4 relative (fp32, against
+the fp64 oracle) after the fixed iteration count (north-star tolerances)."""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from helpers import oracle_workload, rel_err
+
+import paper_1902_10559_b200 as P
+from paper_1902_10559_b200.configs import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+TOL_F64 = 1e-10
+TOL_F32 = 1e-4
+
+_cache = {}
+
+
+def workload(idx):
+    if idx not in _cache:
+        w, cfg, a, csr, f_true, p = oracle_workload(idx, literal=idx <= 2)
+        sys_ = P.build_system(w.scan_config())
+        _cache[idx] = (w, cfg, a, csr, f_true, p, sys_)
+    return _cache[idx]
+
+
+def same_bytes(x, y):
+    x, y = np.asarray(x), np.asarray(y)
+    return x.dtype == y.dtype and x.shape == y.shape and x.tobytes() == y.tobytes()
+
+
+# ------------------------------------------------------------------ build / fold
+@pytest.mark.parametrize("idx", [1, 2])
+def test_build_system_bitexact(idx):
+    w, cfg, a, csr, f_true, p, s = workload(idx)
+    assert s.a.shape == (w.m, w.n) and s.symmetry_tol == 0.0 and np.all(s.p == 0)
+    got = s.a.to_csr()
+    want = csr.arrays()
+    assert all(same_bytes(g, e) for g, e in zip(got, want))
+    got_c = s.a.to_csc()
+    want_c = a.get_csc()
+    assert all(same_bytes(g, e) for g, e in zip(got_c, want_c))
+
+
+def test_build_system_config3_bitexact():
+    w, cfg, a, csr, f_true, p, s = workload(3)
+    got = s.a.to_csr()
+    assert all(same_bytes(g, e) for g, e in zip(got, csr.arrays()))
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_split_system_bitexact(idx):
+    w, cfg, a, csr, f_true, p, s = workload(idx)
+    want = O.split_system(a, p, 0.0)
+    got = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    for g, e in ((got.a1, want.a1), (got.a2, want.a2)):
+        assert all(same_bytes(x, y) for x, y in zip(g.to_csr(), e.to_csr().arrays()))
+        assert all(same_bytes(x, y) for x, y in zip(g.to_csc(), e.get_csc()))
+    assert same_bytes(got.p1, want.p1) and same_bytes(got.p2, want.p2)
+    assert got.parent_fill == want.parent_fill
+    assert got.fill1 == want.fill1 and got.fill2 == want.fill2
+
+
+def test_fold_config3_bitexact():
+    w, cfg, a, csr, f_true, p, s = workload(3)
+    f1, f2 = O.fold_rows_csr(csr)
+    got = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    for g, e in ((got.a1, f1), (got.a2, f2)):
+        assert all(same_bytes(x, y) for x, y in zip(g.to_csr(), e.arrays()))
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_phantom_and_projection_bitexact(idx):
+    w, cfg, a, csr, f_true, p, s = workload(idx)
+    grid = P.make_grid(w.scan_config())
+    ell = P.random_ellipses(w.seed(), 8)
+    assert same_bytes(ell, O.random_ellipses(w.seed(), 8))
+    img = P.rasterize(ell, grid)
+    assert same_bytes(img, f_true)
+    pg = P.forward_project(s.a, img)
+    if w.noise_frac:
+        pg = P.forward_project(s.a, img, w.noise_frac * float(np.max(pg)), w.noise_seed())
+    assert same_bytes(pg, p)
+
+
+def test_verify_symmetry_built():
+    w, cfg, a, csr, f_true, p, s = workload(1)
+    r = P.verify_symmetry(s.a, 0.0)
+    assert r.holds and r.max_violation == 0.0 and (r.worst_row, r.worst_col) == (1, 1)
+
+
+# ------------------------------------------------------------------ SART parity
+@pytest.mark.parametrize("idx", [1, 2])
+def test_solve_split_f64(idx):
+    w, cfg, a, csr, f_true, p, s = workload(idx)
+    want = O.solve_split(a, p, 0.0, w.iters, 0.0, w.relaxation)
+    got = P.solve_split(P.CentroSystem(s.a, p, 0.0),
+                        P.SolveOptions(max_iters=w.iters, tol=0.0, relaxation=w.relaxation))
+    assert got.iterations == want.iterations == w.iters
+    assert rel_err(got.f, want.f) <= TOL_F64
+    pn = np.linalg.norm(p)
+    assert abs(got.residual_norm - want.residual_norm) / pn <= TOL_F64
+    assert abs(got.solution_norm - want.solution_norm) <= TOL_F64 * want.solution_norm
+
+
+@pytest.mark.parametrize("idx", [2, 3])
+def test_solve_split_f32(idx):
+    w, cfg, a, csr, f_true, p, s = workload(idx)
+    iters = w.iters if idx == 2 else 10  # config 3: bounded oracle time
+    if a is None:
+        f1, f2 = O.fold_rows_csr(csr)
+        p1, p2 = O.split_rhs(p)
+        want_f, it, _ = O.solve_split_prepared(f1.to_matrix(), f2.to_matrix(), p1, p2, iters,
+                                               0.0, w.relaxation)  # recombined f
+        want_res = np.linalg.norm(csr_apply(csr, want_f) - p)
+    else:
+        want = O.solve_split(a, p, 0.0, iters, 0.0, w.relaxation)
+        want_f, want_res = want.f, want.residual_norm
+    got = P.solve_split(P.CentroSystem(s.a, p, 0.0),
+                        P.SolveOptions(max_iters=iters, tol=0.0, relaxation=w.relaxation,
+                                       dtype="f32"))
+    assert rel_err(got.f, want_f) <= TOL_F32
+    assert abs(got.residual_norm - want_res) / np.linalg.norm(p) <= TOL_F32
+
+
+def csr_apply(csr, x):
+    ptr, idx, val = csr.arrays()
+    rows = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    return np.bincount(rows, weights=val * x[idx], minlength=len(ptr) - 1)
+
+
+def test_sart_solve_history_f64():
+    w, cfg, a, csr, f_true, p, s = workload(1)
+    sp = O.split_system(a, p, 0.0)
+    want = O.sart_solve(sp.a1, sp.p1, max_iters=30, tol=0.0, relaxation=1.0)
+    gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    got = P.sart_solve(gs.a1, gs.p1, P.SolveOptions(max_iters=30, tol=0.0))
+    assert got.iterations == want.iterations == 30
+    assert len(got.residual_history) == len(want.residual_history) == 30
+    assert np.max(np.abs(np.array(got.residual_history) - want.residual_history) /
+                  want.residual_history) <= TOL_F64
+    assert rel_err(got.f, want.f) <= TOL_F64
+
+
+def test_sart_tolerance_stop_matches():
+    w, cfg, a, csr, f_true, p, s = workload(1)
+    sp = O.split_system(a, p, 0.0)
+    want = O.sart_solve(sp.a2, sp.p2, max_iters=200, tol=0.05)
+    gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    got = P.sart_solve(gs.a2, gs.p2, P.SolveOptions(max_iters=200, tol=0.05))
+    assert got.iterations == want.iterations < 200
+    assert len(got.residual_history) == want.iterations + 1
+    assert rel_err(got.f, want.f) <= TOL_F64
+
+
+def test_determinism_and_parallelism_invariance():
+    w, cfg, a, csr, f_true, p, s = workload(2)
+    sysg = P.CentroSystem(s.a, p, 0.0)
+    r1 = P.solve_split(sysg, P.SolveOptions(max_iters=20, tol=0.0, parallelism=1))
+    r8 = P.solve_split(sysg, P.SolveOptions(max_iters=20, tol=0.0, parallelism=8))
+    r8b = P.solve_split(sysg, P.SolveOptions(max_iters=20, tol=0.0, parallelism=8))
+    assert r1.f.tobytes() == r8.f.tobytes() == r8b.f.tobytes()
+
+
+def test_multi_rhs_plan_matches_single():
+    w, cfg, a, csr, f_true, p, s = workload(1)
+    gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    S = 5
+    rng = np.random.default_rng(7)
+    ps1 = np.stack([gs.p1 * (1 + 0.1 * k) + rng.standard_normal(len(gs.p1)) * 0.01 for k in range(S)])
+    ps2 = np.stack([gs.p2 * (1 - 0.05 * k) for k in range(S)])
+    opts = P.SolveOptions(max_iters=25, tol=0.0)
+    multi = P.SartPlan(gs.a1, gs.a2, opts, nrhs=S)
+    multi.set_rhs(0, ps1.reshape(-1))
+    multi.set_rhs(1, ps2.reshape(-1))
+    multi.run()
+    m1, m2 = multi.solution(0), multi.solution(1)
+    for k in range(S):
+        single = P.SartPlan(gs.a1, gs.a2, opts)
+        single.set_rhs(0, ps1[k])
+        single.set_rhs(1, ps2[k])
+        single.run()
+        assert rel_err(m1[k], single.solution(0)) <= 1e-12
+        assert rel_err(m2[k], single.solution(1)) <= 1e-12
+        want = O.sart_solve(O.split_system(a, p, 0.0).a1, ps1[k], max_iters=25, tol=0.0)
+        assert rel_err(m1[k], want.f) <= TOL_F64
+        assert np.allclose(multi.history(0, k), want.residual_history, rtol=TOL_F64, atol=0)
+
+
+# ------------------------------------------------------------------ reference pins on the GPU
+def ex1(pins):
+    return np.array(pins["example1"]["matrix"], float), np.array(pins["example1"]["rhs"], float)
+
+
+def test_example1_split_pins(pins):
+    d, p = ex1(pins)
+    s = P.split_system(P.CentroSystem(P.Matrix.dense(d), p, 0.0))
+    e = pins["example1_split"]
+    assert np.array_equal(s.a1.to_dense(), e["a1"]) and np.array_equal(s.a2.to_dense(), e["a2"])
+    assert np.array_equal(s.p1, e["p1"]) and np.array_equal(s.p2, e["p2"])
+    assert s.a1.nonzeros() == e["a1_nonzeros"] and s.a1.stored == 5
+    c = pins["split_2x2"]
+    s = P.split_system(P.CentroSystem(P.Matrix.dense(c["matrix"]), c["rhs"], 0.0))
+    assert s.a1.to_dense()[0, 0] == c["a1"] and s.a2.to_dense()[0, 0] == c["a2"]
+    assert s.p1[0] == c["p1"] and s.p2[0] == c["p2"]
+
+
+def test_symmetry_errors(pins):
+    d, p = ex1(pins)
+    i, j, v = pins["verify_symmetry_perturbed"]["perturb"]
+    d[i, j] = v
+    a = P.Matrix.dense(d)
+    r = P.verify_symmetry(a, 0.0)
+    assert not r.holds and r.max_violation == 8.0 and (r.worst_row, r.worst_col) == (1, 1)
+    with pytest.raises(P.SymmetryError) as ei:
+        P.split_system(P.CentroSystem(a, p, 1e-12))
+    assert ei.value.report.max_violation == 8.0
+    assert "not centrosymmetric (max violation 8 at (1,1), tol 1e-12)" in str(ei.value)
+    with pytest.raises(P.SymmetryError):
+        P.solve_split(P.CentroSystem(a, p, 1e-12), P.SolveOptions(tol=0.0))
+    r = P.verify_symmetry(P.Matrix.dense(np.eye(3)), 1.0)
+    assert not r.holds and r.status == 1
+    assert P.verify_symmetry(P.Matrix.dense(np.ones((2, 3))), 1.0).status == 2
+
+
+def test_rhs_and_recombine_pins(pins):
+    for c in pins["split_rhs_cases"]["cases"]:
+        p1, p2 = P.split_rhs(c["p"])
+        assert np.array_equal(p1, c["p1"]) and np.array_equal(p2, c["p2"])
+    with pytest.raises(P.Error):
+        P.split_rhs(np.zeros(3))
+    c = pins["recombine_general"]
+    assert np.array_equal(P.recombine_solution(c["f1"], c["f2"]), c["f"])
+    c = pins["recombine_published"]
+    assert np.max(np.abs(P.recombine_solution(c["f1"], c["f2"]) - c["f"])) <= c["tol"]
+    c = pins["decompose_published"]
+    pair = P.decompose_solution(c["f"])
+    assert np.max(np.abs(pair.f1 - c["f1"])) <= c["tol"]
+    with pytest.raises(P.Error, match="component lengths differ"):
+        P.recombine_solution(np.zeros(3), np.zeros(2))
+    with pytest.raises(P.Error, match="non-finite component"):
+        P.recombine_solution(np.array([np.inf]), np.zeros(1))
+
+
+def test_forward_project_pin(pins):
+    d, _ = ex1(pins)
+    a = P.Matrix.dense(d)
+    e1 = np.zeros(6)
+    e1[0] = 1.0
+    assert np.array_equal(P.forward_project(a, e1), pins["forward_project_e1"]["column0"])
+    with pytest.raises(P.Error):
+        P.forward_project(a, np.zeros(5))
+
+
+def test_sart_identity_and_errors(pins):
+    c = pins["sart_identity"]
+    p = O.rng_uniform(c["seed"], c["n"], 0.1, 1.0)
+    r = P.sart_solve(P.Matrix.dense(np.eye(c["n"])), p, P.SolveOptions(tol=c["tol"]))
+    assert r.iterations == 1 and np.max(np.abs(r.f - p)) <= c["tol"]
+    a = P.Matrix.dense(np.eye(2))
+    with pytest.raises(P.Error, match="no nonzero rows"):
+        P.sart_solve(P.Matrix.from_triplets(4, 4, [], [], []), np.ones(4))
+    with pytest.raises(P.Error, match=r"relaxation must be in \(0, 2\]"):
+        P.sart_solve(a, np.ones(2), P.SolveOptions(relaxation=2.5))
+    with pytest.raises(P.Error, match="max_iters must be >= 1"):
+        P.sart_solve(a, np.ones(2), P.SolveOptions(max_iters=0))
+    with pytest.raises(P.Error, match="rhs length 3 does not match rows 2"):
+        P.sart_solve(a, np.ones(3))
+    with pytest.raises(P.Error, match="non-finite rhs"):
+        P.sart_solve(a, np.array([1.0, np.nan]))
+
+
+def test_split_limit_and_branch_failure(pins):
+    from test_oracle_pins import split_limit_system
+    c = pins["sart_split_limit"]
+    ao, p = split_limit_system(c)
+    outer, inner, val = ao.get_csc() if ao.is_sparse else (None, None, None)
+    a = P.Matrix.dense(ao.to_dense())
+    opts = P.SolveOptions(max_iters=c["iters"], tol=c["tol"])
+    full = P.sart_solve(a, p, opts)
+    split = P.solve_split(P.CentroSystem(a, p, 1e-10), opts)
+    assert np.linalg.norm(full.f - split.f) <= c["agree"] * max(1.0, np.linalg.norm(full.f))
+    cc = np.array([[1.0, 2.0], [3.0, 0.5]])
+    z = O.reconstruct_matrix(O.Matrix.dense(np.zeros((2, 2))), O.Matrix.dense(2.0 * cc))
+    with pytest.raises(P.Error, match=r"branch failure: \[system 1\] sart_solve: matrix has no nonzero rows"):
+        P.solve_split(P.CentroSystem(P.Matrix.dense(z.to_dense()), np.ones(4), 1e-12),
+                      P.SolveOptions(max_iters=10, tol=0.0))
+
+
+def test_triplets_and_csc_roundtrip():
+    a = P.Matrix.from_triplets(2, 2, [0, 1, 0, 0], [0, 1, 0, 0], [1e16, 5.0, 1.0, -1e16])
+    outer, inner, val = a.to_csc()
+    assert list(outer) == [0, 1, 2] and list(inner) == [0, 1]
+    assert val[0] == (1e16 + 1.0) - 1e16 and val[1] == 5.0
+    w, cfg, ao, csr, f_true, p, s = workload(1)
+    o, i, v = ao.get_csc()
+    b = P.Matrix.from_csc(w.m, w.n, o, i, v)
+    assert all(same_bytes(x, y) for x, y in zip(b.to_csr(), csr.arrays()))
+    x = np.linspace(-1, 1, w.n)
+    assert rel_err(b.apply(x), ao.apply(x)) <= 1e-14
+    y = np.linspace(0, 1, w.m)
+    assert rel_err(b.apply_transpose(y), ao.apply_transpose(y)) <= 1e-14
