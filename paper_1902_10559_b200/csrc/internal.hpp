@@ -35,6 +35,8 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 // Owning device buffer (cudaMalloc; 256-byte aligned, which the 128-bit
 // loads of the SpMV kernels rely on).
+constexpr std::size_t kSlackBytes = 128;
+
 template <class T>
 class DBuf {
  public:
@@ -58,7 +60,9 @@ class DBuf {
     release();
     if (n == 0) n = 1;  // keep a valid pointer for empty arrays
     void* q = nullptr;
-    SSB_CUDA(cudaMalloc(&q, n * sizeof(T)));
+    // 128 bytes of slack: the TMA streams of the SpMV kernels round their
+    // last bulk copy up to a 16-byte multiple and may read past the end.
+    SSB_CUDA(cudaMalloc(&q, n * sizeof(T) + kSlackBytes));
     p_ = static_cast<T*>(q);
     n_ = n;
   }

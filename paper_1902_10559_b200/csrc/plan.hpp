@@ -12,8 +12,17 @@ struct Plan {
   int nrhs = 1;
   int dtype = SS_F64;
   int vs_fwd = 32, vs_back = 8;
+  bool noalloc = false;  // matrix loads with L1::no_allocate
+  int uf_fwd = 2, uf_back = 2;  // load steps in flight per lane before the gathers
   int fwd_blocks = 0, back_blocks = 0;
   bool sharded = false;
+  bool stream = false;  // work-table kernels (mode 1 TMA ring, mode 2 flat stream)
+  int mode = 0;
+  int q_fwd = 4, q_back = 4;  // flat kernels: entries per lane per batch
+  int sys_blocks_f = 0x7fffffff, sys_blocks_b = 0x7fffffff;  // first CTA of system 1
+  int u_fwd = 4, u_back = 4;
+  int nwork_f = 0, nwork_b = 0;
+  DBuf<int2> work_f, work_b;  // per-warp [begin, end) vector ranges
   std::int64_t row_begin = 0, row_end = 0;  // sharded: rows kept by this rank
   ss_solve_options opts{};
   Matrix* a[2] = {nullptr, nullptr};
