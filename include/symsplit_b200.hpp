@@ -1,0 +1,394 @@
+// C++ facade of symsplit_b200 with the reference's API shape
+// (/root/reference/proj/include/symsplit/{matrix,centro,geometry,solvers}.hpp):
+// the same function names, argument meaning and exception types
+// (symsplit::Error, symsplit::SymmetryError), over the C ABI in
+// symsplit_b200.h. Header-only; link against libsymsplit_b200.so.
+//
+// Differences from the reference, all deliberate:
+//  * Eigen types are replaced by Eigen-free equivalents: Vector is
+//    std::vector<double>; Matrix is a device-resident sparse matrix handle
+//    (construct from compressed-column arrays, triplets or a dense
+//    column-major array);
+//  * only Method::sart is available (dense min-norm and CGLS are not on the
+//    B200 path); SolveOptions gains `dtype` (fp64 = reference arithmetic,
+//    fp32 = the bandwidth-halving variant);
+//  * every call runs on the GPU of the Context it was created on.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "symsplit_b200.h"
+
+namespace symsplit {
+
+using Index = std::int64_t;
+using Vector = std::vector<double>;
+
+// reference matrix.hpp:22-25
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+enum class SymmetryStatus { ok = 0, odd_row_count = 1, odd_col_count = 2 };
+
+// reference centro.hpp:16-22
+struct SymmetryReport {
+  bool holds = false;
+  double max_violation = 0.0;
+  Index worst_row = 1;
+  Index worst_col = 1;
+  SymmetryStatus status = SymmetryStatus::ok;
+};
+
+// reference centro.hpp:73-78
+class SymmetryError : public Error {
+ public:
+  SymmetryError(const std::string& what, SymmetryReport r) : Error(what), report(r) {}
+  SymmetryReport report;
+};
+
+namespace detail {
+inline SymmetryReport to_report(const ss_symmetry_report& r) {
+  return SymmetryReport{r.holds != 0, r.max_violation, r.worst_row, r.worst_col,
+                        static_cast<SymmetryStatus>(r.status)};
+}
+inline void check(int rc, const ss_symmetry_report* rep = nullptr) {
+  if (rc == SS_OK) return;
+  const std::string msg = ss_last_error();
+  if (rc == SS_ERR_SYMMETRY) {
+    throw SymmetryError(msg, rep ? to_report(*rep) : SymmetryReport{});
+  }
+  throw Error(msg);
+}
+}  // namespace detail
+
+// One CUDA stream + workspace on one device.
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    ss_ctx_t h = nullptr;
+    detail::check(ss_ctx_create(device, &h));
+    h_.reset(h, [](ss_ctx_t c) { ss_ctx_destroy(c); });
+  }
+  ss_ctx_t get() const { return h_.get(); }
+  static Context& default_context() {
+    static Context ctx(0);
+    return ctx;
+  }
+
+ private:
+  std::shared_ptr<ss_context> h_;
+};
+
+// reference matrix.hpp:34-87 (device sparse storage only)
+class Matrix {
+ public:
+  Matrix() = default;
+  explicit Matrix(ss_matrix_t h) : h_(h, [](ss_matrix_t m) { ss_matrix_destroy(m); }) {}
+
+  static Matrix from_csc(Index rows, Index cols, const std::vector<int32_t>& outer,
+                         const std::vector<int32_t>& inner, const Vector& values,
+                         const Context& ctx = Context::default_context()) {
+    ss_matrix_t h = nullptr;
+    detail::check(ss_matrix_from_csc(ctx.get(), rows, cols, static_cast<int64_t>(values.size()),
+                                     outer.data(), inner.data(), values.data(), &h));
+    return Matrix(h);
+  }
+  struct Triplet {
+    int32_t row, col;
+    double value;
+  };
+  // Matrix::from_triplets (matrix.cpp:12-18): repeats summed in order
+  static Matrix from_triplets(Index rows, Index cols, const std::vector<Triplet>& ts,
+                              const Context& ctx = Context::default_context()) {
+    std::vector<int32_t> r(ts.size()), c(ts.size());
+    Vector v(ts.size());
+    for (std::size_t k = 0; k < ts.size(); ++k) {
+      r[k] = ts[k].row;
+      c[k] = ts[k].col;
+      v[k] = ts[k].value;
+    }
+    ss_matrix_t h = nullptr;
+    detail::check(ss_matrix_from_triplets(ctx.get(), rows, cols, static_cast<int64_t>(ts.size()),
+                                          r.data(), c.data(), v.data(), &h));
+    return Matrix(h);
+  }
+  // Dense column-major data; nonzeros are stored.
+  static Matrix dense(Index rows, Index cols, const Vector& colmajor,
+                      const Context& ctx = Context::default_context()) {
+    std::vector<Triplet> ts;
+    for (Index j = 0; j < cols; ++j) {
+      for (Index i = 0; i < rows; ++i) {
+        const double v = colmajor[static_cast<std::size_t>(j * rows + i)];
+        if (v != 0.0) ts.push_back({static_cast<int32_t>(i), static_cast<int32_t>(j), v});
+      }
+    }
+    return from_triplets(rows, cols, ts, ctx);
+  }
+
+  Index rows() const { return shape().first; }
+  Index cols() const { return shape().second; }
+  std::pair<Index, Index> shape() const {
+    int64_t r = 0, c = 0, s = 0;
+    detail::check(ss_matrix_shape(h_.get(), &r, &c, &s));
+    return {r, c};
+  }
+  std::int64_t stored() const {
+    int64_t r = 0, c = 0, s = 0;
+    detail::check(ss_matrix_shape(h_.get(), &r, &c, &s));
+    return s;
+  }
+  std::int64_t nonzeros() const {
+    int64_t n = 0;
+    detail::check(ss_matrix_nonzeros(h_.get(), &n));
+    return n;
+  }
+  double fill_ratio() const {
+    double f = 0.0;
+    detail::check(ss_matrix_fill_ratio(h_.get(), &f));
+    return f;
+  }
+  Vector apply(const Vector& x) const {
+    if (static_cast<Index>(x.size()) != cols()) throw Error("matrix-vector size mismatch");
+    Vector y(static_cast<std::size_t>(rows()));
+    detail::check(ss_matrix_apply(h_.get(), x.data(), y.data()));
+    return y;
+  }
+  Vector apply_transpose(const Vector& y) const {
+    if (static_cast<Index>(y.size()) != rows()) throw Error("matrix-vector size mismatch");
+    Vector x(static_cast<std::size_t>(cols()));
+    detail::check(ss_matrix_apply_transpose(h_.get(), y.data(), x.data()));
+    return x;
+  }
+  // CSC download (reference Eigen compressed storage): outer, inner, values
+  void to_csc(std::vector<int32_t>& outer, std::vector<int32_t>& inner, Vector& values) const {
+    outer.resize(static_cast<std::size_t>(cols() + 1));
+    inner.resize(static_cast<std::size_t>(stored()));
+    values.resize(static_cast<std::size_t>(stored()));
+    detail::check(ss_matrix_download_csc(h_.get(), outer.data(), inner.data(), values.data()));
+  }
+  ss_matrix_t get() const { return h_.get(); }
+
+ private:
+  std::shared_ptr<ss_matrix> h_;
+};
+
+// reference centro.hpp:24-51
+struct CentroSystem {
+  Matrix a;
+  Vector p;
+  double symmetry_tol = 1e-12;
+};
+
+struct SplitSystem {
+  Matrix a1;
+  Vector p1;
+  Matrix a2;
+  Vector p2;
+  double parent_fill = 0.0;
+  double fill1 = 0.0;
+  double fill2 = 0.0;
+};
+
+struct SolutionPair {
+  Vector f1;
+  Vector f2;
+};
+
+enum class Method { dense_minnorm, cgls, sart };
+enum class Mode { direct, split };
+
+// reference solvers.hpp:19-27
+struct SolveOptions {
+  Method method = Method::sart;
+  int max_iters = 200;
+  double tol = 1e-10;
+  double relaxation = 1.0;
+  bool deterministic = true;
+  int parallelism = 0;
+  std::int64_t dense_cap = 50'000'000;
+  int dtype = SS_F64;  // B200 addition: SS_F64 or SS_F32
+};
+
+// reference solvers.hpp:29-45
+struct SolveReport {
+  Vector f;
+  double residual_norm = 0.0;
+  double solution_norm = 0.0;
+  int iterations = 0;
+  double wall_time_seconds = 0.0;
+  Method method = Method::sart;
+  Mode mode = Mode::direct;
+  std::vector<double> residual_history;
+  double split_seconds = 0.0;
+  double recombine_seconds = 0.0;
+  double branch1_seconds = 0.0;
+  double branch2_seconds = 0.0;
+};
+
+namespace detail {
+inline ss_solve_options to_c(const SolveOptions& o) {
+  if (o.method != Method::sart) throw Error("only Method::sart runs on the B200 path");
+  return ss_solve_options{o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype};
+}
+inline SolveReport from_c(Vector f, const ss_solve_report& r, Mode mode) {
+  SolveReport rep;
+  rep.f = std::move(f);
+  rep.residual_norm = r.residual_norm;
+  rep.solution_norm = r.solution_norm;
+  rep.iterations = r.iterations;
+  rep.wall_time_seconds = r.wall_time_seconds;
+  rep.mode = mode;
+  rep.split_seconds = r.split_seconds;
+  rep.recombine_seconds = r.recombine_seconds;
+  rep.branch1_seconds = r.branch1_seconds;
+  rep.branch2_seconds = r.branch2_seconds;
+  return rep;
+}
+}  // namespace detail
+
+// ------------------------------------------------------------------ centro
+inline SymmetryReport verify_symmetry(const Matrix& a, double tol) {
+  ss_symmetry_report r{};
+  detail::check(ss_verify_symmetry(a.get(), tol, &r));
+  return detail::to_report(r);
+}
+
+inline std::pair<Vector, Vector> split_rhs(const Vector& p,
+                                           const Context& ctx = Context::default_context()) {
+  Vector p1(p.size() / 2), p2(p.size() / 2);
+  detail::check(ss_split_rhs(ctx.get(), p.data(), static_cast<int64_t>(p.size()), p1.data(),
+                             p2.data()));
+  return {std::move(p1), std::move(p2)};
+}
+
+inline SplitSystem split_system(const CentroSystem& sys) {
+  const std::size_t mh = sys.p.size() / 2;
+  SplitSystem out;
+  out.p1.resize(mh);
+  out.p2.resize(mh);
+  ss_matrix_t a1 = nullptr, a2 = nullptr;
+  double fills[3] = {0, 0, 0};
+  ss_symmetry_report rep{};
+  detail::check(ss_split_system(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
+                                sys.symmetry_tol, &a1, &a2, out.p1.data(), out.p2.data(), fills,
+                                &rep),
+                &rep);
+  out.a1 = Matrix(a1);
+  out.a2 = Matrix(a2);
+  out.parent_fill = fills[0];
+  out.fill1 = fills[1];
+  out.fill2 = fills[2];
+  return out;
+}
+
+inline SolutionPair decompose_solution(const Vector& f,
+                                       const Context& ctx = Context::default_context()) {
+  SolutionPair s{Vector(f.size() / 2), Vector(f.size() / 2)};
+  detail::check(ss_decompose_solution(ctx.get(), f.data(), static_cast<int64_t>(f.size()),
+                                      s.f1.data(), s.f2.data()));
+  return s;
+}
+
+inline Vector recombine_solution(const SolutionPair& pair,
+                                 const Context& ctx = Context::default_context()) {
+  if (pair.f1.size() != pair.f2.size()) {
+    throw Error("recombine_solution: component lengths differ");
+  }
+  Vector f(2 * pair.f1.size());
+  detail::check(ss_recombine_solution(ctx.get(), pair.f1.data(), pair.f2.data(),
+                                      static_cast<int64_t>(pair.f1.size()), f.data()));
+  return f;
+}
+
+// ------------------------------------------------------------------ solvers
+inline SolveReport sart_solve(const Matrix& a, const Vector& p, const SolveOptions& opts) {
+  const ss_solve_options o = detail::to_c(opts);
+  Vector f(static_cast<std::size_t>(a.cols()));
+  Vector hist(static_cast<std::size_t>(opts.max_iters > 0 ? opts.max_iters + 1 : 1));
+  ss_solve_report r{};
+  detail::check(ss_sart_solve(a.get(), p.data(), static_cast<int64_t>(p.size()), &o, f.data(),
+                              static_cast<int64_t>(f.size()), &r, hist.data()));
+  SolveReport rep = detail::from_c(std::move(f), r, Mode::direct);
+  rep.residual_history.assign(hist.begin(), hist.begin() + r.history_len);
+  return rep;
+}
+
+inline SolveReport solve_direct(const CentroSystem& sys, const SolveOptions& opts) {
+  return sart_solve(sys.a, sys.p, opts);
+}
+
+inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts) {
+  const ss_solve_options o = detail::to_c(opts);
+  Vector f(static_cast<std::size_t>(sys.a.cols()));
+  ss_solve_report r{};
+  detail::check(ss_solve_split(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
+                               sys.symmetry_tol, &o, f.data(), static_cast<int64_t>(f.size()),
+                               &r));
+  return detail::from_c(std::move(f), r, Mode::split);
+}
+
+// ------------------------------------------------------------------ geometry
+using ScanConfig = ss_scan_config;
+using GridSpec = ss_grid_spec;
+
+inline constexpr double kPi = 3.14159265358979323846;
+inline constexpr double degrees_to_radians(double deg) { return deg * kPi / 180.0; }
+
+inline ScanConfig parse_scan_config(const std::string& text) {
+  ScanConfig c{};
+  detail::check(ss_parse_scan_config(text.c_str(), &c));
+  return c;
+}
+
+inline GridSpec make_grid(const ScanConfig& c) {
+  GridSpec g{};
+  detail::check(ss_make_grid(&c, &g));
+  return g;
+}
+
+inline int snake_index(int c, int r, const GridSpec& g) {
+  int j = 0;
+  detail::check(ss_snake_index(c, r, &g, &j));
+  return j;
+}
+
+// reference geometry.hpp:118: A on the GPU, p = 0, symmetry_tol = 0
+inline CentroSystem build_system(const ScanConfig& cfg, int parallelism = 0,
+                                 const Context& ctx = Context::default_context()) {
+  ss_matrix_t h = nullptr;
+  detail::check(ss_build_system(ctx.get(), &cfg, parallelism, &h));
+  CentroSystem sys{Matrix(h), {}, 0.0};
+  sys.p.assign(static_cast<std::size_t>(sys.a.rows()), 0.0);
+  return sys;
+}
+
+// ------------------------------------------------------------------ phantom
+inline Vector rasterize(const std::vector<double>& ellipses6, const GridSpec& g,
+                        const Context& ctx = Context::default_context()) {
+  Vector out(static_cast<std::size_t>(g.n_x) * static_cast<std::size_t>(g.n_y));
+  detail::check(ss_rasterize(ctx.get(), ellipses6.data(),
+                             static_cast<int>(ellipses6.size() / 6), &g, out.data()));
+  return out;
+}
+
+inline Vector forward_project(const Matrix& a, const Vector& f, double noise_sigma = 0.0,
+                              std::uint64_t seed = 0) {
+  if (static_cast<Index>(f.size()) != a.cols()) {
+    throw Error("forward_project: image length does not match columns");
+  }
+  Vector p(static_cast<std::size_t>(a.rows()));
+  detail::check(ss_forward_project(a.get(), f.data(), p.data()));
+  if (noise_sigma != 0.0) {
+    detail::check(ss_add_noise(p.data(), static_cast<int64_t>(p.size()), noise_sigma, seed));
+  }
+  return p;
+}
+
+}  // namespace symsplit

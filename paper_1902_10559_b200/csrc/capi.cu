@@ -1,7 +1,6 @@
 // extern "C" surface (include/symsplit_b200.h). Each function validates like
 // the reference function it replaces, runs on the device, and converts
 // exceptions to status codes + a thread-local message.
-#include <nccl.h>
 
 #include <chrono>
 #include <cmath>
@@ -10,6 +9,7 @@
 #include <sstream>
 #include <string>
 
+#include "nccl_dyn.hpp"
 #include "plan.hpp"
 
 namespace {
@@ -200,7 +200,7 @@ int ss_ctx_destroy(ss_ctx_t h) {
     ssb::Context* ctx = CX(h);
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->comm));
+    if (ctx->comm) ssb::nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
     ctx->scratch.release();
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -708,10 +708,7 @@ int ss_nccl_unique_id(void* out128) {
   return guarded([&] {
     need(out128, "out");
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) {
-      ssb::fail(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r), SS_ERR_NCCL);
-    }
+    ssb::nccl_check(ssb::nccl().GetUniqueId(&id), "ncclGetUniqueId");
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(out128, &id, sizeof id);
   });
@@ -725,10 +722,7 @@ int ss_ctx_attach_nccl(ss_ctx_t h, const void* uid, int nranks, int rank) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     ncclComm_t comm;
-    const ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
-    if (r != ncclSuccess) {
-      ssb::fail(std::string("ncclCommInitRank: ") + ncclGetErrorString(r), SS_ERR_NCCL);
-    }
+    ssb::nccl_check(ssb::nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
     ctx->comm = comm;
     ctx->nranks = nranks;
     ctx->rank = rank;

@@ -12,7 +12,6 @@
 // fixed-order two-level reduction (no float atomics): results are bitwise
 // reproducible run to run and independent of `parallelism`.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -21,6 +20,7 @@
 #include <cstring>
 #include <memory>
 
+#include "nccl_dyn.hpp"
 #include "plan.hpp"
 
 namespace ssb {
@@ -1219,12 +1219,10 @@ void do_iterations(Plan& P, int first, int count) {
       P.ctx->check_launch("sharded_r2_kernel");
       launch_back<T>(P, k, it);
       P.ctx->check_launch("sart_back(sharded)");
-      ncclResult_t nr = ncclAllReduce(bp, bp, static_cast<std::size_t>(cols + 1),
-                                      sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum,
-                                      static_cast<ncclComm_t>(P.ctx->comm), P.ctx->stream);
-      if (nr != ncclSuccess) {
-        fail(std::string("ncclAllReduce: ") + ncclGetErrorString(nr), SS_ERR_NCCL);
-      }
+      nccl_check(nccl().AllReduce(bp, bp, static_cast<std::size_t>(cols + 1),
+                                  sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum,
+                                  static_cast<ncclComm_t>(P.ctx->comm), P.ctx->stream),
+                 "ncclAllReduce");
       sart_sharded_update_kernel<T><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(
           reinterpret_cast<T*>(P.x[0].get()), bp, reinterpret_cast<const T*>(P.cinv[0].get()),
           cols, P.pnorm.get(), P.opts.tol, P.opts.relaxation, P.history.get(), P.state.get(), it);
@@ -1340,9 +1338,9 @@ void Plan::finish_rhs(int which) {
     // ||p||^2 = sum over ranks of the local ||p_g||^2
     square_kernel<<<1, 32, 0, ctx->stream>>>(pn, nrhs);
     ctx->check_launch("square_kernel");
-    const ncclResult_t r = ncclAllReduce(pn, pn, nrhs, ncclFloat64, ncclSum,
-                                         static_cast<ncclComm_t>(ctx->comm), ctx->stream);
-    if (r != ncclSuccess) fail(std::string("ncclAllReduce: ") + ncclGetErrorString(r), SS_ERR_NCCL);
+    nccl_check(nccl().AllReduce(pn, pn, nrhs, ncclFloat64, ncclSum,
+                                static_cast<ncclComm_t>(ctx->comm), ctx->stream),
+               "ncclAllReduce");
     sqrt_kernel<<<1, 32, 0, ctx->stream>>>(pn, nrhs);
     ctx->check_launch("sqrt_kernel");
   }

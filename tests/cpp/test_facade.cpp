@@ -1,0 +1,109 @@
+// C++ facade (include/symsplit_b200.hpp) exercised like the reference's own
+// doctest unit tests (proj/tests/unit/test_centro.cpp, test_solvers.cpp),
+// checked against the oracle (test infrastructure). Prints "ALL PASSED".
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "../../include/symsplit_b200.hpp"
+#include "../../oracle/oracle.hpp"
+
+static int failures = 0;
+#define CHECK(c)                                                        \
+  do {                                                                  \
+    if (!(c)) {                                                         \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+      ++failures;                                                       \
+    }                                                                   \
+  } while (0)
+
+int main() {
+  using namespace symsplit;
+  // Example 1 (oracles.hpp:165-178), column-major
+  const Vector ex1 = {1, 2, 7, 1, 3, 4, 3, 9, 5, 6, 8, 7, 7, 8, 6, 5, 9, 3, 4, 3, 1, 7, 2, 1};
+  const Vector rhs = {5, 6, 8, 7};
+  {  // test_centro.cpp:66-85, :126-133
+    const SplitSystem s = split_system({Matrix::dense(4, 6, ex1), rhs, 0.0});
+    std::vector<int32_t> o, i;
+    Vector v;
+    s.a1.to_csc(o, i, v);
+    CHECK(s.a1.nonzeros() == 5 && v.size() == 5);
+    CHECK(s.p1[0] == -2.0 && s.p1[1] == -2.0 && s.p2[0] == 12.0 && s.p2[1] == 14.0);
+    const Vector e2 = {2, 9, 12, 7, 12, 14};  // a2 column-major
+    s.a2.to_csc(o, i, v);
+    CHECK(v.size() == 6);
+    for (std::size_t k = 0; k < v.size(); ++k) CHECK(v[k] == e2[k]);
+  }
+  {  // test_centro.cpp:114-124
+    Vector bad = ex1;
+    bad[0] = 9;
+    bool thrown = false;
+    try {
+      split_system({Matrix::dense(4, 6, bad), rhs, 1e-12});
+    } catch (const SymmetryError& e) {
+      thrown = e.report.max_violation == 8.0 && e.report.worst_row == 1;
+    }
+    CHECK(thrown);
+  }
+  {  // test_centro.cpp:215-228
+    const Vector f = recombine_solution({{14, 10, -29}, {84, 80, -93}});
+    const Vector want = {49, 45, -61, -32, 35, 35};
+    for (int k = 0; k < 6; ++k) CHECK(f[k] == want[k]);
+  }
+  {  // test_solvers.cpp:153-171
+    Vector eye(25, 0.0), p = {0.5, 0.25, 0.75, 0.125, 1.0};
+    for (int k = 0; k < 5; ++k) eye[k * 5 + k] = 1.0;
+    SolveOptions o;
+    o.tol = 1e-12;
+    const SolveReport r = sart_solve(Matrix::dense(5, 5, eye), p, o);
+    CHECK(r.iterations == 1);
+    for (int k = 0; k < 5; ++k) CHECK(std::abs(r.f[k] - p[k]) <= 1e-12);
+    bool thrown = false;
+    try {
+      sart_solve(Matrix::from_triplets(4, 4, {}), Vector(4, 1.0), SolveOptions{});
+    } catch (const Error& e) {
+      thrown = std::string(e.what()).find("no nonzero rows") != std::string::npos;
+    }
+    CHECK(thrown);
+  }
+  {  // BASELINE config 1 through the facade vs the oracle
+    ScanConfig cfg{10, degrees_to_radians(18.0), 2.0, 1e-4, 1.0, 128, 7e-4, 1.0, 64, 64};
+    CentroSystem sys = build_system(cfg);
+    CHECK(sys.a.rows() == 1280 && sys.a.stored() == 98032);
+    const GridSpec g = make_grid(cfg);
+    std::vector<double> ell(48);
+    ss_random_ellipses(1000, 8, ell.data());
+    const Vector f_true = rasterize(ell, g);
+    sys.p = forward_project(sys.a, f_true);
+    SolveOptions o;
+    o.max_iters = 50;
+    o.tol = 0.0;
+    const SolveReport got = solve_split(sys, o);
+
+    oracle::ScanConfig oc;
+    oc.geom.k = 10;
+    oc.geom.gamma = oracle::degrees_to_radians(18.0);
+    oc.geom.h_e = 2.0;
+    oc.geom.h_m = 1e-4;
+    oc.geom.l_m = 1.0;
+    oc.geom.n_p = 128;
+    oc.geom.obj_size = 1.0;
+    oc.grid_nx = oc.grid_ny = 64;
+    oracle::CentroSystem os = oracle::build_system(oc.geom, oracle::make_grid(oc));
+    os.p = sys.p;
+    oracle::SolveOptions oo;
+    oo.max_iters = 50;
+    oo.tol = 0.0;
+    const oracle::SolveReport want = oracle::solve_split_sart(os, oo);
+    double num = 0, den = 0;
+    for (std::size_t k = 0; k < want.f.size(); ++k) {
+      num += (got.f[k] - want.f[k]) * (got.f[k] - want.f[k]);
+      den += want.f[k] * want.f[k];
+    }
+    CHECK(std::sqrt(num / den) <= 1e-10);
+    CHECK(got.iterations == 50 && got.mode == Mode::split);
+  }
+  if (failures == 0) std::printf("ALL PASSED\n");
+  return failures == 0 ? 0 : 1;
+}

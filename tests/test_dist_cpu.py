@@ -1,0 +1,132 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): the row-sharded SART of
+SURVEY §8e — nnz-balanced row blocks from the product's partition_rows, a
+per-iteration all-reduce of [A_g^T w_g | ||r_g||^2], identical updates on every
+rank — must reproduce the unsharded oracle sart_solve. The GPU version of the
+same decomposition is ss_plan_create_sharded (NCCL inside the library)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def csr_matvec(ptr, idx, val, x):
+    rows = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    return np.bincount(rows, weights=val * x[idx], minlength=len(ptr) - 1)
+
+
+def csr_rmatvec(ptr, idx, val, y, ncols):
+    rows = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    return np.bincount(idx, weights=val * y[rows], minlength=ncols)
+
+
+def sharded_sart(rank, world, ptr, idx, val, p, iters, relax, tol):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1902_10559_b200 as P
+    rows, ncols = len(ptr) - 1, int(idx.max()) + 1
+    bounds = P.symsplit.partition_rows(ptr, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    lptr = ptr[rb:re + 1] - ptr[rb]
+    lidx, lval = idx[ptr[rb]:ptr[re]], val[ptr[rb]:ptr[re]]
+    # normalisers: local rows, global columns (every rank holds the same col sums)
+    rsum = np.add.reduceat(np.abs(val), ptr[:-1]) if len(val) else np.zeros(rows)
+    rsum[np.diff(ptr) == 0] = 0.0
+    csum = np.bincount(idx, weights=np.abs(val), minlength=ncols)
+    rinv = np.where(rsum > 0, 1.0 / np.where(rsum > 0, rsum, 1.0), 0.0)[rb:re]
+    cinv = np.where(csum > 0, 1.0 / np.where(csum > 0, csum, 1.0), 0.0)
+    pl = p[rb:re]
+    pn2 = torch.tensor([float(pl @ pl)], dtype=torch.float64)
+    dist.all_reduce(pn2)
+    pnorm = float(np.sqrt(pn2.item()))
+    x = np.zeros(ncols)
+    hist = []
+    for it in range(iters):
+        r = pl - csr_matvec(lptr, lidx, lval, x)
+        w = rinv * r
+        buf = np.concatenate([csr_rmatvec(lptr, lidx, lval, w, ncols), [float(r @ r)]])
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t)
+        bp, r2 = t.numpy()[:-1], float(t.numpy()[-1])
+        res = np.sqrt(r2)
+        hist.append(res)
+        if res <= tol * pnorm:
+            break
+        x = x + relax * (bp * cinv)
+    return x, hist, (rb, re)
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    import pyoracle as O
+    from helpers import oracle_workload
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, cfg, a, csr, f_true, p = oracle_workload(1, literal=True)
+        f1, f2 = O.fold_rows_csr(csr)
+        p1, p2 = O.split_rhs(p)
+        out = {}
+        for name, m, pp in (("A1", f1, p1), ("A2", f2, p2)):
+            ptr, idx, val = m.arrays()
+            x, hist, rng = sharded_sart(rank, world, ptr, idx, val, pp, 30, w.relaxation, 0.0)
+            out[name] = (x, hist, rng)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_sart_matches_unsharded_oracle():
+    import torch.multiprocessing as mp
+
+    import pyoracle as O
+    from helpers import oracle_workload
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    w, cfg, a, csr, f_true, p = oracle_workload(1, literal=True)
+    split = O.split_system(a, p, 0.0)
+    for name, m, pp in (("A1", split.a1, split.p1), ("A2", split.a2, split.p2)):
+        want = O.sart_solve(m, pp, max_iters=30, tol=0.0, relaxation=w.relaxation)
+        x0, h0, r0 = results[0][name]
+        x1, h1, r1 = results[1][name]
+        assert r0[1] == r1[0] and r0[0] == 0 and r1[1] == m.shape[0]  # rows covered once
+        assert x0.tobytes() == x1.tobytes()  # identical update on every rank
+        assert np.linalg.norm(x0 - want.f) <= 1e-10 * np.linalg.norm(want.f)
+        assert np.allclose(h0, want.residual_history, rtol=1e-10, atol=0)
+
+
+def test_group_layout():
+    from paper_1902_10559_b200.dist import group_layout
+    assert group_layout(0, 4) == (0, 0, 2, [0, 1])
+    assert group_layout(3, 4) == (1, 1, 2, [2, 3])
+    assert group_layout(5, 8) == (1, 1, 4, [4, 5, 6, 7])
+    with pytest.raises(ValueError):
+        group_layout(0, 2)
+    with pytest.raises(ValueError):
+        group_layout(0, 6 + 1)
