@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsymsplit_b200.so")
+LIB_PATH = os.environ.get("SSB_LIB") or os.path.join(HERE, "libsymsplit_b200.so")  # SSB_LIB: A/B builds
 
 SS_OK, SS_ERR_INVALID, SS_ERR_SYMMETRY, SS_ERR_DIVERGED, SS_ERR_CUDA, SS_ERR_NCCL, SS_ERR_OOM = (
     0, 1, 2, 3, 4, 5, 6)

@@ -30,7 +30,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 #ifndef SSB_DIRECT_MIN_BLOCKS
-#define SSB_DIRECT_MIN_BLOCKS 1
+#define SSB_DIRECT_MIN_BLOCKS 4
 #endif
 constexpr int kDirectMinBlocks = SSB_DIRECT_MIN_BLOCKS;  // 32 registers: full occupancy
 
@@ -230,35 +230,78 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
 }
 
 // ------------------------------------------------------------ single RHS kernels
-// Grid-stride over the compressed vectors of both systems, VS lanes each. The
+// Grid-stride over the compressed vectors of one system, VS lanes each. The
+// system is CTA-uniform and a template parameter (CTAs [0, split) serve
+// system 0), so array pointers come straight from the parameter bank. The
 // next vector's pointer pair and epilogue operands are fetched before the
 // current dot product so their latency hides behind it.
 template <class T>
 struct VecCursor {
-  int s, i, beg, end;
+  int i, beg, end;
   T e1, e2;
 };
 
-template <class T, bool FWD>
-__device__ __forceinline__ void fetch_vec(const SartK<T>& k, long long g, int lane,
-                                          VecCursor<T>& c) {
-  const long long split = FWD ? k.rows0 : k.cols0;
-  c.s = g >= split ? 1 : 0;
-  c.i = static_cast<int>(g - (c.s ? split : 0));
-  const SysK<T>& S = k.s[c.s];
+template <class T, bool FWD, int SYS>
+__device__ __forceinline__ void fetch_vec(const SartK<T>& k, int i, int lane, VecCursor<T>& c) {
+  const SysK<T>& S = k.s[SYS];
   const int* ptr = FWD ? S.rp : S.cp;
-  c.beg = __ldg(ptr + c.i);
-  c.end = __ldg(ptr + c.i + 1);
+  c.i = i;
+  c.beg = __ldg(ptr + i);
+  c.end = __ldg(ptr + i + 1);
   c.e1 = T(0);
   c.e2 = T(0);
   if (lane == 0) {
     if (FWD) {
-      c.e1 = S.p[c.i];
-      c.e2 = S.rinv[c.i];
+      c.e1 = S.p[i];
+      c.e2 = S.rinv[i];
     } else {
-      c.e1 = k.bp_out ? T(0) : S.x[c.i];
-      c.e2 = S.cinv[c.i];
+      c.e1 = k.bp_out ? T(0) : S.x[i];
+      c.e2 = S.cinv[i];
     }
+  }
+}
+
+template <class T, int VS, int UF, bool NA, int SYS>
+__device__ __forceinline__ double fwd_rows(const SartK<T>& k, long long group, long long ngroups,
+                                           int lane, unsigned mask) {
+  const SysK<T>& S = k.s[SYS];
+  const long long n = SYS ? k.rows_total - k.rows0 : k.rows0;
+  double acc = 0.0;
+  VecCursor<T> cur, nxt;
+  if (group < n) fetch_vec<T, true, SYS>(k, static_cast<int>(group), lane, cur);
+  for (long long g = group; g < n; g += ngroups) {
+    if (g + ngroups < n) fetch_vec<T, true, SYS>(k, static_cast<int>(g + ngroups), lane, nxt);
+    const T dot = seg_dot<T, VS, UF, NA>(S.ci, S.rv, S.x, cur.beg, cur.end, lane, mask);
+    if (lane == 0) {
+      const T r = cur.e1 - dot;
+      S.w[cur.i] = cur.e2 * r;
+      acc += static_cast<double>(r) * static_cast<double>(r);
+    }
+    cur = nxt;
+  }
+  return acc;
+}
+
+template <class T, int VS, int UF, bool NA, int SYS>
+__device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, long long ngroups,
+                                          int lane, unsigned mask, int it) {
+  const SysK<T>& S = k.s[SYS];
+  const long long n = SYS ? k.cols_total - k.cols0 : k.cols0;
+  VecCursor<T> cur, nxt;
+  if (group < n) fetch_vec<T, false, SYS>(k, static_cast<int>(group), lane, cur);
+  for (long long g = group; g < n; g += ngroups) {
+    if (g + ngroups < n) fetch_vec<T, false, SYS>(k, static_cast<int>(g + ngroups), lane, nxt);
+    const T u = seg_dot<T, VS, UF, NA>(S.ri, S.cv, S.w, cur.beg, cur.end, lane, mask);
+    if (lane == 0) {
+      if (k.bp_out) {
+        k.bp_out[cur.i] = u;
+      } else {
+        const T xn = upd(cur.e1, k.relax, u, cur.e2);
+        S.x[cur.i] = xn;
+        if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * SYS + 2], 0, it + 1);
+      }
+    }
+    cur = nxt;
   }
 }
 
@@ -267,41 +310,27 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(Sa
   __shared__ double red[2][kWarps];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
-  const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
-  const long long ngroups = (long long)gridDim.x * kThreads / VS;
-  const bool on0 = sys_on(k.state, 0);
-  const bool on1 = k.nsys > 1 && sys_on(k.state, 1);
-  double acc0 = 0.0, acc1 = 0.0;
-  VecCursor<T> cur, nxt;
-  if (group < k.rows_total) fetch_vec<T, true>(k, group, lane, cur);
-  for (long long g = group; g < k.rows_total; g += ngroups) {
-    if (g + ngroups < k.rows_total) fetch_vec<T, true>(k, g + ngroups, lane, nxt);
-    if (cur.s ? on1 : on0) {
-      const SysK<T>& S = k.s[cur.s];
-      const T dot = seg_dot<T, VS, UF, NA>(S.ci, S.rv, S.x, cur.beg, cur.end, lane, mask);
-      if (lane == 0) {
-        const T r = cur.e1 - dot;
-        S.w[cur.i] = cur.e2 * r;
-        const double rd = static_cast<double>(r);
-        if (cur.s) acc1 += rd * rd; else acc0 += rd * rd;
-      }
-    }
-    cur = nxt;
+  const int split = k.sys_blocks[0];
+  const int sys = static_cast<int>(blockIdx.x) >= split ? 1 : 0;
+  const int bx = sys ? blockIdx.x - split : blockIdx.x;
+  const int nb = sys ? gridDim.x - split : min(split, static_cast<int>(gridDim.x));
+  const long long group = (bx * (long long)kThreads + threadIdx.x) / VS;
+  const long long ngroups = (long long)nb * kThreads / VS;
+  double acc = 0.0;
+  if (sys_on(k.state, sys)) {
+    acc = sys ? fwd_rows<T, VS, UF, NA, 1>(k, group, ngroups, lane, mask)
+              : fwd_rows<T, VS, UF, NA, 0>(k, group, ngroups, lane, mask);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
-    acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
-  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    red[0][warp] = acc0;
-    red[1][warp] = acc1;
-  }
+  if ((threadIdx.x & 31) == 0) red[0][warp] = acc;
   __syncthreads();
   if (threadIdx.x < k.nsys) {
     double t = 0.0;
-    for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
+    if (threadIdx.x == sys) {
+      for (int q = 0; q < kWarps; ++q) t += red[0][q];
+    }
     k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
   }
   if (k.bp_out) return;  // sharded plans reduce ||r||^2 across ranks instead
@@ -316,29 +345,15 @@ template <class T, int VS, int UF, bool NA>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(SartK<T> k, int it) {
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
-  const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
-  const long long ngroups = (long long)gridDim.x * kThreads / VS;
-  const bool on0 = sys_on(k.state, 0);
-  const bool on1 = k.nsys > 1 && sys_on(k.state, 1);
-  VecCursor<T> cur, nxt;
-  if (group < k.cols_total) fetch_vec<T, false>(k, group, lane, cur);
-  for (long long g = group; g < k.cols_total; g += ngroups) {
-    if (g + ngroups < k.cols_total) fetch_vec<T, false>(k, g + ngroups, lane, nxt);
-    if (cur.s ? on1 : on0) {
-      const SysK<T>& S = k.s[cur.s];
-      const T u = seg_dot<T, VS, UF, NA>(S.ri, S.cv, S.w, cur.beg, cur.end, lane, mask);
-      if (lane == 0) {
-        if (k.bp_out) {
-          k.bp_out[cur.i] = u;
-        } else {
-          const T xn = upd(cur.e1, k.relax, u, cur.e2);
-          S.x[cur.i] = xn;
-          if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * cur.s + 2], 0, it + 1);
-        }
-      }
-    }
-    cur = nxt;
-  }
+  const int split = k.sys_blocks[1];
+  const int sys = static_cast<int>(blockIdx.x) >= split ? 1 : 0;
+  const int bx = sys ? blockIdx.x - split : blockIdx.x;
+  const int nb = sys ? gridDim.x - split : min(split, static_cast<int>(gridDim.x));
+  const long long group = (bx * (long long)kThreads + threadIdx.x) / VS;
+  const long long ngroups = (long long)nb * kThreads / VS;
+  if (!sys_on(k.state, sys)) return;
+  if (sys) back_cols<T, VS, UF, NA, 1>(k, group, ngroups, lane, mask, it);
+  else back_cols<T, VS, UF, NA, 0>(k, group, ngroups, lane, mask, it);
 }
 
 // ------------------------------------------------------------ TMA-streamed kernels
@@ -1026,7 +1041,7 @@ int env_int(const char* name, int dflt) {
 // dependency chains in flight; adjacent rows (rays) share x lines in L1.
 int pick_vs(double avg) {
   if (avg >= 384) return 16;
-  if (avg >= 96) return 8;
+  if (avg >= 160) return 8;
   return 4;
 }
 
@@ -1708,6 +1723,17 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
       1, std::min<long long>(P->fwd_blocks, (fwd_groups + kThreads - 1) / kThreads)));
   P->back_blocks = static_cast<int>(std::max<long long>(
       1, std::min<long long>(P->back_blocks, (back_groups + kThreads - 1) / kThreads)));
+  if (nrhs == 1 && P->nsys == 2) {
+    // CTA-uniform systems: split the grid in proportion to each system's work
+    const auto split = [&](int& blocks, double w0, double w1) {
+      blocks = std::max(blocks, 2);
+      const int b0 = static_cast<int>(std::llround(blocks * w0 / std::max(w0 + w1, 1.0)));
+      return std::max(1, std::min(blocks - 1, b0));
+    };
+    const double n0 = static_cast<double>(a1->nnz), n1 = static_cast<double>(a2->nnz);
+    P->sys_blocks_f = split(P->fwd_blocks, n0 + 16.0 * a1->rows, n1 + 16.0 * a2->rows);
+    P->sys_blocks_b = split(P->back_blocks, n0 + 16.0 * a1->cols, n1 + 16.0 * a2->cols);
+  }
   if (nrhs == 1 && kernel_mode() != 0) setup_stream(*P, kernel_mode());
   alloc_common(*P);
   for (int s = 0; s < P->nsys; ++s) {
