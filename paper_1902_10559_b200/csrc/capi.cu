@@ -3,6 +3,8 @@
 // exceptions to status codes + a thread-local message.
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -53,7 +55,10 @@ ssb::Plan* PL(ss_plan_t p) {
 ss_matrix_t wrap(ssb::Matrix* a) { return reinterpret_cast<ss_matrix_t>(a); }
 ss_plan_t wrap(ssb::Plan* p) { return reinterpret_cast<ss_plan_t>(p); }
 
-void use_device(ssb::Context* c) { SSB_CUDA(cudaSetDevice(c->device)); }
+void use_device(ssb::Context* c) {
+  SSB_CUDA(cudaSetDevice(c->device));
+  ssb::alloc_stream() = c->stream;
+}
 
 template <class T>
 ssb::DBuf<T> to_device(ssb::Context* c, const T* h, std::int64_t n) {
@@ -95,6 +100,21 @@ double now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Phase timing of the host-facing calls (SSB_TRACE=1 prints to stderr).
+struct Trace {
+  ssb::Context* ctx;
+  bool on;
+  double t;
+  explicit Trace(ssb::Context* c) : ctx(c), on(std::getenv("SSB_TRACE") != nullptr), t(now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    ctx->sync();
+    const double n = now();
+    std::fprintf(stderr, "[ssb] %-28s %9.3f ms\n", what, (n - t) * 1e3);
+    t = n;
+  }
+};
+
 // ||A f - p|| and ||f|| on the device in fp64, after the timed loop like the
 // reference (solvers.cpp:194-197, :266-267).
 void fill_report(ssb::Matrix& a, const double* f_dev, const double* p_dev, ss_solve_report* rep) {
@@ -129,13 +149,16 @@ struct SplitOut {
 void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double tol, SplitOut& o,
                   ss_symmetry_report* rep) {
   if (m != a.rows) ssb::fail("split_system: right-hand side length does not match rows");
+  Trace tr(a.ctx);
   const ss_symmetry_report r = ssb::verify_symmetry(a, tol);
+  tr.mark("  verify_symmetry");
   if (!r.holds) {
     if (rep) *rep = r;
     throw ssb::Failure(SS_ERR_SYMMETRY, symmetry_message("split_system", r, tol));
   }
   ssb::Matrix *x = nullptr, *y = nullptr;
   ssb::fold(a, x, y);
+  tr.mark("  fold");
   o.a1.reset(x);
   o.a2.reset(y);
   o.p1.alloc(m / 2);
@@ -146,6 +169,7 @@ void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double to
   o.fills[0] = parent > 0 ? static_cast<double>(ssb::nonzeros(a)) / parent : 0.0;
   o.fills[1] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a1)) / half : 0.0;
   o.fills[2] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a2)) / half : 0.0;
+  tr.mark("  split_rhs + fills");
 }
 
 ssb::Grid to_grid(const ss_grid_spec* g) {
@@ -186,6 +210,12 @@ int ss_ctx_create(int device, ss_ctx_t* out) {
     auto c = std::make_unique<ssb::Context>();
     c->device = device;
     SSB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // keep freed pool memory for reuse instead of returning it to the driver
+    cudaMemPool_t pool;
+    SSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    std::uint64_t keep = UINT64_MAX;
+    SSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    ssb::alloc_stream() = c->stream;
     SSB_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     int l2 = 0;
     SSB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
@@ -199,6 +229,7 @@ int ss_ctx_destroy(ss_ctx_t h) {
     if (!h) return;
     ssb::Context* ctx = CX(h);
     cudaSetDevice(ctx->device);
+    ssb::alloc_stream() = ctx->stream;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) ssb::nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
     ctx->scratch.release();
@@ -250,8 +281,7 @@ int ss_matrix_destroy(ss_matrix_t a) {
   return guarded([&] {
     if (!a) return;
     ssb::Matrix* m = M(a);
-    cudaSetDevice(m->ctx->device);
-    m->ctx->sync();
+    use_device(m->ctx);
     delete m;
   });
 }
@@ -490,12 +520,15 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     ssb::Context* c = A->ctx;
     use_device(c);
     need(opts, "opts");
+    Trace tr(c);
     const double t0 = now();
     auto dp = to_device(c, p, m);
+    tr.mark("h2d p");
     SplitOut o;
     split_device(*A, dp.get(), m, symmetry_tol, o, nullptr);
     c->sync();
     const double split_seconds = now() - t0;
+    tr.mark("split_system");
     if (n != A->cols) ssb::fail("solve_split: solution length does not match columns");
     // Branch validation in the reference's order; failures of both branches
     // aggregate into one message (solvers.cpp:235-247).
@@ -521,17 +554,21 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       }
     }
     raise_if_failed(SS_ERR_INVALID);
+    tr.mark("branch validation");
     std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1));
+    tr.mark("plan (csc, norms, graph)");
     for (int s = 0; s < 2; ++s) {
       if (P->empty_rows[s]) errs[s] = "sart_solve: matrix has no nonzero rows";
     }
     raise_if_failed(SS_ERR_INVALID);
     P->set_rhs_device_f64(0, o.p1.get());
     P->set_rhs_device_f64(1, o.p2.get());
+    tr.mark("set rhs");
     P->launch();
     ss_solve_report rep{};
     try {
       P->finish(&rep);
+      tr.mark("sart loop");
     } catch (const ssb::Failure& e) {
       if (e.code != SS_ERR_DIVERGED) throw;
       for (int s = 0; s < 2; ++s) {
@@ -548,7 +585,9 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     P->recombine_device(fd.get());
     to_host(c, f, fd.get(), n);
     const double recombine_seconds = now() - t_rec0;
+    tr.mark("recombine + d2h f");
     fill_report(*A, fd.get(), dp.get(), &rep);
+    tr.mark("residual");
     rep.split_seconds = split_seconds;
     rep.recombine_seconds = recombine_seconds;
     rep.wall_time_seconds = split_seconds + rep.branch1_seconds + recombine_seconds;
@@ -615,8 +654,7 @@ int ss_plan_destroy(ss_plan_t plan) {
   return guarded([&] {
     if (!plan) return;
     ssb::Plan* P = PL(plan);
-    cudaSetDevice(P->ctx->device);
-    P->ctx->sync();
+    use_device(P->ctx);
     delete P;
   });
 }

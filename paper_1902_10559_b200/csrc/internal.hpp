@@ -3,6 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -33,10 +37,16 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define SSB_CUDA(x) ::ssb::cuda_check((x), #x)
 
-// Owning device buffer (cudaMalloc; 256-byte aligned, which the 128-bit
-// loads of the SpMV kernels rely on).
 constexpr std::size_t kSlackBytes = 128;
 
+// Stream on which device buffers are allocated and freed (stream-ordered
+// pool allocator). Every C-ABI entry point sets it to its context's stream,
+// so allocation, use and release are ordered on one stream and the pool
+// hands memory back without device-wide synchronisation.
+cudaStream_t& alloc_stream();
+
+// Owning device buffer from the stream-ordered pool (cudaMallocAsync; 256-byte
+// aligned, which the 128-bit loads of the SpMV kernels rely on).
 template <class T>
 class DBuf {
  public:
@@ -44,12 +54,13 @@ class DBuf {
   explicit DBuf(std::size_t n) { alloc(n); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      s_ = o.s_;
       o.p_ = nullptr;
       o.n_ = 0;
     }
@@ -60,14 +71,14 @@ class DBuf {
     release();
     if (n == 0) n = 1;  // keep a valid pointer for empty arrays
     void* q = nullptr;
-    // 128 bytes of slack: the TMA streams of the SpMV kernels round their
-    // last bulk copy up to a 16-byte multiple and may read past the end.
-    SSB_CUDA(cudaMalloc(&q, n * sizeof(T) + kSlackBytes));
+    s_ = alloc_stream();
+    // 128 bytes of slack: vector loads may round the last access up.
+    SSB_CUDA(cudaMallocAsync(&q, n * sizeof(T) + kSlackBytes, s_));
     p_ = static_cast<T*>(q);
     n_ = n;
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) cudaFreeAsync(p_, s_);
     p_ = nullptr;
     n_ = 0;
   }
@@ -78,6 +89,7 @@ class DBuf {
  private:
   T* p_ = nullptr;
   std::size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
 };
 
 struct Context {
@@ -96,11 +108,33 @@ struct Context {
     return scratch.get();
   }
   void launched(int n = 1) { launches += n; }
+  // blocking copy ordered on this context's stream (never on the legacy stream)
+  void copy(void* dst, const void* src, std::size_t bytes) {
+    if (bytes) SSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream));
+    sync();
+  }
   void sync() { SSB_CUDA(cudaStreamSynchronize(stream)); }
   void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) cuda_check(e, what);
     ++launches;
+  }
+};
+
+// Phase timing for diagnostics (SSB_TRACE=1 prints to stderr).
+struct PhaseTrace {
+  Context* ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTrace(Context* c)
+      : ctx(c), on(std::getenv("SSB_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    ctx->sync();
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ssb]     %-24s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
   }
 };
 

@@ -16,6 +16,11 @@
 
 namespace ssb {
 
+cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
 namespace {
 
 constexpr int kT = 256;
@@ -278,29 +283,48 @@ __global__ void count_nonzero_kernel(const double* v, std::int64_t n, unsigned l
 
 // ------------------------------------------------------------------ symmetry
 // Row i against the reflected row M-1-i (centro.cpp:46-66): for every stored
-// (i,j,v), d = |v - a(M-1-i, N-1-j)| (0 if absent). Keeps the row maximum
-// and the smallest column reaching it (strict '>' in column-major order).
+// (i,j,v), d = |v - a(M-1-i, N-1-j)| (0 if absent; the mirror coefficient is
+// found by binary search in the mirror row, like SparseMatrix::coeff). Keeps
+// the row maximum and the smallest column reaching it — the first entry in
+// column-major order with strict '>'. One warp per row.
 __global__ void symmetry_rows_kernel(const int* ptr, const int* col, const double* val,
                                      std::int64_t m, std::int64_t n, double* rmax, int* rarg) {
-  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (std::int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t w0 = (blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nw = ((std::int64_t)gridDim.x * blockDim.x) >> 5;
+  for (std::int64_t i = w0; i < m; i += nw) {
     const std::int64_t mi = m - 1 - i;
-    int q = ptr[mi + 1] - 1;
-    const int qb = ptr[mi];
+    const int mb = ptr[mi], me = ptr[mi + 1];
     double best = 0.0;
-    int arg = -1;
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    int arg = 0x7fffffff;
+    for (int k = ptr[i] + lane; k < ptr[i + 1]; k += 32) {
       const int j = col[k];
-      while (q >= qb && (n - 1 - col[q]) < j) --q;
-      const double mv = (q >= qb && (n - 1 - col[q]) == j) ? val[q] : 0.0;
+      const std::int64_t target = n - 1 - j;
+      int lo = mb, hi = me;
+      while (lo < hi) {
+        const int mid = lo + ((hi - lo) >> 1);
+        if (col[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      const double mv = (lo < me && col[lo] == target) ? val[lo] : 0.0;
       const double d = fabs(sub(val[k], mv));
-      if (d > best) {
+      if (d > best) {  // entries of a lane ascend in j: first maximum kept
         best = d;
         arg = j;
       }
     }
-    rmax[i] = best;
-    rarg[i] = arg;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+      if (ob > best || (ob == best && oa < arg)) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    if (lane == 0) {
+      rmax[i] = best;
+      rarg[i] = best > 0.0 ? arg : -1;
+    }
   }
 }
 
@@ -345,8 +369,10 @@ struct FoldArgs {
   std::int64_t m, n, mh, nh;
   const int* ptr1;  // fill pass: output row pointers
   const int* ptr2;
-  int* cnt1;        // count pass outputs
+  int* cnt1;        // per-lane bucket counts [mh][32] (count pass out, fill pass in)
   int* cnt2;
+  int* rcnt1;       // per-row counts (count pass)
+  int* rcnt2;
   int* col1;
   double* val1;
   int* col2;
@@ -366,65 +392,114 @@ __device__ __forceinline__ int first_at_least(const int* col, int b, int e, std:
 // (centro.cpp:109-128 visits them in this column-major triplet order). Each
 // term enters as h = 0.5*v (A1 signs +,-,-,+; A2 all +), summed left to right
 // from the first present term, then exact zeros (either sign) are pruned.
+// One warp per output row: the row's bucket range is cut into 32 equal bj
+// segments, lane q merges segment q (cursors placed by binary search). The
+// count pass records per-lane counts; the fill pass writes each lane's
+// buckets at the row offset plus the exclusive prefix of the lanes before it,
+// so the output is sorted by bj exactly as a sequential merge would be.
 template <bool FILL>
 __global__ void fold_kernel(FoldArgs a) {
-  for (std::int64_t bi = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; bi < a.mh;
-       bi += (std::int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t w0 = (blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nw = ((std::int64_t)gridDim.x * blockDim.x) >> 5;
+  const std::int64_t nm1 = a.n - 1;
+  for (std::int64_t bi = w0; bi < a.mh; bi += nw) {
     const std::int64_t top = bi, bot = a.m - 1 - bi;
-    int tl = a.ptr[top];
-    const int tl_end = first_at_least(a.col, a.ptr[top], a.ptr[top + 1], a.nh);
-    int tr = a.ptr[top + 1] - 1;
-    int bl = a.ptr[bot];
-    const int bl_end = first_at_least(a.col, a.ptr[bot], a.ptr[bot + 1], a.nh);
-    int br = a.ptr[bot + 1] - 1;
-    int o1 = FILL ? a.ptr1[bi] : 0, o2 = FILL ? a.ptr2[bi] : 0;
+    const int tb = a.ptr[top], te = a.ptr[top + 1];
+    const int bb = a.ptr[bot], be = a.ptr[bot + 1];
+    const int tmid = first_at_least(a.col, tb, te, a.nh);  // first TR entry of top
+    const int bmid = first_at_least(a.col, bb, be, a.nh);
+    // bucket span of the row (all four lists)
+    std::int64_t lo = a.nh, hi = -1;
+    if (tmid > tb) { lo = min(lo, (std::int64_t)a.col[tb]); hi = max(hi, (std::int64_t)a.col[tmid - 1]); }
+    if (bmid > bb) { lo = min(lo, (std::int64_t)a.col[bb]); hi = max(hi, (std::int64_t)a.col[bmid - 1]); }
+    if (te > tmid) { lo = min(lo, nm1 - a.col[te - 1]); hi = max(hi, nm1 - a.col[tmid]); }
+    if (be > bmid) { lo = min(lo, nm1 - a.col[be - 1]); hi = max(hi, nm1 - a.col[bmid]); }
     int n1 = 0, n2 = 0;
-    const std::int64_t nm1 = a.n - 1;
-    for (;;) {
-      std::int64_t bj = a.nh;
-      if (tl < tl_end) bj = min(bj, (std::int64_t)a.col[tl]);
-      if (bl < bl_end) bj = min(bj, (std::int64_t)a.col[bl]);
-      if (tr >= tl_end) bj = min(bj, (std::int64_t)nm1 - a.col[tr]);
-      if (br >= bl_end) bj = min(bj, (std::int64_t)nm1 - a.col[br]);
-      if (bj == a.nh) break;
-      bool have = false;
-      double s1 = 0.0, s2 = 0.0;
-      auto term = [&](double v, bool neg) {
-        const double h = mul(0.5, v);
-        const double t1 = neg ? -h : h;
-        if (!have) {
-          s1 = t1;
-          s2 = h;
-          have = true;
-        } else {
-          s1 = add(s1, t1);
-          s2 = add(s2, h);
+    if (hi >= lo) {
+      const std::int64_t span = hi - lo + 1;
+      const std::int64_t s_lo = lo + span * lane / 32, s_hi = lo + span * (lane + 1) / 32;
+      // TL/BL: columns in [s_lo, s_hi); TR/BR: columns in [n-s_hi, n-1-s_lo], walked down
+      int tl = first_at_least(a.col, tb, tmid, s_lo);
+      const int tl_end = first_at_least(a.col, tl, tmid, s_hi);
+      int bl = first_at_least(a.col, bb, bmid, s_lo);
+      const int bl_end = first_at_least(a.col, bl, bmid, s_hi);
+      const int tr_stop = first_at_least(a.col, tmid, te, a.n - s_hi);
+      int tr = first_at_least(a.col, tr_stop, te, a.n - s_lo) - 1;
+      const int br_stop = first_at_least(a.col, bmid, be, a.n - s_hi);
+      int br = first_at_least(a.col, br_stop, be, a.n - s_lo) - 1;
+      int o1 = 0, o2 = 0;
+      if (FILL) {
+        const int c1 = a.cnt1[bi * 32 + lane], c2 = a.cnt2[bi * 32 + lane];
+        int x1 = c1, x2 = c2;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
+          const int y2 = __shfl_up_sync(0xffffffffu, x2, off);
+          if (lane >= off) {
+            x1 += y1;
+            x2 += y2;
+          }
         }
-      };
-      if (tl < tl_end && a.col[tl] == bj) term(a.val[tl++], false);
-      if (bl < bl_end && a.col[bl] == bj) term(a.val[bl++], true);
-      if (tr >= tl_end && nm1 - a.col[tr] == bj) term(a.val[tr--], true);
-      if (br >= bl_end && nm1 - a.col[br] == bj) term(a.val[br--], false);
-      if (s1 != 0.0) {
-        if (FILL) {
-          a.col1[o1] = static_cast<int>(bj);
-          a.val1[o1] = s1;
-          ++o1;
-        }
-        ++n1;
+        o1 = a.ptr1[bi] + x1 - c1;
+        o2 = a.ptr2[bi] + x2 - c2;
       }
-      if (s2 != 0.0) {
-        if (FILL) {
-          a.col2[o2] = static_cast<int>(bj);
-          a.val2[o2] = s2;
-          ++o2;
+      for (;;) {
+        std::int64_t bj = s_hi;
+        if (tl < tl_end) bj = min(bj, (std::int64_t)a.col[tl]);
+        if (bl < bl_end) bj = min(bj, (std::int64_t)a.col[bl]);
+        if (tr >= tr_stop) bj = min(bj, nm1 - a.col[tr]);
+        if (br >= br_stop) bj = min(bj, nm1 - a.col[br]);
+        if (bj == s_hi) break;
+        bool have = false;
+        double s1 = 0.0, s2 = 0.0;
+        auto term = [&](double v, bool neg) {
+          const double h = mul(0.5, v);
+          const double t1 = neg ? -h : h;
+          if (!have) {
+            s1 = t1;
+            s2 = h;
+            have = true;
+          } else {
+            s1 = add(s1, t1);
+            s2 = add(s2, h);
+          }
+        };
+        if (tl < tl_end && a.col[tl] == bj) term(a.val[tl++], false);
+        if (bl < bl_end && a.col[bl] == bj) term(a.val[bl++], true);
+        if (tr >= tr_stop && nm1 - a.col[tr] == bj) term(a.val[tr--], true);
+        if (br >= br_stop && nm1 - a.col[br] == bj) term(a.val[br--], false);
+        if (s1 != 0.0) {
+          if (FILL) {
+            a.col1[o1] = static_cast<int>(bj);
+            a.val1[o1] = s1;
+            ++o1;
+          }
+          ++n1;
         }
-        ++n2;
+        if (s2 != 0.0) {
+          if (FILL) {
+            a.col2[o2] = static_cast<int>(bj);
+            a.val2[o2] = s2;
+            ++o2;
+          }
+          ++n2;
+        }
       }
     }
     if (!FILL) {
-      a.cnt1[bi] = n1;
-      a.cnt2[bi] = n2;
+      a.cnt1[bi * 32 + lane] = n1;
+      a.cnt2[bi * 32 + lane] = n2;
+      int t1 = n1, t2 = n2;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        t1 += __shfl_xor_sync(0xffffffffu, t1, off);
+        t2 += __shfl_xor_sync(0xffffffffu, t2, off);
+      }
+      if (lane == 0) {
+        a.rcnt1[bi] = t1;
+        a.rcnt2[bi] = t2;
+      }
     }
   }
 }
@@ -915,7 +990,7 @@ ss_symmetry_report verify_symmetry(Matrix& a, double tol) {
     DBuf<double> rmax(a.rows);
     DBuf<int> rarg(a.rows);
     DBuf<Worst> w(1);
-    symmetry_rows_kernel<<<grid_for(ctx, a.rows), kT, 0, ctx->stream>>>(
+    symmetry_rows_kernel<<<grid_for(ctx, a.rows * 32), kT, 0, ctx->stream>>>(
         a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, rmax.get(), rarg.get());
     ctx->check_launch("symmetry_rows_kernel");
     symmetry_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(rmax.get(), rarg.get(), a.rows, w.get());
@@ -935,13 +1010,14 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   if (a.rows % 2 != 0 || a.cols % 2 != 0) fail("split_matrix: dimensions must be even");
   Context* ctx = a.ctx;
   const std::int64_t mh = a.rows / 2, nh = a.cols / 2;
-  DBuf<int> c1(mh + 1), c2(mh + 1);
+  DBuf<int> lane1(mh * 32), lane2(mh * 32), c1(mh + 1), c2(mh + 1);
   SSB_CUDA(cudaMemsetAsync(c1.get() + mh, 0, sizeof(int), ctx->stream));
   SSB_CUDA(cudaMemsetAsync(c2.get() + mh, 0, sizeof(int), ctx->stream));
   FoldArgs fa{a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, mh, nh,
-              nullptr, nullptr, c1.get(), c2.get(), nullptr, nullptr, nullptr, nullptr};
+              nullptr, nullptr, lane1.get(), lane2.get(), c1.get(), c2.get(),
+              nullptr, nullptr, nullptr, nullptr};
   if (mh > 0) {
-    fold_kernel<false><<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(fa);
+    fold_kernel<false><<<grid_for(ctx, mh * 32), kT, 0, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<count>");
   }
   DBuf<int> p1(mh + 1), p2(mh + 1);
@@ -958,7 +1034,7 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   fa.col2 = col2.get();
   fa.val2 = val2.get();
   if (mh > 0) {
-    fold_kernel<true><<<grid_for(ctx, mh, 128), 128, 0, ctx->stream>>>(fa);
+    fold_kernel<true><<<grid_for(ctx, mh * 32), kT, 0, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<fill>");
   }
   ctx->sync();

@@ -1319,7 +1319,7 @@ void Plan::finish(ss_solve_report* rep) {
   SSB_CUDA(cudaEventSynchronize(ev1));
   SSB_CUDA(cudaEventElapsedTime(&last_ms, ev0, ev1));
   std::vector<int> st(state.size());
-  SSB_CUDA(cudaMemcpy(st.data(), state.get(), st.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  ctx->copy(st.data(), state.get(), st.size() * sizeof(int));
   int iters = 0;
   for (int q = 0; q < nsys * nrhs; ++q) {
     if (st[4 * q + 2] != 0) {
@@ -1395,7 +1395,7 @@ void Plan::set_rhs_device(int which, const void* p_dev) {
 
 int Plan::diverged_at(int which) const {
   int st[4] = {0, 0, 0, 0};
-  SSB_CUDA(cudaMemcpy(st, state.get() + 4 * which * nrhs, sizeof st, cudaMemcpyDeviceToHost));
+  ctx->copy(st, state.get() + 4 * which * nrhs, sizeof st);
   return st[2];
 }
 
@@ -1443,11 +1443,11 @@ void Plan::get_history(int which, int slice, double* h, int* len) {
   if (which < 0 || which >= nsys || slice < 0 || slice >= nrhs) fail("plan: index out of range");
   const int q = which * nrhs + slice;
   int st[4];
-  SSB_CUDA(cudaMemcpy(st, state.get() + 4 * q, sizeof st, cudaMemcpyDeviceToHost));
+  ctx->copy(st, state.get() + 4 * q, sizeof st);
   const int n = st[0] ? st[1] + 1 : opts.max_iters;
   if (h) {
-    SSB_CUDA(cudaMemcpy(h, history.get() + static_cast<std::int64_t>(q) * (opts.max_iters + 1),
-                        n * sizeof(double), cudaMemcpyDeviceToHost));
+    ctx->copy(h, history.get() + static_cast<std::int64_t>(q) * (opts.max_iters + 1),
+                        n * sizeof(double));
   }
   *len = n;
 }
@@ -1552,7 +1552,9 @@ void alloc_common(Plan& P) {
 void normalisers(Plan& P, int s, double* max_row_sum) {
   Matrix* a = P.a[s];
   DBuf<double> rs(P.rows[s]), cs(P.cols[s]);
+  if (a->ctx != P.ctx) P.ctx->sync();  // matrix on another context's stream
   abs_sums(*a, rs.get(), cs.get());
+  if (a->ctx != P.ctx) a->ctx->sync();
   *max_row_sum = max_dev(P.ctx, rs.get(), P.rows[s]);
   const int gr = grid1(P.ctx, P.rows[s]), gc = grid1(P.ctx, P.cols[s]);
   if (P.dtype == SS_F32) {
@@ -1594,8 +1596,8 @@ void build_work(Plan& P, bool fwd, int warps_per_block, long long max_warps, DBu
     Matrix* a = P.a[s];
     const long long n = fwd ? P.rows[s] : P.cols[s];
     ptr[s].resize(n + 1);
-    SSB_CUDA(cudaMemcpy(ptr[s].data(), fwd ? a->rowptr.get() : a->colptr.get(),
-                        (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    P.ctx->copy(ptr[s].data(), fwd ? a->rowptr.get() : a->colptr.get(),
+                        (n + 1) * sizeof(int));
     wsum[s] = static_cast<double>(ptr[s][n]) + 16.0 * n;
     nvec_total += n;
     nnz_total += ptr[s][n];
@@ -1636,7 +1638,7 @@ void build_work(Plan& P, bool fwd, int warps_per_block, long long max_warps, DBu
     off += n;
   }
   out.alloc(wk.size());
-  SSB_CUDA(cudaMemcpy(out.get(), wk.data(), wk.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  P.ctx->copy(out.get(), wk.data(), wk.size() * sizeof(int2));
   nwork = static_cast<int>(wk.size());
   blocks = static_cast<int>((wk.size() + warps_per_block - 1) / warps_per_block);
   unroll = pick_unroll(nvec_total > 0 ? static_cast<double>(nnz_total) / nvec_total : 0.0);
@@ -1692,10 +1694,13 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   P->a[0] = a1;
   P->a[1] = a2;
   double nnz_total = 0, rows_total = 0, cols_total = 0;
+  PhaseTrace tr(ctx);
   for (int s = 0; s < P->nsys; ++s) {
     Matrix* a = P->a[s];
     a->ensure_csc();
+    tr.mark("csc");
     if (o.dtype == SS_F32) a->ensure_f32();
+    tr.mark("f32 copies");
     P->rows[s] = a->rows;
     P->cols[s] = a->cols;
     nnz_total += a->nnz;
@@ -1736,13 +1741,16 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   }
   if (nrhs == 1 && kernel_mode() != 0) setup_stream(*P, kernel_mode());
   alloc_common(*P);
+  tr.mark("occupancy + alloc");
   for (int s = 0; s < P->nsys; ++s) {
     double mx = 0;
     normalisers(*P, s, &mx);
     P->empty_rows[s] = !(mx > 0.0);
   }
+  tr.mark("normalisers");
   if (P->nsys == 1 && P->empty_rows[0]) fail("sart_solve: matrix has no nonzero rows");
   P->build_graph();
+  tr.mark("graph capture");
   return P.release();
 }
 
@@ -1772,14 +1780,13 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   a->ensure_csc();
   // host-side slice of the CSR row block, then a local matrix on device
   std::vector<int> ptr(a->rows + 1);
-  SSB_CUDA(cudaMemcpy(ptr.data(), a->rowptr.get(), ptr.size() * sizeof(int),
-                      cudaMemcpyDeviceToHost));
+  ctx->copy(ptr.data(), a->rowptr.get(), ptr.size() * sizeof(int));
   const std::int64_t k0 = ptr[rb], k1 = ptr[re], nloc = k1 - k0, rloc = re - rb;
   std::vector<int> lptr(rloc + 1), lcol(nloc), lrow(nloc);
   std::vector<double> lval(nloc);
   for (std::int64_t r = 0; r <= rloc; ++r) lptr[r] = static_cast<int>(ptr[rb + r] - k0);
-  SSB_CUDA(cudaMemcpy(lcol.data(), a->colidx.get() + k0, nloc * sizeof(int), cudaMemcpyDeviceToHost));
-  SSB_CUDA(cudaMemcpy(lval.data(), a->val.get() + k0, nloc * sizeof(double), cudaMemcpyDeviceToHost));
+  ctx->copy(lcol.data(), a->colidx.get() + k0, nloc * sizeof(int));
+  ctx->copy(lval.data(), a->val.get() + k0, nloc * sizeof(double));
   for (std::int64_t r = 0; r < rloc; ++r) {
     for (int k = lptr[r]; k < lptr[r + 1]; ++k) lrow[k] = static_cast<int>(r);
   }
@@ -1813,7 +1820,11 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   P->bp.alloc((a->cols + 1) * P->tsize());
   // normalisers: rows from the local block, columns from the full matrix
   DBuf<double> rs_full(a->rows), cs_full(a->cols);
+  // `a` may live on another context (stream): order the buffers' allocation
+  // before, and the sums' completion after, the work on a->ctx's stream.
+  ctx->sync();
   abs_sums(*a, rs_full.get(), cs_full.get());
+  a->ctx->sync();
   const int gr = grid1(ctx, rloc), gc = grid1(ctx, a->cols);
   if (o.dtype == SS_F32) {
     inv_kernel<float><<<gr, 256, 0, ctx->stream>>>(rs_full.get() + rb,

@@ -303,3 +303,26 @@ def test_triplets_and_csc_roundtrip():
     assert rel_err(b.apply(x), ao.apply(x)) <= 1e-14
     y = np.linspace(0, 1, w.m)
     assert rel_err(b.apply_transpose(y), ao.apply_transpose(y)) <= 1e-14
+
+
+def test_sharded_plan_single_rank_nccl():
+    """Row-sharded plan (ss_plan_create_sharded: K1 on local rows, partial
+    back-projection, ncclAllReduce of [A^T w | ||r||^2], shared update) on a
+    1-rank NCCL communicator must equal the unsharded plan."""
+    import torch  # noqa: F401  (loads PyTorch's NCCL first, like bench.py)
+    w, cfg, a, csr, f_true, p, s = workload(2)
+    gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    ctx = P.Context(0)
+    P.symsplit.attach_nccl(ctx, P.symsplit.nccl_unique_id(), 1, 0)
+    for dtype in ("f64", "f32"):
+        opts = P.SolveOptions(max_iters=20, tol=0.0, relaxation=w.relaxation, dtype=dtype)
+        ref = P.SartPlan(gs.a2, None, opts)
+        ref.set_rhs(0, gs.p2)
+        ref.run()
+        rows = gs.a2.shape[0]
+        sh = P.symsplit.ShardedSartPlan(ctx, gs.a2, 0, rows, opts)
+        sh.set_rhs(0, gs.p2)
+        sh.run()
+        tol = 1e-12 if dtype == "f64" else 1e-5
+        assert rel_err(sh.solution(0), ref.solution(0)) <= tol
+        assert np.allclose(sh.history(0), ref.history(0), rtol=tol)
