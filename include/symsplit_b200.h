@@ -213,6 +213,9 @@ void* ss_plan_solution_device(ss_plan_t plan, int which);
 /* algorithmic bytes per iteration (matrices + pointers), kernels per iteration */
 int ss_plan_stats(ss_plan_t plan, int64_t* matrix_bytes_per_iter,
                   int64_t* vector_bytes_per_iter, int* kernels_per_iter);
+/* matrix bytes each SART kernel streams per launch in this plan's format
+ * (paired plans share one index stream between the two folded systems) */
+int ss_plan_kernel_bytes(ss_plan_t plan, int64_t* fwd_bytes, int64_t* back_bytes);
 /* time `iters` bare iterations of the loop with CUDA events on the context
  * stream (per-kernel split: fwd_ms = forward kernels, back_ms = back kernels) */
 int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms);

@@ -731,6 +731,10 @@ int ss_plan_stats(ss_plan_t plan, int64_t* mb, int64_t* vb, int* kernels) {
   return guarded([&] { PL(plan)->stats(mb, vb, kernels); });
 }
 
+int ss_plan_kernel_bytes(ss_plan_t plan, int64_t* fwd_bytes, int64_t* back_bytes) {
+  return guarded([&] { PL(plan)->kernel_bytes(fwd_bytes, back_bytes); });
+}
+
 int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms) {
   return guarded([&] {
     ssb::Plan* P = PL(plan);

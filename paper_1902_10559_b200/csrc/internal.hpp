@@ -203,6 +203,8 @@ void check_finite(Matrix& a);
 std::int64_t nonzeros(Matrix& a);
 ss_symmetry_report verify_symmetry(Matrix& a, double tol);
 void fold(Matrix& a, Matrix*& a1, Matrix*& a2);
+bool same_pattern(Matrix& a, Matrix& b);
+void union_pattern(Matrix& a, Matrix& b, Matrix*& ua, Matrix*& ub);
 void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh);
 void recombine_dev(Context* ctx, const double* f1, const double* f2, double* f,
                    std::int64_t nh, std::int64_t nrhs);

@@ -671,6 +671,45 @@ __global__ void forward_project_kernel(const int* ptr, const int* col, const dou
   }
 }
 
+
+// ------------------------------------------------------------------ paired pattern
+__global__ void diff_kernel(const int* a, const int* b, std::int64_t n, int* flag) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    if (a[k] != b[k]) {
+      atomicOr(flag, 1);
+      return;
+    }
+  }
+}
+
+// Union of the row patterns of two CSR matrices of equal shape; the value of
+// an entry missing from one of them is 0.0 (exactly what the fold pruned).
+template <bool FILL>
+__global__ void union_rows_kernel(const int* pa, const int* ca, const double* va, const int* pb,
+                                  const int* cb, const double* vb, std::int64_t rows, int* cnt,
+                                  const int* up, int* uc, double* ua, double* ub) {
+  for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (std::int64_t)gridDim.x * blockDim.x) {
+    int x = pa[i], xe = pa[i + 1], y = pb[i], ye = pb[i + 1];
+    int o = FILL ? up[i] : 0, n = 0;
+    while (x < xe || y < ye) {
+      const int cx = x < xe ? ca[x] : 0x7fffffff, cy = y < ye ? cb[y] : 0x7fffffff;
+      const int c = min(cx, cy);
+      if (FILL) {
+        uc[o] = c;
+        ua[o] = cx == c ? va[x] : 0.0;
+        ub[o] = cy == c ? vb[y] : 0.0;
+        ++o;
+      }
+      if (cx == c) ++x;
+      if (cy == c) ++y;
+      ++n;
+    }
+    if (!FILL) cnt[i] = n;
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 template <class T>
 void upload(Context* ctx, T* dst, const T* src, std::size_t n) {
@@ -1152,6 +1191,51 @@ void forward_project_dev(Matrix& a, const double* f, double* p) {
   forward_project_kernel<<<grid_for(a.ctx, a.rows), kT, 0, a.ctx->stream>>>(
       a.rowptr.get(), a.colidx.get(), a.val.get(), f, a.rows, a.cols, p);
   a.ctx->check_launch("forward_project_kernel");
+}
+
+
+bool same_pattern(Matrix& a, Matrix& b) {
+  if (a.rows != b.rows || a.cols != b.cols || a.nnz != b.nnz) return false;
+  Context* ctx = a.ctx;
+  DBuf<int> flag(1);
+  SSB_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
+  diff_kernel<<<grid_for(ctx, a.rows + 1), kT, 0, ctx->stream>>>(a.rowptr.get(), b.rowptr.get(),
+                                                               a.rows + 1, flag.get());
+  ctx->check_launch("diff_kernel<ptr>");
+  if (a.nnz > 0) {
+    diff_kernel<<<grid_for(ctx, a.nnz), kT, 0, ctx->stream>>>(a.colidx.get(), b.colidx.get(),
+                                                             a.nnz, flag.get());
+    ctx->check_launch("diff_kernel<idx>");
+  }
+  return read_scalar(ctx, flag.get()) == 0;
+}
+
+void union_pattern(Matrix& a, Matrix& b, Matrix*& ua, Matrix*& ub) {
+  if (a.rows != b.rows || a.cols != b.cols) fail("union_pattern: shapes differ");
+  Context* ctx = a.ctx;
+  const std::int64_t rows = a.rows;
+  DBuf<int> cnt(rows + 1), ptr(rows + 1), ptr2(rows + 1);
+  SSB_CUDA(cudaMemsetAsync(cnt.get() + rows, 0, sizeof(int), ctx->stream));
+  union_rows_kernel<false><<<grid_for(ctx, rows), kT, 0, ctx->stream>>>(
+      a.rowptr.get(), a.colidx.get(), a.val.get(), b.rowptr.get(), b.colidx.get(), b.val.get(),
+      rows, cnt.get(), nullptr, nullptr, nullptr, nullptr);
+  ctx->check_launch("union_rows_kernel<count>");
+  counts_to_ptr(ctx, cnt.get(), ptr.get(), rows);
+  const int n = read_scalar(ctx, ptr.get() + rows);
+  DBuf<int> col(n), col2(n);
+  DBuf<double> va(n), vb(n);
+  union_rows_kernel<true><<<grid_for(ctx, rows), kT, 0, ctx->stream>>>(
+      a.rowptr.get(), a.colidx.get(), a.val.get(), b.rowptr.get(), b.colidx.get(), b.val.get(),
+      rows, nullptr, ptr.get(), col.get(), va.get(), vb.get());
+  ctx->check_launch("union_rows_kernel<fill>");
+  SSB_CUDA(cudaMemcpyAsync(ptr2.get(), ptr.get(), (rows + 1) * sizeof(int),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(col2.get(), col.get(), n * sizeof(int), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  ctx->sync();
+  ua = matrix_from_csr_device(ctx, rows, a.cols, n, std::move(ptr), std::move(col), std::move(va));
+  ub = matrix_from_csr_device(ctx, rows, a.cols, n, std::move(ptr2), std::move(col2),
+                              std::move(vb));
 }
 
 }  // namespace ssb

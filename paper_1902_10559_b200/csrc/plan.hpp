@@ -16,6 +16,8 @@ struct Plan {
   int uf_fwd = 2, uf_back = 2;  // load steps in flight per lane before the gathers
   int fwd_blocks = 0, back_blocks = 0;
   bool sharded = false;
+  bool paired = false;  // folded pair on one shared index stream
+  Matrix* pair_own[2] = {nullptr, nullptr};  // union-pattern copies (when patterns differ)
   bool stream = false;  // work-table kernels (mode 1 TMA ring, mode 2 flat stream)
   int mode = 0;
   int q_fwd = 4, q_back = 4;  // flat kernels: entries per lane per batch
@@ -37,6 +39,7 @@ struct Plan {
   DBuf<int> state;        // [nsys*nrhs][4] stopped, stop_it, diverged_at, -
   DBuf<unsigned> ticket;  // last-block ticket of the forward kernel
   DBuf<char> bp;          // sharded: back-projection + ||r||^2 slot (all-reduced)
+  DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;
@@ -48,6 +51,7 @@ struct Plan {
   void build_graph();
   void enqueue_iterations(int first, int count);  // raw launches (no graph)
   void enqueue_reset();
+  void enqueue_epilogue();  // paired: de-interleave x1/x2
   void set_rhs_host(int which, const double* p_slice_major);
   void set_rhs_device(int which, const void* p_dev);
   void set_rhs_device_f64(int which, const double* p_dev);  // [rows] fp64, nrhs == 1
@@ -61,6 +65,7 @@ struct Plan {
   void recombine(double* f_slice_major);
   void profile(int iters, float* fwd_ms, float* back_ms);
   void stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const;
+  void kernel_bytes(std::int64_t* fwd, std::int64_t* back) const;
 };
 
 Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs);

@@ -65,6 +65,8 @@ struct SartK {
   int* state;                   // [nsys*nrhs][4]
   unsigned* ticket;
   int sys_blocks[2];            // flat kernels: first CTA of system 1 (fwd, back)
+  T* xx;                        // paired plans: iterates interleaved [cols][2]
+  T* ww;                        //               weighted residuals [rows][2]
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
@@ -354,6 +356,213 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(S
   if (!sys_on(k.state, sys)) return;
   if (sys) back_cols<T, VS, UF, NA, 1>(k, group, ngroups, lane, mask, it);
   else back_cols<T, VS, UF, NA, 0>(k, group, ngroups, lane, mask, it);
+}
+
+// ------------------------------------------------------------ paired kernels
+// The fold puts A1 = TL - BL and A2 = TL + BL on the same buckets; a plan over
+// the folded pair streams ONE index array and two value arrays (the union
+// pattern, cancelled A1 entries as explicit zeros, which leaves every sum
+// unchanged) and gathers x1/x2 (w1/w2) together: 4 + 2b bytes per bucket
+// instead of 2(4 + b), and one pointer/epilogue chain per row for both systems.
+template <class T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+template <class T, int VS, int UF>
+__device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* __restrict__ va,
+                                         const T* __restrict__ vb,
+                                         const typename Vec2<T>::type* __restrict__ xv, int beg,
+                                         int end, int lane, unsigned mask, T& acc_a, T& acc_b) {
+  using T2 = typename Vec2<T>::type;
+  T sa = T(0), sb = T(0);
+  int a = (beg + 3) & ~3;
+  if (a > end) a = end;
+  const int nvec = (end - a) >> 2;
+  const int b = a + (nvec << 2);
+  const bool hon = beg + lane < a, ton = b + lane < end;
+  T ha = T(0), hb = T(0), ta = T(0), tb = T(0);
+  int hc = 0, tc = 0;
+  if (hon) {
+    hc = __ldg(idx + beg + lane);
+    ha = __ldg(va + beg + lane);
+    hb = __ldg(vb + beg + lane);
+  }
+  if (ton) {
+    tc = __ldg(idx + b + lane);
+    ta = __ldg(va + b + lane);
+    tb = __ldg(vb + b + lane);
+  }
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    int4 c[UF];
+    T v1[UF][4], v2[UF][4];
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = a + ((q + u * VS) << 2);
+      c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
+      load4(va + k0, v1[u]);
+      load4(vb + k0, v2[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const T2 g0 = __ldg(xv + c[u].x), g1 = __ldg(xv + c[u].y), g2 = __ldg(xv + c[u].z),
+               g3 = __ldg(xv + c[u].w);
+      sa += v1[u][0] * g0.x + v1[u][1] * g1.x + v1[u][2] * g2.x + v1[u][3] * g3.x;
+      sb += v2[u][0] * g0.y + v2[u][1] * g1.y + v2[u][2] * g2.y + v2[u][3] * g3.y;
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = a + (q << 2);
+    const int4 c0 = __ldg(reinterpret_cast<const int4*>(idx + k0));
+    T v1[4], v2[4];
+    load4(va + k0, v1);
+    load4(vb + k0, v2);
+    const T2 g0 = __ldg(xv + c0.x), g1 = __ldg(xv + c0.y), g2 = __ldg(xv + c0.z),
+             g3 = __ldg(xv + c0.w);
+    sa += v1[0] * g0.x + v1[1] * g1.x + v1[2] * g2.x + v1[3] * g3.x;
+    sb += v2[0] * g0.y + v2[1] * g1.y + v2[2] * g2.y + v2[3] * g3.y;
+  }
+  if (hon) {
+    const T2 g = __ldg(xv + hc);
+    sa += ha * g.x;
+    sb += hb * g.y;
+  }
+  if (ton) {
+    const T2 g = __ldg(xv + tc);
+    sa += ta * g.x;
+    sb += tb * g.y;
+  }
+#pragma unroll
+  for (int off = VS / 2; off > 0; off >>= 1) {
+    sa += __shfl_xor_sync(mask, sa, off, VS);
+    sb += __shfl_xor_sync(mask, sb, off, VS);
+  }
+  acc_a = sa;
+  acc_b = sb;
+}
+
+template <class T>
+struct PairCursor {
+  int i, beg, end;
+  T a1, a2, b1, b2;  // epilogue operands of system 0 (a) and 1 (b)
+};
+
+template <class T, bool FWD>
+__device__ __forceinline__ void fetch_pair(const SartK<T>& k, int i, int lane, PairCursor<T>& c) {
+  const int* ptr = FWD ? k.s[0].rp : k.s[0].cp;
+  c.i = i;
+  c.beg = __ldg(ptr + i);
+  c.end = __ldg(ptr + i + 1);
+  c.a1 = c.a2 = c.b1 = c.b2 = T(0);
+  if (lane == 0) {
+    if (FWD) {
+      c.a1 = k.s[0].p[i];
+      c.a2 = k.s[0].rinv[i];
+      c.b1 = k.s[1].p[i];
+      c.b2 = k.s[1].rinv[i];
+    } else {
+      c.a1 = k.xx[2 * i];
+      c.b1 = k.xx[2 * i + 1];
+      c.a2 = k.s[0].cinv[i];
+      c.b2 = k.s[1].cinv[i];
+    }
+  }
+}
+
+template <class T, int VS, int UF>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
+  using T2 = typename Vec2<T>::type;
+  __shared__ double red[2][kWarps];
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
+  const long long ngroups = (long long)gridDim.x * kThreads / VS;
+  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  const long long n = k.rows0;
+  const T2* __restrict__ xv = reinterpret_cast<const T2*>(k.xx);
+  T2* __restrict__ wv = reinterpret_cast<T2*>(k.ww);
+  double r2a = 0.0, r2b = 0.0;
+  if (on0 || on1) {
+    PairCursor<T> cur, nxt;
+    if (group < n) fetch_pair<T, true>(k, static_cast<int>(group), lane, cur);
+    for (long long g = group; g < n; g += ngroups) {
+      if (g + ngroups < n) fetch_pair<T, true>(k, static_cast<int>(g + ngroups), lane, nxt);
+      T da, db;
+      seg_dot2<T, VS, UF>(k.s[0].ci, k.s[0].rv, k.s[1].rv, xv, cur.beg, cur.end, lane, mask, da,
+                          db);
+      if (lane == 0) {
+        const T ra = cur.a1 - da, rb = cur.b1 - db;
+        T2 wo;
+        wo.x = on0 ? cur.a2 * ra : T(0);
+        wo.y = on1 ? cur.b2 * rb : T(0);
+        wv[cur.i] = wo;
+        if (on0) r2a += static_cast<double>(ra) * static_cast<double>(ra);
+        if (on1) r2b += static_cast<double>(rb) * static_cast<double>(rb);
+      }
+      cur = nxt;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r2a += __shfl_xor_sync(0xffffffffu, r2a, o);
+    r2b += __shfl_xor_sync(0xffffffffu, r2b, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][warp] = r2a;
+    red[1][warp] = r2b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
+    k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+  if (last_block(k.ticket)) {
+    finish_norms(k.partial, gridDim.x, 2, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
+template <class T, int VS, int UF>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
+  using T2 = typename Vec2<T>::type;
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
+  const long long ngroups = (long long)gridDim.x * kThreads / VS;
+  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  if (!on0 && !on1) return;
+  const long long n = k.cols0;
+  const T2* __restrict__ wv = reinterpret_cast<const T2*>(k.ww);
+  T2* __restrict__ xv = reinterpret_cast<T2*>(k.xx);
+  PairCursor<T> cur, nxt;
+  if (group < n) fetch_pair<T, false>(k, static_cast<int>(group), lane, cur);
+  for (long long g = group; g < n; g += ngroups) {
+    if (g + ngroups < n) fetch_pair<T, false>(k, static_cast<int>(g + ngroups), lane, nxt);
+    T ua, ub;
+    seg_dot2<T, VS, UF>(k.s[0].ri, k.s[0].cv, k.s[1].cv, wv, cur.beg, cur.end, lane, mask, ua,
+                        ub);
+    if (lane == 0) {
+      T2 xo;
+      xo.x = on0 ? upd(cur.a1, k.relax, ua, cur.a2) : cur.a1;
+      xo.y = on1 ? upd(cur.b1, k.relax, ub, cur.b2) : cur.b1;
+      xv[cur.i] = xo;
+      if (on0 && !isfinite(static_cast<double>(xo.x))) atomicCAS(&k.state[2], 0, it + 1);
+      if (on1 && !isfinite(static_cast<double>(xo.y))) atomicCAS(&k.state[4 + 2], 0, it + 1);
+    }
+    cur = nxt;
+  }
+}
+
+// x1, x2 of a paired plan out of the interleaved iterate (end of every solve)
+template <class T>
+__global__ void deinterleave_kernel(const T* xx, T* x1, T* x2, long long n) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    x1[j] = xx[2 * j];
+    x2[j] = xx[2 * j + 1];
+  }
 }
 
 // ------------------------------------------------------------ TMA-streamed kernels
@@ -1085,6 +1294,8 @@ SartK<T> make_args(Plan& P) {
   k.ticket = P.ticket.get();
   k.sys_blocks[0] = P.sys_blocks_f;
   k.sys_blocks[1] = P.sys_blocks_b;
+  k.xx = reinterpret_cast<T*>(P.xx.get());
+  k.ww = reinterpret_cast<T*>(P.ww.get());
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
@@ -1148,7 +1359,28 @@ void stream_attributes() {
 }
 
 template <class T>
+void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
+  const int vs = fwd ? P.vs_fwd : P.vs_back;
+  const int uf = fwd ? P.uf_fwd : P.uf_back;
+  const int blocks = fwd ? P.fwd_blocks : P.back_blocks;
+#define SSB_PAIR(V, U)                                                                     \
+  if (vs == V && uf == U) {                                                                \
+    if (fwd) sart_fwd_pair_kernel<T, V, U><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
+    else sart_back_pair_kernel<T, V, U><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
+    return;                                                                                \
+  }
+  SSB_PAIR(4, 2) SSB_PAIR(8, 2) SSB_PAIR(16, 2) SSB_PAIR(32, 2)
+  SSB_PAIR(4, 4) SSB_PAIR(8, 4) SSB_PAIR(16, 4) SSB_PAIR(32, 4)
+#undef SSB_PAIR
+  fail("plan: unsupported paired kernel shape");
+}
+
+template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
+  if (P.paired) {
+    launch_pair<T>(P, k, it, true);
+    return;
+  }
   if (P.stream) {
     launch_stream<T, true>(P, k, it);
     return;
@@ -1175,6 +1407,10 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
 
 template <class T>
 void launch_back(Plan& P, const SartK<T>& k, int it) {
+  if (P.paired) {
+    launch_pair<T>(P, k, it, false);
+    return;
+  }
   if (P.stream) {
     launch_stream<T, false>(P, k, it);
     return;
@@ -1215,6 +1451,22 @@ int occupancy_blocks(Plan& P, bool fwd) {
                                                             kThreads, 0);
   }
   SSB_CUDA(e);
+  return std::max(1, per_sm) * P.ctx->sm_count;
+}
+
+int occupancy_pair_blocks(Plan& P, bool fwd) {
+  int per_sm = 0;
+  if (P.dtype == SS_F32) {
+    SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                       &per_sm, sart_fwd_pair_kernel<float, 16, 2>, kThreads, 0)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                       &per_sm, sart_back_pair_kernel<float, 4, 2>, kThreads, 0));
+  } else {
+    SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                       &per_sm, sart_fwd_pair_kernel<double, 16, 2>, kThreads, 0)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                       &per_sm, sart_back_pair_kernel<double, 4, 2>, kThreads, 0));
+  }
   return std::max(1, per_sm) * P.ctx->sm_count;
 }
 
@@ -1267,12 +1519,15 @@ Plan::~Plan() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   delete own;
+  delete pair_own[0];
+  delete pair_own[1];
 }
 
 void Plan::enqueue_reset() {
   for (int s = 0; s < nsys; ++s) {
     SSB_CUDA(cudaMemsetAsync(x[s].get(), 0, cols[s] * nrhs * tsize(), ctx->stream));
   }
+  if (paired) SSB_CUDA(cudaMemsetAsync(xx.get(), 0, 2 * cols[0] * tsize(), ctx->stream));
   SSB_CUDA(cudaMemsetAsync(state.get(), 0, state.size() * sizeof(int), ctx->stream));
   SSB_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
 }
@@ -1280,6 +1535,21 @@ void Plan::enqueue_reset() {
 void Plan::enqueue_iterations(int first, int count) {
   if (dtype == SS_F32) do_iterations<float>(*this, first, count);
   else do_iterations<double>(*this, first, count);
+}
+
+void Plan::enqueue_epilogue() {
+  if (!paired) return;
+  const int g = grid1(ctx, cols[0]);
+  if (dtype == SS_F32) {
+    deinterleave_kernel<float><<<g, 256, 0, ctx->stream>>>(
+        reinterpret_cast<const float*>(xx.get()), reinterpret_cast<float*>(x[0].get()),
+        reinterpret_cast<float*>(x[1].get()), cols[0]);
+  } else {
+    deinterleave_kernel<double><<<g, 256, 0, ctx->stream>>>(
+        reinterpret_cast<const double*>(xx.get()), reinterpret_cast<double*>(x[0].get()),
+        reinterpret_cast<double*>(x[1].get()), cols[0]);
+  }
+  ctx->check_launch("deinterleave_kernel");
 }
 
 void Plan::build_graph() {
@@ -1290,6 +1560,7 @@ void Plan::build_graph() {
   try {
     enqueue_reset();
     enqueue_iterations(0, opts.max_iters);
+    enqueue_epilogue();
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -1305,10 +1576,11 @@ void Plan::launch() {
   SSB_CUDA(cudaEventRecord(ev0, ctx->stream));
   if (graph) {
     SSB_CUDA(cudaGraphLaunch(graph, ctx->stream));
-    ctx->launches += static_cast<std::int64_t>(2) * opts.max_iters;
+    ctx->launches += static_cast<std::int64_t>(2) * opts.max_iters + (paired ? 1 : 0);
   } else {
     enqueue_reset();
     enqueue_iterations(0, opts.max_iters);
+    enqueue_epilogue();
   }
   SSB_CUDA(cudaEventRecord(ev1, ctx->stream));
   launched = true;
@@ -1510,15 +1782,29 @@ void Plan::profile(int iters, float* fwd_ms, float* back_ms) {
   *back_ms = tb;
 }
 
-void Plan::stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const {
-  std::int64_t mb = 0, vb = 0;
+void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
+  // bytes of matrix data each kernel must stream per launch, in this plan's format
   const std::int64_t b = static_cast<std::int64_t>(tsize());
-  for (int s = 0; s < nsys; ++s) {
-    const std::int64_t nnz = a[s]->nnz;
-    mb += 2 * nnz * (b + 4) + 4 * ((rows[s] + 1) + (cols[s] + 1));
-    vb += (3 * rows[s] + 4 * cols[s]) * b * nrhs;
+  std::int64_t f = 0, k = 0;
+  if (paired) {
+    f = a[0]->nnz * (4 + 2 * b) + 4 * (rows[0] + 1);
+    k = a[0]->nnz * (4 + 2 * b) + 4 * (cols[0] + 1);
+  } else {
+    for (int s = 0; s < nsys; ++s) {
+      f += a[s]->nnz * (4 + b) + 4 * (rows[s] + 1);
+      k += a[s]->nnz * (4 + b) + 4 * (cols[s] + 1);
+    }
   }
-  if (mbytes) *mbytes = mb;
+  if (fwd) *fwd = f;
+  if (back) *back = k;
+}
+
+void Plan::stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const {
+  std::int64_t f = 0, k = 0, vb = 0;
+  kernel_bytes(&f, &k);
+  const std::int64_t b = static_cast<std::int64_t>(tsize());
+  for (int s = 0; s < nsys; ++s) vb += (3 * rows[s] + 4 * cols[s]) * b * nrhs;
+  if (mbytes) *mbytes = f + k;
   if (vbytes) *vbytes = vb;
   if (kernels) *kernels = 2;
 }
@@ -1533,6 +1819,12 @@ void alloc_common(Plan& P) {
     P.rinv[s].alloc(P.rows[s] * tb);
     P.cinv[s].alloc(P.cols[s] * tb);
     SSB_CUDA(cudaMemsetAsync(P.p[s].get(), 0, P.rows[s] * P.nrhs * tb, P.ctx->stream));
+  }
+  if (P.paired) {
+    P.xx.alloc(2 * P.cols[0] * tb);
+    P.ww.alloc(2 * P.rows[0] * tb);
+    SSB_CUDA(cudaMemsetAsync(P.xx.get(), 0, 2 * P.cols[0] * tb, P.ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(P.ww.get(), 0, 2 * P.rows[0] * tb, P.ctx->stream));
   }
   const int nsr = P.nsys * P.nrhs;
   P.partial.alloc(static_cast<std::size_t>(nsr) * P.fwd_blocks);
@@ -1695,9 +1987,24 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   P->a[1] = a2;
   double nnz_total = 0, rows_total = 0, cols_total = 0;
   PhaseTrace tr(ctx);
+  if (a2 && nrhs == 1 && env_int("SSB_PAIRED", 1) != 0) {
+    // one shared index stream for the folded pair (identical patterns unless
+    // the fold pruned cancellations; then the union with explicit zeros)
+    if (!same_pattern(*a1, *a2)) {
+      union_pattern(*a1, *a2, P->pair_own[0], P->pair_own[1]);
+      P->a[0] = P->pair_own[0];
+      P->a[1] = P->pair_own[1];
+    }
+    P->paired = true;
+    tr.mark("pair pattern");
+  }
   for (int s = 0; s < P->nsys; ++s) {
     Matrix* a = P->a[s];
-    a->ensure_csc();
+    if (P->paired && s == 1 && P->pair_own[1]) {
+      a->ensure_csc();  // same pattern as a[0]: the stable sort yields the same CSC order
+    } else {
+      a->ensure_csc();
+    }
     tr.mark("csc");
     if (o.dtype == SS_F32) a->ensure_f32();
     tr.mark("f32 copies");
@@ -1709,8 +2016,16 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   }
   P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(rows_total > 0 ? nnz_total / rows_total : 0));
   P->vs_back = env_int("SSB_VS_BACK", pick_vs(cols_total > 0 ? nnz_total / cols_total : 0));
-  P->uf_fwd = env_int("SSB_UF_FWD", 4);
-  P->uf_back = env_int("SSB_UF_BACK", 4);
+  if (P->paired) {
+    P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(nnz_total / std::max(rows_total, 1.0)));
+    P->vs_back = env_int("SSB_VS_BACK", pick_vs(nnz_total / std::max(cols_total, 1.0)));
+    P->uf_fwd = env_int("SSB_UF_FWD", 2);  // two value streams: half the steps in flight
+    P->uf_back = env_int("SSB_UF_BACK", 4);
+  }
+  if (!P->paired) {
+    P->uf_fwd = env_int("SSB_UF_FWD", 4);
+    P->uf_back = env_int("SSB_UF_BACK", 4);
+  }
   P->noalloc = env_int("SSB_NOALLOC", 0) != 0;
   if (o.dtype == SS_F32) {
     P->fwd_blocks = occupancy_blocks<float>(*P, true);
@@ -1728,7 +2043,14 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
       1, std::min<long long>(P->fwd_blocks, (fwd_groups + kThreads - 1) / kThreads)));
   P->back_blocks = static_cast<int>(std::max<long long>(
       1, std::min<long long>(P->back_blocks, (back_groups + kThreads - 1) / kThreads)));
-  if (nrhs == 1 && P->nsys == 2) {
+  if (P->paired) {
+    const long long fg = static_cast<long long>(P->rows[0]) * P->vs_fwd;
+    const long long bg = static_cast<long long>(P->cols[0]) * P->vs_back;
+    P->fwd_blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(
+        occupancy_pair_blocks(*P, true), (fg + kThreads - 1) / kThreads)));
+    P->back_blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(
+        occupancy_pair_blocks(*P, false), (bg + kThreads - 1) / kThreads)));
+  } else if (nrhs == 1 && P->nsys == 2) {
     // CTA-uniform systems: split the grid in proportion to each system's work
     const auto split = [&](int& blocks, double w0, double w1) {
       blocks = std::max(blocks, 2);

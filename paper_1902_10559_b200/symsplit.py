@@ -580,6 +580,11 @@ class SartPlan:
         _check(_lib().ss_plan_stats(self.h, C.byref(mb), C.byref(vb), C.byref(k)))
         return mb.value, vb.value, k.value
 
+    def kernel_bytes(self):
+        f, b = N.i64(), N.i64()
+        _check(_lib().ss_plan_kernel_bytes(self.h, C.byref(f), C.byref(b)))
+        return f.value, b.value
+
     def profile(self, iters):
         a, b = C.c_float(), C.c_float()
         _check(_lib().ss_plan_profile(self.h, iters, C.byref(a), C.byref(b)))
