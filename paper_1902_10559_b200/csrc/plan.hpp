@@ -40,6 +40,8 @@ struct Plan {
   DBuf<unsigned> ticket;  // last-block ticket of the forward kernel
   DBuf<char> bp;          // sharded: back-projection + ||r||^2 slot (all-reduced)
   DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
+  DBuf<char> rv2, cv2;    // paired: CSR / CSC values interleaved [nnz][2]
+  DBuf<char> pe, cc;      // paired: {p1,p2,rinv1,rinv2} per row, {cinv1,cinv2} per column
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;

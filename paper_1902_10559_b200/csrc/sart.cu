@@ -67,6 +67,10 @@ struct SartK {
   int sys_blocks[2];            // flat kernels: first CTA of system 1 (fwd, back)
   T* xx;                        // paired plans: iterates interleaved [cols][2]
   T* ww;                        //               weighted residuals [rows][2]
+  const T* rv2;                 //               CSR values interleaved [nnz][2]
+  const T* cv2;                 //               CSC values interleaved [nnz][2]
+  const T* pe;                  //               per row {p1, p2, rinv1, rinv2}
+  const T* cc;                  //               per column {cinv1, cinv2}
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
@@ -368,9 +372,25 @@ template <class T> struct Vec2;
 template <> struct Vec2<float> { using type = float2; };
 template <> struct Vec2<double> { using type = double2; };
 
+// 4 consecutive entries of the interleaved value stream: v[2q] (system 0),
+// v[2q+1] (system 1).
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p) + h);
+    v[2 * h] = a.x;
+    v[2 * h + 1] = a.y;
+  }
+}
+
 template <class T, int VS, int UF>
-__device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* __restrict__ va,
-                                         const T* __restrict__ vb,
+__device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* __restrict__ v2,
                                          const typename Vec2<T>::type* __restrict__ xv, int beg,
                                          int end, int lane, unsigned mask, T& acc_a, T& acc_b) {
   using T2 = typename Vec2<T>::type;
@@ -380,57 +400,54 @@ __device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* _
   const int nvec = (end - a) >> 2;
   const int b = a + (nvec << 2);
   const bool hon = beg + lane < a, ton = b + lane < end;
-  T ha = T(0), hb = T(0), ta = T(0), tb = T(0);
+  T2 hv, tv;
+  hv.x = hv.y = tv.x = tv.y = T(0);
   int hc = 0, tc = 0;
   if (hon) {
     hc = __ldg(idx + beg + lane);
-    ha = __ldg(va + beg + lane);
-    hb = __ldg(vb + beg + lane);
+    hv = __ldg(reinterpret_cast<const T2*>(v2) + beg + lane);
   }
   if (ton) {
     tc = __ldg(idx + b + lane);
-    ta = __ldg(va + b + lane);
-    tb = __ldg(vb + b + lane);
+    tv = __ldg(reinterpret_cast<const T2*>(v2) + b + lane);
   }
   int q = lane;
   for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
     int4 c[UF];
-    T v1[UF][4], v2[UF][4];
+    T v[UF][8];
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
       const int k0 = a + ((q + u * VS) << 2);
       c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
-      load4(va + k0, v1[u]);
-      load4(vb + k0, v2[u]);
+      load8(v2 + 2 * k0, v[u]);
     }
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
       const T2 g0 = __ldg(xv + c[u].x), g1 = __ldg(xv + c[u].y), g2 = __ldg(xv + c[u].z),
                g3 = __ldg(xv + c[u].w);
-      sa += v1[u][0] * g0.x + v1[u][1] * g1.x + v1[u][2] * g2.x + v1[u][3] * g3.x;
-      sb += v2[u][0] * g0.y + v2[u][1] * g1.y + v2[u][2] * g2.y + v2[u][3] * g3.y;
+      sa += v[u][0] * g0.x + v[u][2] * g1.x + v[u][4] * g2.x + v[u][6] * g3.x;
+      sb += v[u][1] * g0.y + v[u][3] * g1.y + v[u][5] * g2.y + v[u][7] * g3.y;
     }
   }
   for (; q < nvec; q += VS) {
     const int k0 = a + (q << 2);
     const int4 c0 = __ldg(reinterpret_cast<const int4*>(idx + k0));
-    T v1[4], v2[4];
-    load4(va + k0, v1);
-    load4(vb + k0, v2);
+    T v[8];
+    load8(v2 + 2 * k0, v);
     const T2 g0 = __ldg(xv + c0.x), g1 = __ldg(xv + c0.y), g2 = __ldg(xv + c0.z),
              g3 = __ldg(xv + c0.w);
-    sa += v1[0] * g0.x + v1[1] * g1.x + v1[2] * g2.x + v1[3] * g3.x;
-    sb += v2[0] * g0.y + v2[1] * g1.y + v2[2] * g2.y + v2[3] * g3.y;
+    sa += v[0] * g0.x + v[2] * g1.x + v[4] * g2.x + v[6] * g3.x;
+    sb += v[1] * g0.y + v[3] * g1.y + v[5] * g2.y + v[7] * g3.y;
   }
   if (hon) {
     const T2 g = __ldg(xv + hc);
-    sa += ha * g.x;
-    sb += hb * g.y;
+    sa += hv.x * g.x;
+    sb += hv.y * g.y;
   }
   if (ton) {
     const T2 g = __ldg(xv + tc);
-    sa += ta * g.x;
-    sb += tb * g.y;
+    sa += tv.x * g.x;
+    sb += tv.y * g.y;
   }
 #pragma unroll
   for (int off = VS / 2; off > 0; off >>= 1) {
@@ -439,34 +456,6 @@ __device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* _
   }
   acc_a = sa;
   acc_b = sb;
-}
-
-template <class T>
-struct PairCursor {
-  int i, beg, end;
-  T a1, a2, b1, b2;  // epilogue operands of system 0 (a) and 1 (b)
-};
-
-template <class T, bool FWD>
-__device__ __forceinline__ void fetch_pair(const SartK<T>& k, int i, int lane, PairCursor<T>& c) {
-  const int* ptr = FWD ? k.s[0].rp : k.s[0].cp;
-  c.i = i;
-  c.beg = __ldg(ptr + i);
-  c.end = __ldg(ptr + i + 1);
-  c.a1 = c.a2 = c.b1 = c.b2 = T(0);
-  if (lane == 0) {
-    if (FWD) {
-      c.a1 = k.s[0].p[i];
-      c.a2 = k.s[0].rinv[i];
-      c.b1 = k.s[1].p[i];
-      c.b2 = k.s[1].rinv[i];
-    } else {
-      c.a1 = k.xx[2 * i];
-      c.b1 = k.xx[2 * i + 1];
-      c.a2 = k.s[0].cinv[i];
-      c.b2 = k.s[1].cinv[i];
-    }
-  }
 }
 
 template <class T, int VS, int UF>
@@ -478,28 +467,39 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
-  const long long n = k.rows0;
-  const T2* __restrict__ xv = reinterpret_cast<const T2*>(k.xx);
-  T2* __restrict__ wv = reinterpret_cast<T2*>(k.ww);
+  const int n = static_cast<int>(k.rows0);
+  const int* __restrict__ ptr = k.s[0].rp;
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    PairCursor<T> cur, nxt;
-    if (group < n) fetch_pair<T, true>(k, static_cast<int>(group), lane, cur);
-    for (long long g = group; g < n; g += ngroups) {
-      if (g + ngroups < n) fetch_pair<T, true>(k, static_cast<int>(g + ngroups), lane, nxt);
+    int g = static_cast<int>(group);
+    int beg = 0, end = 0;
+    if (g < n) {
+      beg = __ldg(ptr + g);
+      end = __ldg(ptr + g + 1);
+    }
+    for (; g < n; g += static_cast<int>(ngroups)) {
+      const int gn = g + static_cast<int>(ngroups);
+      int nbeg = 0, nend = 0;
+      if (gn < n) {  // next row's bounds, ahead of this row's dot product
+        nbeg = __ldg(ptr + gn);
+        nend = __ldg(ptr + gn + 1);
+      }
+      T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
+      if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      seg_dot2<T, VS, UF>(k.s[0].ci, k.s[0].rv, k.s[1].rv, xv, cur.beg, cur.end, lane, mask, da,
-                          db);
+      seg_dot2<T, VS, UF>(k.s[0].ci, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
+                          mask, da, db);
       if (lane == 0) {
-        const T ra = cur.a1 - da, rb = cur.b1 - db;
+        const T ra = e[0] - da, rb = e[1] - db;
         T2 wo;
-        wo.x = on0 ? cur.a2 * ra : T(0);
-        wo.y = on1 ? cur.b2 * rb : T(0);
-        wv[cur.i] = wo;
+        wo.x = on0 ? e[2] * ra : T(0);
+        wo.y = on1 ? e[3] * rb : T(0);
+        reinterpret_cast<T2*>(k.ww)[g] = wo;
         if (on0) r2a += static_cast<double>(ra) * static_cast<double>(ra);
         if (on1) r2b += static_cast<double>(rb) * static_cast<double>(rb);
       }
-      cur = nxt;
+      beg = nbeg;
+      end = nend;
     }
   }
 #pragma unroll
@@ -533,25 +533,48 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   if (!on0 && !on1) return;
-  const long long n = k.cols0;
-  const T2* __restrict__ wv = reinterpret_cast<const T2*>(k.ww);
-  T2* __restrict__ xv = reinterpret_cast<T2*>(k.xx);
-  PairCursor<T> cur, nxt;
-  if (group < n) fetch_pair<T, false>(k, static_cast<int>(group), lane, cur);
-  for (long long g = group; g < n; g += ngroups) {
-    if (g + ngroups < n) fetch_pair<T, false>(k, static_cast<int>(g + ngroups), lane, nxt);
+  const int n = static_cast<int>(k.cols0);
+  const int* __restrict__ ptr = k.s[0].cp;
+  int g = static_cast<int>(group);
+  int beg = 0, end = 0;
+  if (g < n) {
+    beg = __ldg(ptr + g);
+    end = __ldg(ptr + g + 1);
+  }
+  for (; g < n; g += static_cast<int>(ngroups)) {
+    const int gn = g + static_cast<int>(ngroups);
+    int nbeg = 0, nend = 0;
+    if (gn < n) {
+      nbeg = __ldg(ptr + gn);
+      nend = __ldg(ptr + gn + 1);
+    }
+    T2 xo, ci;
+    xo.x = xo.y = ci.x = ci.y = T(0);
+    if (lane == 0) {  // {x1, x2} and {cinv1, cinv2}, issued before the dot
+      xo = reinterpret_cast<const T2*>(k.xx)[g];
+      ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
+    }
     T ua, ub;
-    seg_dot2<T, VS, UF>(k.s[0].ri, k.s[0].cv, k.s[1].cv, wv, cur.beg, cur.end, lane, mask, ua,
-                        ub);
+    seg_dot2<T, VS, UF>(k.s[0].ri, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane,
+                        mask, ua, ub);
     if (lane == 0) {
-      T2 xo;
-      xo.x = on0 ? upd(cur.a1, k.relax, ua, cur.a2) : cur.a1;
-      xo.y = on1 ? upd(cur.b1, k.relax, ub, cur.b2) : cur.b1;
-      xv[cur.i] = xo;
+      if (on0) xo.x = upd(xo.x, k.relax, ua, ci.x);
+      if (on1) xo.y = upd(xo.y, k.relax, ub, ci.y);
+      reinterpret_cast<T2*>(k.xx)[g] = xo;
       if (on0 && !isfinite(static_cast<double>(xo.x))) atomicCAS(&k.state[2], 0, it + 1);
       if (on1 && !isfinite(static_cast<double>(xo.y))) atomicCAS(&k.state[4 + 2], 0, it + 1);
     }
-    cur = nxt;
+    beg = nbeg;
+    end = nend;
+  }
+}
+
+// dst[stride*i + slot] = src[i] (building interleaved paired streams)
+template <class T, class S>
+__global__ void interleave_kernel(const S* src, T* dst, long long n, int stride, int slot) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    dst[stride * i + slot] = static_cast<T>(src[i]);
   }
 }
 
@@ -1296,6 +1319,10 @@ SartK<T> make_args(Plan& P) {
   k.sys_blocks[1] = P.sys_blocks_b;
   k.xx = reinterpret_cast<T*>(P.xx.get());
   k.ww = reinterpret_cast<T*>(P.ww.get());
+  k.rv2 = reinterpret_cast<const T*>(P.rv2.get());
+  k.cv2 = reinterpret_cast<const T*>(P.cv2.get());
+  k.pe = reinterpret_cast<const T*>(P.pe.get());
+  k.cc = reinterpret_cast<const T*>(P.cc.get());
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
@@ -1369,6 +1396,7 @@ void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
     else sart_back_pair_kernel<T, V, U><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
     return;                                                                                \
   }
+  SSB_PAIR(4, 1) SSB_PAIR(8, 1) SSB_PAIR(16, 1) SSB_PAIR(32, 1)
   SSB_PAIR(4, 2) SSB_PAIR(8, 2) SSB_PAIR(16, 2) SSB_PAIR(32, 2)
   SSB_PAIR(4, 4) SSB_PAIR(8, 4) SSB_PAIR(16, 4) SSB_PAIR(32, 4)
 #undef SSB_PAIR
@@ -1613,6 +1641,19 @@ void Plan::finish(ss_solve_report* rep) {
 
 void Plan::finish_rhs(int which) {
   double* pn = pnorm.get() + which * nrhs;
+  if (paired) {  // p of this system into slot `which` of the {p1, p2, rinv1, rinv2} records
+    const int g = grid1(ctx, rows[which]);
+    if (dtype == SS_F32) {
+      interleave_kernel<float, float><<<g, 256, 0, ctx->stream>>>(
+          reinterpret_cast<const float*>(p[which].get()), reinterpret_cast<float*>(pe.get()),
+          rows[which], 4, which);
+    } else {
+      interleave_kernel<double, double><<<g, 256, 0, ctx->stream>>>(
+          reinterpret_cast<const double*>(p[which].get()), reinterpret_cast<double*>(pe.get()),
+          rows[which], 4, which);
+    }
+    ctx->check_launch("interleave_kernel<p>");
+  }
   if (dtype == SS_F32) {
     pnorm_kernel<float><<<nrhs, kThreads, 0, ctx->stream>>>(
         reinterpret_cast<const float*>(p[which].get()), rows[which], nrhs, pn);
@@ -1969,6 +2010,43 @@ void setup_stream(Plan& P, int mode) {
 }
 }  // namespace
 
+namespace {
+template <class T>
+void build_paired_t(Plan& P) {
+  const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
+  const std::size_t tb = sizeof(T);
+  P.rv2.alloc(2 * nnz * tb);
+  P.cv2.alloc(2 * nnz * tb);
+  P.pe.alloc(4 * rows * tb);
+  P.cc.alloc(2 * cols * tb);
+  SSB_CUDA(cudaMemsetAsync(P.pe.get(), 0, 4 * rows * tb, P.ctx->stream));
+  T* rv2 = reinterpret_cast<T*>(P.rv2.get());
+  T* cv2 = reinterpret_cast<T*>(P.cv2.get());
+  const int gn = grid1(P.ctx, nnz), gr = grid1(P.ctx, rows), gc = grid1(P.ctx, cols);
+  for (int s = 0; s < 2; ++s) {
+    const T* rv = nullptr;
+    const T* cv = nullptr;
+    if constexpr (sizeof(T) == 4) {
+      rv = P.a[s]->val32.get();
+      cv = P.a[s]->cval32.get();
+    } else {
+      rv = P.a[s]->val.get();
+      cv = P.a[s]->cval.get();
+    }
+    interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(rv, rv2, nnz, 2, s);
+    interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(cv, cv2, nnz, 2, s);
+    interleave_kernel<T, T><<<gr, 256, 0, P.ctx->stream>>>(
+        reinterpret_cast<const T*>(P.rinv[s].get()), reinterpret_cast<T*>(P.pe.get()), rows, 4,
+        2 + s);
+    interleave_kernel<T, T><<<gc, 256, 0, P.ctx->stream>>>(
+        reinterpret_cast<const T*>(P.cinv[s].get()), reinterpret_cast<T*>(P.cc.get()), cols, 2,
+        s);
+    P.ctx->check_launch("interleave_kernel");
+  }
+  P.ctx->sync();
+}
+}  // namespace
+
 Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs) {
   if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
   if (o.max_iters < 1) fail("sart_solve: max_iters must be >= 1");
@@ -2019,8 +2097,8 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   if (P->paired) {
     P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(nnz_total / std::max(rows_total, 1.0)));
     P->vs_back = env_int("SSB_VS_BACK", pick_vs(nnz_total / std::max(cols_total, 1.0)));
-    P->uf_fwd = env_int("SSB_UF_FWD", 2);  // two value streams: half the steps in flight
-    P->uf_back = env_int("SSB_UF_BACK", 4);
+    P->uf_fwd = env_int("SSB_UF_FWD", 4);  // measured best for the paired streams
+    P->uf_back = env_int("SSB_UF_BACK", 2);
   }
   if (!P->paired) {
     P->uf_fwd = env_int("SSB_UF_FWD", 4);
@@ -2070,6 +2148,11 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->empty_rows[s] = !(mx > 0.0);
   }
   tr.mark("normalisers");
+  if (P->paired) {
+    if (o.dtype == SS_F32) build_paired_t<float>(*P);
+    else build_paired_t<double>(*P);
+    tr.mark("paired streams");
+  }
   if (P->nsys == 1 && P->empty_rows[0]) fail("sart_solve: matrix has no nonzero rows");
   P->build_graph();
   tr.mark("graph capture");
