@@ -1022,6 +1022,46 @@ __global__ void __launch_bounds__(kFlatThreads, 8)
 // Slices share A; X/W/P are [n][S] so one warp's 32 lanes read 32 consecutive
 // slices of a gathered row (coalesced 128 B for fp32) while the matrix entry
 // is loaded once per warp and broadcast: matrix bytes amortise over S.
+// One compressed vector against S slices: the warp loads 32 (index, value)
+// pairs coalesced, then broadcasts them 8 at a time so 8 independent
+// slice-row gathers (128 B each for fp32, S = 32) are in flight per lane.
+// Entries past `end` carry value 0 and index 0 (a harmless gather).
+template <class T, int SPL>
+__device__ __forceinline__ void multi_row_dot(const int* __restrict__ idx, const T* __restrict__ val,
+                                              const T* __restrict__ X, int beg, int end,
+                                              int lane, int S, T (&acc)[SPL]) {
+  for (int base = beg; base < end; base += 32) {
+    const int kk = base + lane;
+    const int c = kk < end ? __ldg(idx + kk) : 0;
+    const T v = kk < end ? __ldg(val + kk) : T(0);
+    const int cnt = min(32, end - base);
+    for (int e0 = 0; e0 < cnt; e0 += 8) {
+      int ce[8];
+      T ve[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        ce[u] = __shfl_sync(0xffffffffu, c, (e0 + u) & 31);
+        ve[u] = __shfl_sync(0xffffffffu, v, (e0 + u) & 31);
+        if (e0 + u >= cnt) {
+          ce[u] = 0;
+          ve[u] = T(0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < SPL; ++q) {
+        const int sl = lane + 32 * q;
+        if (sl < S) {
+          T g[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) g[u] = __ldg(X + static_cast<long long>(ce[u]) * S + sl);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[q] += ve[u] * g[u];
+        }
+      }
+    }
+  }
+}
+
 template <class T, int SPL>
 __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, int it) {
   extern __shared__ double mred[];  // [kWarps][nsys*S]
@@ -1046,22 +1086,7 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
 #pragma unroll
     for (int q = 0; q < SPL; ++q) acc[q] = T(0);
     const int beg = Sy.rp[i], end = Sy.rp[i + 1];
-    for (int base = beg; base < end; base += 32) {
-      const int kk = base + lane;
-      const int c = kk < end ? __ldg(Sy.ci + kk) : 0;
-      const T v = kk < end ? __ldg(Sy.rv + kk) : T(0);
-      const int cnt = min(32, end - base);
-      for (int e = 0; e < cnt; ++e) {
-        const int ce = __shfl_sync(0xffffffffu, c, e);
-        const T ve = __shfl_sync(0xffffffffu, v, e);
-        const T* xr = Sy.x + static_cast<long long>(ce) * S;
-#pragma unroll
-        for (int q = 0; q < SPL; ++q) {
-          const int sl = lane + 32 * q;
-          if (sl < S) acc[q] += ve * __ldg(xr + sl);
-        }
-      }
-    }
+    multi_row_dot<T, SPL>(Sy.ci, Sy.rv, Sy.x, beg, end, lane, S, acc);
     const T ri = Sy.rinv[i];
 #pragma unroll
     for (int q = 0; q < SPL; ++q) {
@@ -1118,22 +1143,7 @@ __global__ void __launch_bounds__(kThreads) sart_back_multi_kernel(SartK<T> k, i
 #pragma unroll
     for (int q = 0; q < SPL; ++q) acc[q] = T(0);
     const int beg = Sy.cp[j], end = Sy.cp[j + 1];
-    for (int base = beg; base < end; base += 32) {
-      const int kk = base + lane;
-      const int r = kk < end ? __ldg(Sy.ri + kk) : 0;
-      const T v = kk < end ? __ldg(Sy.cv + kk) : T(0);
-      const int cnt = min(32, end - base);
-      for (int e = 0; e < cnt; ++e) {
-        const int re = __shfl_sync(0xffffffffu, r, e);
-        const T ve = __shfl_sync(0xffffffffu, v, e);
-        const T* wr = Sy.w + static_cast<long long>(re) * S;
-#pragma unroll
-        for (int q = 0; q < SPL; ++q) {
-          const int sl = lane + 32 * q;
-          if (sl < S) acc[q] += ve * __ldg(wr + sl);
-        }
-      }
-    }
+    multi_row_dot<T, SPL>(Sy.ri, Sy.cv, Sy.w, beg, end, lane, S, acc);
     const T ci = Sy.cinv[j];
 #pragma unroll
     for (int q = 0; q < SPL; ++q) {
