@@ -63,13 +63,18 @@ typedef struct {
   double voxel_size, center_x, y_bottom;
 } ss_grid_spec;
 
-/* replaces SolveOptions (solvers.hpp:19-27); method is always SART here */
+/* iterative methods on the device (reference Method, solvers.hpp:14) */
+#define SS_METHOD_SART 0
+#define SS_METHOD_CGLS 1
+
+/* replaces SolveOptions (solvers.hpp:19-27) */
 typedef struct {
   int max_iters;      /* default 200                           */
-  double tol;         /* default 1e-10; 0 = fixed iteration count */
-  double relaxation;  /* default 1.0, in (0, 2]                */
+  double tol;         /* default 1e-10; 0 = fixed iteration count (SART) */
+  double relaxation;  /* default 1.0, in (0, 2] (SART only)    */
   int parallelism;    /* accepted for parity; results never depend on it */
   int dtype;          /* SS_F64 (reference) or SS_F32          */
+  int method;         /* SS_METHOD_SART (default) or SS_METHOD_CGLS */
 } ss_solve_options;
 
 /* replaces SolveReport scalars (solvers.hpp:29-45) */
@@ -166,11 +171,15 @@ int ss_recombine_solution(ss_ctx_t ctx, const double* f1, const double* f2, int6
  * for max_iters + 1 entries. */
 int ss_sart_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
                   double* f, int64_t n, ss_solve_report* report, double* history);
-/* replaces solve_split (solvers.cpp:207-269) with method = sart */
+/* replaces cgls_solve (solvers.cpp:99-146); history may be NULL, else room
+ * for max_iters entries */
+int ss_cgls_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
+                  double* f, int64_t n, ss_solve_report* report, double* history);
+/* replaces solve_split (solvers.cpp:207-269) with method = sart or cgls */
 int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_tol,
                    const ss_solve_options* opts, double* f, int64_t n,
                    ss_solve_report* report);
-/* replaces solve_direct (solvers.cpp:201-205) with method = sart */
+/* replaces solve_direct (solvers.cpp:201-205) with method = sart or cgls */
 int ss_solve_direct(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
                     double* f, int64_t n, ss_solve_report* report);
 

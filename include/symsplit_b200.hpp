@@ -234,8 +234,11 @@ struct SolveReport {
 
 namespace detail {
 inline ss_solve_options to_c(const SolveOptions& o) {
-  if (o.method != Method::sart) throw Error("only Method::sart runs on the B200 path");
-  return ss_solve_options{o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype};
+  if (o.method == Method::dense_minnorm) {
+    throw Error("Method::dense_minnorm is not on the B200 path (use sart or cgls)");
+  }
+  return ss_solve_options{o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype,
+                          o.method == Method::cgls ? SS_METHOD_CGLS : SS_METHOD_SART};
 }
 inline SolveReport from_c(Vector f, const ss_solve_report& r, Mode mode) {
   SolveReport rep;
@@ -320,8 +323,25 @@ inline SolveReport sart_solve(const Matrix& a, const Vector& p, const SolveOptio
   return rep;
 }
 
+// reference solvers.cpp:99-146
+inline SolveReport cgls_solve(const Matrix& a, const Vector& p, const SolveOptions& opts) {
+  SolveOptions o = opts;
+  o.method = Method::cgls;
+  const ss_solve_options c = detail::to_c(o);
+  Vector f(static_cast<std::size_t>(a.cols()));
+  Vector hist(static_cast<std::size_t>(opts.max_iters > 0 ? opts.max_iters + 1 : 1));
+  ss_solve_report r{};
+  detail::check(ss_cgls_solve(a.get(), p.data(), static_cast<int64_t>(p.size()), &c, f.data(),
+                              static_cast<int64_t>(f.size()), &r, hist.data()));
+  SolveReport rep = detail::from_c(std::move(f), r, Mode::direct);
+  rep.method = Method::cgls;
+  rep.residual_history.assign(hist.begin(), hist.begin() + r.history_len);
+  return rep;
+}
+
 inline SolveReport solve_direct(const CentroSystem& sys, const SolveOptions& opts) {
-  return sart_solve(sys.a, sys.p, opts);
+  return opts.method == Method::cgls ? cgls_solve(sys.a, sys.p, opts)
+                                     : sart_solve(sys.a, sys.p, opts);
 }
 
 inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts) {
@@ -331,7 +351,9 @@ inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts
   detail::check(ss_solve_split(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
                                sys.symmetry_tol, &o, f.data(), static_cast<int64_t>(f.size()),
                                &r));
-  return detail::from_c(std::move(f), r, Mode::split);
+  SolveReport rep = detail::from_c(std::move(f), r, Mode::split);
+  rep.method = opts.method;
+  return rep;
 }
 
 // ------------------------------------------------------------------ geometry

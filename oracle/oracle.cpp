@@ -1152,9 +1152,63 @@ SolveReport sart_solve(const Matrix& a, const Vector& p, const SolveOptions& opt
   return rep;
 }
 
-// src/solvers.cpp:201-205 (method = sart)
+// src/solvers.cpp:99-146
+SolveReport cgls_solve(const Matrix& a, const Vector& p, const SolveOptions& opts) {
+  check_system(a, p, "cgls_solve");
+  if (opts.tol <= 0) throw Error("cgls_solve: tol must be positive");
+  if (opts.max_iters < 1) throw Error("cgls_solve: max_iters must be >= 1");
+  SolveReport rep;
+  const auto t0 = Clock::now();
+  const Index m = a.rows(), n = a.cols();
+  Vector x(static_cast<std::size_t>(n), 0.0);
+  Vector r = p;
+  Vector s = a.apply_transpose(r);
+  Vector d = s;
+  double gamma = squared_norm(s);
+  const double stop = opts.tol * std::sqrt(gamma);
+  int it = 0;
+  while (it < opts.max_iters && std::sqrt(gamma) > stop) {
+    const Vector q = a.apply(d);
+    const double qq = squared_norm(q);
+    if (qq == 0.0) break;
+    const double alpha = gamma / qq;
+    if (!std::isfinite(alpha)) {
+      throw Error("cgls_solve: diverged (non-finite step at iteration " + std::to_string(it + 1) +
+                  ")");
+    }
+    for (Index j = 0; j < n; ++j) x[j] += alpha * d[j];
+    for (Index i = 0; i < m; ++i) r[i] -= alpha * q[i];
+    s = a.apply_transpose(r);
+    const double gamma_new = squared_norm(s);
+    if (!std::isfinite(gamma_new)) {
+      throw Error("cgls_solve: diverged (non-finite residual at iteration " +
+                  std::to_string(it + 1) + ")");
+    }
+    const double beta = gamma_new / gamma;
+    for (Index j = 0; j < n; ++j) d[j] = s[j] + beta * d[j];
+    gamma = gamma_new;
+    ++it;
+    rep.residual_history.push_back(norm(r));
+  }
+  rep.f = std::move(x);
+  rep.iterations = it;
+  rep.wall_time_seconds = seconds_since(t0);
+  const Vector af = a.apply(rep.f);
+  Vector rr(static_cast<std::size_t>(m));
+  for (Index i = 0; i < m; ++i) rr[i] = af[i] - p[i];
+  rep.residual_norm = norm(rr);
+  rep.solution_norm = norm(rep.f);
+  return rep;
+}
+
+// src/solvers.cpp:38-57 (iterative methods)
+SolveReport run_method(const Matrix& a, const Vector& p, const SolveOptions& o) {
+  return o.method == Method::cgls ? cgls_solve(a, p, o) : sart_solve(a, p, o);
+}
+
+// src/solvers.cpp:201-205
 SolveReport solve_direct_sart(const CentroSystem& sys, const SolveOptions& o) {
-  return sart_solve(sys.a, sys.p, o);
+  return run_method(sys.a, sys.p, o);
 }
 
 SolveReport solve_split_prepared(const SplitSystem& ss, const SolveOptions& opts,
@@ -1165,7 +1219,7 @@ SolveReport solve_split_prepared(const SplitSystem& ss, const SolveOptions& opts
     try {
       const Matrix& a = which == 0 ? ss.a1 : ss.a2;
       const Vector& p = which == 0 ? ss.p1 : ss.p2;
-      branch[which] = sart_solve(a, p, opts);
+      branch[which] = run_method(a, p, opts);
     } catch (...) {
       errors[which] = std::current_exception();
     }

@@ -270,7 +270,10 @@ class Rng {
 };
 
 // ---------------------------------------------------------------- solvers
+enum class Method { sart, cgls };
+
 struct SolveOptions {
+  Method method = Method::sart;
   int max_iters = 200;
   double tol = 1e-10;
   double relaxation = 1.0;
@@ -289,6 +292,8 @@ struct SolveReport {
 };
 
 SolveReport sart_solve(const Matrix& a, const Vector& p, const SolveOptions& o);
+SolveReport cgls_solve(const Matrix& a, const Vector& p, const SolveOptions& o);
+SolveReport run_method(const Matrix& a, const Vector& p, const SolveOptions& o);
 SolveReport solve_direct_sart(const CentroSystem& sys, const SolveOptions& o);
 SolveReport solve_split_sart(const CentroSystem& sys, const SolveOptions& o);
 // Same loop on an already folded pair (the part the reference times as

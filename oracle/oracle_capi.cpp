@@ -295,6 +295,41 @@ int or_sart_solve(void* m, const double* p, std::int64_t plen, int max_iters, do
   });
 }
 
+int or_cgls_solve(void* m, const double* p, std::int64_t plen, int max_iters, double tol,
+                  double* f, int* iters, double* resnorm, double* solnorm, double* hist,
+                  int* hist_len) {
+  return guarded([&] {
+    SolveOptions o;
+    o.method = Method::cgls;
+    o.max_iters = max_iters;
+    o.tol = tol;
+    SolveReport r = cgls_solve(*static_cast<Matrix*>(m), vec(p, plen), o);
+    put(r.f, f);
+    *iters = r.iterations;
+    *resnorm = r.residual_norm;
+    *solnorm = r.solution_norm;
+    if (hist) std::memcpy(hist, r.residual_history.data(), r.residual_history.size() * 8);
+    *hist_len = static_cast<int>(r.residual_history.size());
+  });
+}
+
+int or_solve_split_method(void* m, const double* p, std::int64_t plen, double sym_tol,
+                          int method, int max_iters, double tol, double relax, double* f,
+                          int* iters, double* resnorm) {
+  return guarded([&] {
+    SolveOptions o;
+    o.method = method == 1 ? Method::cgls : Method::sart;
+    o.max_iters = max_iters;
+    o.tol = tol;
+    o.relaxation = relax;
+    CentroSystem sys{*static_cast<Matrix*>(m), vec(p, plen), sym_tol};
+    SolveReport r = solve_split_sart(sys, o);
+    put(r.f, f);
+    *iters = r.iterations;
+    *resnorm = r.residual_norm;
+  });
+}
+
 int or_solve_split(void* m, const double* p, std::int64_t plen, double sym_tol, int max_iters,
                    double tol, double relax, int parallelism, double* f, int* iters,
                    double* resnorm, double* solnorm, double* wall, double* times4) {

@@ -346,6 +346,27 @@ def sart_solve(a: Matrix, p, max_iters=200, tol=1e-10, relaxation=1.0) -> SolveR
     return SolveReport(f, it.value, rn.value, sn.value, wall.value, hist[:hl.value].copy())
 
 
+def cgls_solve(a: Matrix, p, max_iters=200, tol=1e-10) -> SolveReport:
+    p = f64(p)
+    f = np.empty(a.shape[1])
+    hist = np.empty(max_iters + 1)
+    it, rn, sn, hl = C.c_int(), C.c_double(), C.c_double(), C.c_int()
+    _check(lib().or_cgls_solve(a.h, _d(p), _i64(len(p)), max_iters, C.c_double(tol), _d(f),
+                               C.byref(it), C.byref(rn), C.byref(sn), _d(hist), C.byref(hl)))
+    return SolveReport(f, it.value, rn.value, sn.value, 0.0, hist[:hl.value].copy())
+
+
+def solve_split_method(a: Matrix, p, method="cgls", symmetry_tol=1e-12, max_iters=200,
+                       tol=1e-10, relaxation=1.0):
+    p = f64(p)
+    f = np.empty(a.shape[1])
+    it, rn = C.c_int(), C.c_double()
+    _check(lib().or_solve_split_method(a.h, _d(p), _i64(len(p)), C.c_double(symmetry_tol),
+                                       1 if method == "cgls" else 0, max_iters, C.c_double(tol),
+                                       C.c_double(relaxation), _d(f), C.byref(it), C.byref(rn)))
+    return f, it.value, rn.value
+
+
 def solve_split(a: Matrix, p, symmetry_tol=1e-12, max_iters=200, tol=1e-10, relaxation=1.0,
                 parallelism=0) -> SolveReport:
     p = f64(p)

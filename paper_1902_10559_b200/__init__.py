@@ -6,6 +6,7 @@ is its Python mirror of the reference API. No CPU fallback exists.
 """
 from .symsplit import (  # noqa: F401
     CentroSystem, Context, DeviceError, Error, Matrix, SartPlan, SolutionPair, SolveOptions,
+    cgls_solve,
     SolveReport, SplitSystem, SymmetryError, SymmetryReport, SymsplitError, build_system,
     decompose_solution, default_context, degrees_to_radians, enumerate_rays, forward_project,
     make_grid, parse_scan_config, random_ellipses, rasterize, recombine_solution, sart_solve,

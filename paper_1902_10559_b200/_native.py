@@ -40,7 +40,7 @@ class GridSpec(C.Structure):
 
 class SolveOptionsC(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("tol", C.c_double), ("relaxation", C.c_double),
-                ("parallelism", C.c_int), ("dtype", C.c_int)]
+                ("parallelism", C.c_int), ("dtype", C.c_int), ("method", C.c_int)]
 
 
 class SolveReportC(C.Structure):
@@ -91,6 +91,8 @@ SIGNATURES = {
     "ss_decompose_solution": (C.c_int, [vp, dp, i64, dp, dp]),
     "ss_recombine_solution": (C.c_int, [vp, dp, dp, i64, dp]),
     "ss_sart_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
+                                C.POINTER(SolveReportC), dp]),
+    "ss_cgls_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
                                 C.POINTER(SolveReportC), dp]),
     "ss_solve_split": (C.c_int, [vp, dp, i64, C.c_double, C.POINTER(SolveOptionsC), dp, i64,
                                  C.POINTER(SolveReportC)]),

@@ -197,6 +197,7 @@ void ss_default_options(ss_solve_options* o) {
   o->relaxation = 1.0;
   o->parallelism = 0;
   o->dtype = SS_F64;
+  o->method = SS_METHOD_SART;
 }
 
 int ss_device_count(int* out) {
@@ -508,8 +509,28 @@ int ss_sart_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_opti
   });
 }
 
+int ss_cgls_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
+                  double* f, int64_t n, ss_solve_report* report, double* history) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    need(opts, "opts");
+    check_system(A->rows, p, m, "cgls_solve");
+    if (n != A->cols) ssb::fail("cgls_solve: solution length does not match columns");
+    auto dp = to_device(c, p, m);
+    ssb::DBuf<double> fd(n);
+    ss_solve_report rep{};
+    ssb::cgls_device(*A, dp.get(), *opts, fd.get(), &rep, history);
+    to_host(c, f, fd.get(), n);
+    fill_report(*A, fd.get(), dp.get(), &rep);
+    if (report) *report = rep;
+  });
+}
+
 int ss_solve_direct(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
                     double* f, int64_t n, ss_solve_report* report) {
+  if (opts && opts->method == SS_METHOD_CGLS) return ss_cgls_solve(a, p, m, opts, f, n, report, nullptr);
   return ss_sart_solve(a, p, m, opts, f, n, report, nullptr);
 }
 
@@ -544,17 +565,57 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     };
     const std::int64_t mh = m / 2;
     std::vector<double> hp(static_cast<std::size_t>(mh));
+    const bool cgls = opts->method == SS_METHOD_CGLS;
     for (int s = 0; s < 2; ++s) {
       to_host(c, hp.data(), (s ? o.p2 : o.p1).get(), mh);
       try {
-        check_system(o.a1->rows, hp.data(), mh, "sart_solve");
-        check_options(*opts);
+        check_system(o.a1->rows, hp.data(), mh, cgls ? "cgls_solve" : "sart_solve");
+        if (cgls) {
+          if (opts->tol <= 0) ssb::fail("cgls_solve: tol must be positive");
+          if (opts->max_iters < 1) ssb::fail("cgls_solve: max_iters must be >= 1");
+        } else {
+          check_options(*opts);
+        }
       } catch (const ssb::Failure& e) {
         errs[s] = e.what();
       }
     }
     raise_if_failed(SS_ERR_INVALID);
     tr.mark("branch validation");
+    if (cgls) {
+      // both branches on the device, failures aggregated like the reference
+      ssb::DBuf<double> f1(n / 2), f2(n / 2);
+      ss_solve_report rb[2] = {};
+      int code = SS_OK;
+      for (int s = 0; s < 2; ++s) {
+        try {
+          ssb::cgls_device(s ? *o.a2 : *o.a1, (s ? o.p2 : o.p1).get(), *opts,
+                           (s ? f2 : f1).get(), &rb[s], nullptr);
+        } catch (const ssb::Failure& e) {
+          errs[s] = e.what();
+          code = e.code;
+        }
+      }
+      raise_if_failed(code == SS_OK ? SS_ERR_INVALID : code);
+      const double t_rec0 = now();
+      if (!ssb::all_finite_dev(c, f1.get(), n / 2) || !ssb::all_finite_dev(c, f2.get(), n / 2)) {
+        ssb::fail("recombine_solution: non-finite component");
+      }
+      ssb::DBuf<double> fd(n);
+      ssb::recombine_dev(c, f1.get(), f2.get(), fd.get(), n / 2, 1);
+      to_host(c, f, fd.get(), n);
+      ss_solve_report rep{};
+      rep.recombine_seconds = now() - t_rec0;
+      fill_report(*A, fd.get(), dp.get(), &rep);
+      rep.iterations = std::max(rb[0].iterations, rb[1].iterations);
+      rep.branch1_seconds = rb[0].wall_time_seconds;
+      rep.branch2_seconds = rb[1].wall_time_seconds;
+      rep.split_seconds = split_seconds;
+      rep.wall_time_seconds = split_seconds + rep.branch1_seconds + rep.branch2_seconds +
+                              rep.recombine_seconds;
+      if (report) *report = rep;
+      return;
+    }
     std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1));
     tr.mark("plan (csc, norms, graph)");
     for (int s = 0; s < 2; ++s) {

@@ -218,6 +218,9 @@ double max_dev(Context* ctx, const double* v, std::int64_t n);
 bool all_finite_dev(Context* ctx, const double* v, std::int64_t n);
 void rasterize_dev(Context* ctx, const double* ell6, int count, const Grid& g, double* out);
 void forward_project_dev(Matrix& a, const double* f, double* p);
+// CGLS (cgls.cu): f_dev receives x in fp64; report gets iterations/history/time
+void cgls_device(Matrix& a, const double* p_dev, const ss_solve_options& o, double* f_dev,
+                 ss_solve_report* rep, double* hist_host);
 
 template <class T>
 void cast_dev(Context* ctx, const double* src, T* dst, std::int64_t n);

@@ -301,14 +301,16 @@ class SolveOptions:
     method: str = "sart"
 
     def _c(self):
-        if self.method != "sart":
+        if self.method not in ("sart", "cgls"):
+            # solvers.cpp:28-33 method_from_name; dense min-norm is not on the B200 path
             raise Error(f"unknown method name: {self.method}" if self.method not in
-                        ("dense", "dense_minnorm", "cgls") else
+                        ("dense", "dense_minnorm") else
                         f"method {self.method} is not on the B200 path")
         if self.dtype not in ("f64", "f32"):
             raise Error("dtype must be 'f64' or 'f32'")
         return N.SolveOptionsC(int(self.max_iters), float(self.tol), float(self.relaxation),
-                               int(self.parallelism), N.SS_F64 if self.dtype == "f64" else N.SS_F32)
+                               int(self.parallelism), N.SS_F64 if self.dtype == "f64" else N.SS_F32,
+                               1 if self.method == "cgls" else 0)
 
 
 @dataclass
@@ -406,8 +408,27 @@ def sart_solve(a: Matrix, p, opts: Optional[SolveOptions] = None) -> SolveReport
     return _report(f, r, "direct", hist[:r.history_len])
 
 
+def cgls_solve(a: Matrix, p, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """solvers.cpp:99-146 on the device."""
+    opts = opts or SolveOptions(method="cgls")
+    p = _f64(p)
+    rows, cols = a.shape
+    f = np.empty(cols)
+    hist = np.empty(int(opts.max_iters) + 1)
+    r = N.SolveReportC()
+    o = opts._c()
+    _check(_lib().ss_cgls_solve(a.h, _dp(p), len(p), C.byref(o), _dp(f), cols, C.byref(r),
+                                _dp(hist)))
+    rep = _report(f, r, "direct", hist[:r.history_len])
+    rep.method = "cgls"
+    return rep
+
+
 def solve_direct(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> SolveReport:
-    """solvers.cpp:201-205 (method = sart)"""
+    """solvers.cpp:201-205 (method = sart or cgls)"""
+    opts = opts or SolveOptions()
+    if opts.method == "cgls":
+        return cgls_solve(sys.a, sys.p, opts)
     return sart_solve(sys.a, sys.p, opts)
 
 
@@ -421,7 +442,9 @@ def solve_split(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> Solve
     o = opts._c()
     _check(_lib().ss_solve_split(sys.a.h, _dp(p), len(p), C.c_double(sys.symmetry_tol),
                                  C.byref(o), _dp(f), cols, C.byref(r)))
-    return _report(f, r, "split")
+    rep = _report(f, r, "split")
+    rep.method = opts.method
+    return rep
 
 
 # ----------------------------------------------------------------- geometry
