@@ -34,6 +34,7 @@ extern "C" {
 #define SS_ERR_CUDA 4      /* CUDA runtime failure                            */
 #define SS_ERR_NCCL 5      /* NCCL failure                                    */
 #define SS_ERR_OOM 6       /* device allocation failed                        */
+#define SS_ERR_IO 7        /* symsplit::IoError (io.hpp:14-20)                 */
 
 /* arithmetic type of a SART plan */
 #define SS_F64 0
@@ -194,6 +195,16 @@ int ss_rasterize(ss_ctx_t ctx, const double* ellipses6, int count, const ss_grid
 int ss_forward_project(ss_matrix_t a, const double* f, double* p);
 /* replaces the seeded noise of forward_project (phantom.cpp:129-149); host */
 int ss_add_noise(double* p, int64_t m, double sigma, uint64_t seed);
+
+/* ------------------------------------------------------------ file formats (ingestion) */
+/* replaces read_matrix_market (io.cpp:83-187): validated, sorted, no duplicates */
+int ss_read_matrix_market(ss_ctx_t ctx, const char* path, ss_matrix_t* out);
+/* replaces write_matrix_market (io.cpp:189-210): canonical order, %.17g */
+int ss_write_matrix_market(ss_matrix_t a, const char* path);
+/* replaces read_vector_csv (io.cpp:212-230); pass values = NULL to query the length */
+int ss_read_vector_csv(const char* path, double* values, int64_t capacity, int64_t* count);
+/* replaces write_vector_csv (io.cpp:232-238) */
+int ss_write_vector_csv(const char* path, const double* values, int64_t count);
 
 /* ------------------------------------------------------------ plans (device-resident loop) */
 /* A prepared SART over one system (a2 == NULL) or the folded pair (a1, a2),

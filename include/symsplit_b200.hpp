@@ -53,6 +53,12 @@ class SymmetryError : public Error {
   SymmetryReport report;
 };
 
+// reference io.hpp:14-20 (path/line are part of the message here)
+class IoError : public Error {
+ public:
+  using Error::Error;
+};
+
 namespace detail {
 inline SymmetryReport to_report(const ss_symmetry_report& r) {
   return SymmetryReport{r.holds != 0, r.max_violation, r.worst_row, r.worst_col,
@@ -64,6 +70,7 @@ inline void check(int rc, const ss_symmetry_report* rep = nullptr) {
   if (rc == SS_ERR_SYMMETRY) {
     throw SymmetryError(msg, rep ? to_report(*rep) : SymmetryReport{});
   }
+  if (rc == SS_ERR_IO) throw IoError(msg);
   throw Error(msg);
 }
 }  // namespace detail
@@ -348,9 +355,17 @@ inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts
   const ss_solve_options o = detail::to_c(opts);
   Vector f(static_cast<std::size_t>(sys.a.cols()));
   ss_solve_report r{};
-  detail::check(ss_solve_split(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
-                               sys.symmetry_tol, &o, f.data(), static_cast<int64_t>(f.size()),
-                               &r));
+  const int rc = ss_solve_split(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
+                                sys.symmetry_tol, &o, f.data(), static_cast<int64_t>(f.size()),
+                                &r);
+  if (rc == SS_ERR_SYMMETRY) {
+    // the SymmetryError carries its report (reference centro.cpp:144-156)
+    const std::string msg = ss_last_error();
+    ss_symmetry_report sr{};
+    ss_verify_symmetry(sys.a.get(), sys.symmetry_tol, &sr);
+    throw SymmetryError(msg, detail::to_report(sr));
+  }
+  detail::check(rc);
   SolveReport rep = detail::from_c(std::move(f), r, Mode::split);
   rep.method = opts.method;
   return rep;
@@ -389,6 +404,50 @@ inline CentroSystem build_system(const ScanConfig& cfg, int parallelism = 0,
   CentroSystem sys{Matrix(h), {}, 0.0};
   sys.p.assign(static_cast<std::size_t>(sys.a.rows()), 0.0);
   return sys;
+}
+
+// ------------------------------------------------------------------ file formats
+// reference io.hpp:22-36
+inline Matrix read_matrix_market(const std::string& path,
+                                 const Context& ctx = Context::default_context()) {
+  ss_matrix_t h = nullptr;
+  detail::check(ss_read_matrix_market(ctx.get(), path.c_str(), &h));
+  return Matrix(h);
+}
+
+inline void write_matrix_market(const Matrix& a, const std::string& path) {
+  detail::check(ss_write_matrix_market(a.get(), path.c_str()));
+}
+
+inline Vector read_vector_csv(const std::string& path) {
+  int64_t n = 0;
+  detail::check(ss_read_vector_csv(path.c_str(), nullptr, 0, &n));
+  Vector v(static_cast<std::size_t>(n));
+  detail::check(ss_read_vector_csv(path.c_str(), v.data(), n, &n));
+  return v;
+}
+
+inline void write_vector_csv(const Vector& v, const std::string& path) {
+  detail::check(ss_write_vector_csv(path.c_str(), v.data(), static_cast<int64_t>(v.size())));
+}
+
+inline std::vector<double> shepp_logan_ellipses() {
+  // reference phantom.cpp:18-32, rows (x0, y0, a, b, angle rad, density)
+  const double t[10][6] = {{0.0, 0.0, 0.69, 0.92, 0.0, 2.0},
+                           {0.0, -0.0184, 0.6624, 0.874, 0.0, -0.98},
+                           {0.22, 0.0, 0.11, 0.31, -18.0, -0.02},
+                           {-0.22, 0.0, 0.16, 0.41, 18.0, -0.02},
+                           {0.0, 0.35, 0.21, 0.25, 0.0, 0.01},
+                           {0.0, 0.1, 0.046, 0.046, 0.0, 0.01},
+                           {0.0, -0.1, 0.046, 0.046, 0.0, 0.01},
+                           {-0.08, -0.605, 0.046, 0.023, 0.0, 0.01},
+                           {0.0, -0.606, 0.023, 0.023, 0.0, 0.01},
+                           {0.06, -0.605, 0.023, 0.046, 0.0, 0.01}};
+  std::vector<double> out;
+  for (const auto& e : t) {
+    out.insert(out.end(), {e[0], e[1], e[2], e[3], degrees_to_radians(e[4]), e[5]});
+  }
+  return out;
 }
 
 // ------------------------------------------------------------------ phantom

@@ -6,7 +6,8 @@ is its Python mirror of the reference API. No CPU fallback exists.
 """
 from .symsplit import (  # noqa: F401
     CentroSystem, Context, DeviceError, Error, Matrix, SartPlan, SolutionPair, SolveOptions,
-    cgls_solve,
+    IoError, cgls_solve, read_matrix_market, read_vector_csv, write_matrix_market,
+    write_vector_csv,
     SolveReport, SplitSystem, SymmetryError, SymmetryReport, SymsplitError, build_system,
     decompose_solution, default_context, degrees_to_radians, enumerate_rays, forward_project,
     make_grid, parse_scan_config, random_ellipses, rasterize, recombine_solution, sart_solve,

@@ -12,8 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSB_LIB") or os.path.join(HERE, "libsymsplit_b200.so")  # SSB_LIB: A/B builds
 
-SS_OK, SS_ERR_INVALID, SS_ERR_SYMMETRY, SS_ERR_DIVERGED, SS_ERR_CUDA, SS_ERR_NCCL, SS_ERR_OOM = (
-    0, 1, 2, 3, 4, 5, 6)
+(SS_OK, SS_ERR_INVALID, SS_ERR_SYMMETRY, SS_ERR_DIVERGED, SS_ERR_CUDA, SS_ERR_NCCL, SS_ERR_OOM,
+ SS_ERR_IO) = (0, 1, 2, 3, 4, 5, 6, 7)
 SS_F64, SS_F32 = 0, 1
 
 i64 = C.c_int64
@@ -120,6 +120,10 @@ SIGNATURES = {
     "ss_partition_rows": (C.c_int, [i32p, i64, C.c_int, i64p]),
     "ss_plan_create_sharded": (C.c_int, [vp, vp, i64, i64, C.POINTER(SolveOptionsC),
                                          C.POINTER(vp)]),
+    "ss_read_matrix_market": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+    "ss_write_matrix_market": (C.c_int, [vp, C.c_char_p]),
+    "ss_read_vector_csv": (C.c_int, [C.c_char_p, dp, i64, i64p]),
+    "ss_write_vector_csv": (C.c_int, [C.c_char_p, dp, i64]),
 }
 
 _lib = None

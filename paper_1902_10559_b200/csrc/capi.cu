@@ -12,6 +12,7 @@
 #include <string>
 
 #include "nccl_dyn.hpp"
+#include "io.hpp"
 #include "plan.hpp"
 
 namespace {
@@ -696,6 +697,55 @@ int ss_forward_project(ss_matrix_t a, const double* f, double* p) {
 
 int ss_add_noise(double* p, int64_t m, double sigma, uint64_t seed) {
   return guarded([&] { ssb::add_noise(p, m, sigma, seed); });
+}
+
+// ------------------------------------------------------------ file formats
+int ss_read_matrix_market(ss_ctx_t h, const char* path, ss_matrix_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(path, "path");
+    need(out, "out");
+    use_device(ctx);
+    const ssb::MmData d = ssb::read_matrix_market(path);
+    *out = wrap(ssb::matrix_from_triplets_host(ctx, d.rows, d.cols,
+                                               static_cast<int64_t>(d.v.size()), d.r.data(),
+                                               d.c.data(), d.v.data()));
+  });
+}
+
+int ss_write_matrix_market(ss_matrix_t a, const char* path) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    need(path, "path");
+    use_device(m->ctx);
+    std::vector<int> ptr(m->rows + 1), idx(m->nnz);
+    std::vector<double> val(m->nnz);
+    to_host(m->ctx, ptr.data(), m->rowptr.get(), m->rows + 1);
+    to_host(m->ctx, idx.data(), m->colidx.get(), m->nnz);
+    to_host(m->ctx, val.data(), m->val.get(), m->nnz);
+    ssb::write_matrix_market(path, m->rows, m->cols, ptr, idx, val);
+  });
+}
+
+int ss_read_vector_csv(const char* path, double* values, int64_t capacity, int64_t* count) {
+  return guarded([&] {
+    need(path, "path");
+    need(count, "count");
+    const std::vector<double> v = ssb::read_vector_csv(path);
+    *count = static_cast<int64_t>(v.size());
+    if (values) {
+      if (capacity < *count) ssb::fail("read_vector_csv: buffer too small");
+      std::memcpy(values, v.data(), v.size() * sizeof(double));
+    }
+  });
+}
+
+int ss_write_vector_csv(const char* path, const double* values, int64_t count) {
+  return guarded([&] {
+    need(path, "path");
+    if (count) need(values, "values");
+    ssb::write_vector_csv(path, values, count);
+  });
 }
 
 // ------------------------------------------------------------ plans

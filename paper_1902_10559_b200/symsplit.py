@@ -15,6 +15,7 @@ Differences from the reference, all deliberate:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import Optional
@@ -46,6 +47,10 @@ class DeviceError(Error):
     """CUDA / NCCL / out-of-memory failure inside the library."""
 
 
+class IoError(Error):
+    """symsplit::IoError (io.hpp:14-20): file open / parse failures, path and line in the message."""
+
+
 def _lib():
     return N.load()
 
@@ -58,6 +63,8 @@ def _check(rc, report=None):
         raise SymmetryError(msg, report)
     if rc in (N.SS_ERR_CUDA, N.SS_ERR_NCCL, N.SS_ERR_OOM):
         raise DeviceError(msg)
+    if rc == N.SS_ERR_IO:
+        raise IoError(msg)
     raise Error(msg)
 
 
@@ -440,8 +447,12 @@ def solve_split(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> Solve
     f = np.empty(cols)
     r = N.SolveReportC()
     o = opts._c()
-    _check(_lib().ss_solve_split(sys.a.h, _dp(p), len(p), C.c_double(sys.symmetry_tol),
-                                 C.byref(o), _dp(f), cols, C.byref(r)))
+    rc = _lib().ss_solve_split(sys.a.h, _dp(p), len(p), C.c_double(sys.symmetry_tol),
+                               C.byref(o), _dp(f), cols, C.byref(r))
+    if rc == N.SS_ERR_SYMMETRY:
+        msg = _lib().ss_last_error().decode()
+        raise SymmetryError(msg, verify_symmetry(sys.a, sys.symmetry_tol))
+    _check(rc)
     rep = _report(f, r, "split")
     rep.method = opts.method
     return rep
@@ -497,6 +508,35 @@ def build_system(cfg: N.ScanConfig, parallelism: int = 0,
     _check(_lib().ss_build_system(ctx.h, C.byref(cfg), parallelism, C.byref(h)))
     a = Matrix(h, ctx)
     return CentroSystem(a, np.zeros(a.shape[0]), 0.0)
+
+
+# ----------------------------------------------------------------- file formats
+def read_matrix_market(path: str, ctx: Optional[Context] = None) -> Matrix:
+    """io.cpp:83-187: coordinate real general -> device CSR; IoError names path:line."""
+    ctx = ctx or default_context()
+    h = N.vp()
+    _check(_lib().ss_read_matrix_market(ctx.h, os.fsencode(path), C.byref(h)))
+    return Matrix(h, ctx)
+
+
+def write_matrix_market(a: Matrix, path: str) -> None:
+    """io.cpp:189-210: stored non-zeros, 1-based, %.17g."""
+    _check(_lib().ss_write_matrix_market(a.h, os.fsencode(path)))
+
+
+def read_vector_csv(path: str):
+    """io.cpp:212-230: one value per line, blank lines and '#' comments skipped."""
+    n = C.c_int64(0)
+    _check(_lib().ss_read_vector_csv(os.fsencode(path), None, 0, C.byref(n)))
+    out = np.empty(n.value)
+    _check(_lib().ss_read_vector_csv(os.fsencode(path), _dp(out), n.value, C.byref(n)))
+    return out
+
+
+def write_vector_csv(v, path: str) -> None:
+    """io.cpp:232-238."""
+    v = _f64(v)
+    _check(_lib().ss_write_vector_csv(os.fsencode(path), _dp(v), len(v)))
 
 
 # ----------------------------------------------------------------- phantom

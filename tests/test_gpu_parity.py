@@ -219,8 +219,10 @@ def test_symmetry_errors(pins):
         P.split_system(P.CentroSystem(a, p, 1e-12))
     assert ei.value.report.max_violation == 8.0
     assert "not centrosymmetric (max violation 8 at (1,1), tol 1e-12)" in str(ei.value)
-    with pytest.raises(P.SymmetryError):
+    with pytest.raises(P.SymmetryError) as ei:
         P.solve_split(P.CentroSystem(a, p, 1e-12), P.SolveOptions(tol=0.0))
+    r = ei.value.report
+    assert r.max_violation == 8.0 and (r.worst_row, r.worst_col) == (1, 1)
     r = P.verify_symmetry(P.Matrix.dense(np.eye(3)), 1.0)
     assert not r.holds and r.status == 1
     assert P.verify_symmetry(P.Matrix.dense(np.ones((2, 3))), 1.0).status == 2
