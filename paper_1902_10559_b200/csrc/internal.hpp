@@ -204,6 +204,7 @@ std::int64_t nonzeros(Matrix& a);
 ss_symmetry_report verify_symmetry(Matrix& a, double tol);
 void fold(Matrix& a, Matrix*& a1, Matrix*& a2);
 bool same_pattern(Matrix& a, Matrix& b);
+void scan_counts(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n);
 void union_pattern(Matrix& a, Matrix& b, Matrix*& ua, Matrix*& ub);
 void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh);
 void recombine_dev(Context* ctx, const double* f1, const double* f2, double* f,

@@ -746,6 +746,11 @@ T read_scalar(Context* ctx, const T* dev) {
 
 }  // namespace
 
+// counts[0..n] -> exclusive-scan pointer (shared with the plan builder)
+void scan_counts(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n) {
+  counts_to_ptr(ctx, counts_np1, ptr, n);
+}
+
 // ====================================================================== API
 template <class T>
 void cast_dev(Context* ctx, const double* src, T* dst, std::int64_t n) {

@@ -42,6 +42,11 @@ struct Plan {
   DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
   DBuf<char> rv2, cv2;    // paired: CSR / CSC values interleaved [nnz][2]
   DBuf<char> pe, cc;      // paired: {p1,p2,rinv1,rinv2} per row, {cinv1,cinv2} per column
+  // paired + tiled: rows/columns padded to 4 entries and permuted within tiles
+  // of 4*VS entries so each gather instruction covers consecutive entries
+  bool tiled = false;
+  DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
+  std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;

@@ -71,6 +71,10 @@ struct SartK {
   const T* cv2;                 //               CSC values interleaved [nnz][2]
   const T* pe;                  //               per row {p1, p2, rinv1, rinv2}
   const T* cc;                  //               per column {cinv1, cinv2}
+  const int* tpf;               //               tiled: padded row pointer / indices
+  const int* tif;
+  const int* tpb;               //               tiled: padded column pointer / indices
+  const int* tib;
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
@@ -458,7 +462,58 @@ __device__ __forceinline__ void seg_dot2(const int* __restrict__ idx, const T* _
   acc_b = sb;
 }
 
+// Tiled layout (built by tile_stream_kernel): every vector starts on a quad
+// boundary and holds a multiple of 4 entries (zero-valued padding), and
+// within each tile of R <= VS quads the quad of lane l carries the original
+// entries l, l+R, l+2R, l+3R. Component j of the UF steps therefore gathers
+// consecutive entries across the lanes of one instruction -- neighbouring
+// voxels (rays) in the snake numbering -- so one gather touches a few L1
+// lines instead of one per lane. No scalar head/tail: fewer registers.
 template <class T, int VS, int UF>
+__device__ __forceinline__ void seg_dot2t(const int* __restrict__ idx, const T* __restrict__ v2,
+                                          const typename Vec2<T>::type* __restrict__ xv, int beg,
+                                          int end, int lane, unsigned mask, T& acc_a, T& acc_b) {
+  using T2 = typename Vec2<T>::type;
+  T sa = T(0), sb = T(0);
+  const int nvec = (end - beg) >> 2;
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    int4 c[UF];
+    T v[UF][8];
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = beg + ((q + u * VS) << 2);
+      c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
+      load8(v2 + 2 * k0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const T2 g0 = __ldg(xv + c[u].x), g1 = __ldg(xv + c[u].y), g2 = __ldg(xv + c[u].z),
+               g3 = __ldg(xv + c[u].w);
+      sa += v[u][0] * g0.x + v[u][2] * g1.x + v[u][4] * g2.x + v[u][6] * g3.x;
+      sb += v[u][1] * g0.y + v[u][3] * g1.y + v[u][5] * g2.y + v[u][7] * g3.y;
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = beg + (q << 2);
+    const int4 c0 = __ldg(reinterpret_cast<const int4*>(idx + k0));
+    T v[8];
+    load8(v2 + 2 * k0, v);
+    const T2 g0 = __ldg(xv + c0.x), g1 = __ldg(xv + c0.y), g2 = __ldg(xv + c0.z),
+             g3 = __ldg(xv + c0.w);
+    sa += v[0] * g0.x + v[2] * g1.x + v[4] * g2.x + v[6] * g3.x;
+    sb += v[1] * g0.y + v[3] * g1.y + v[5] * g2.y + v[7] * g3.y;
+  }
+#pragma unroll
+  for (int off = VS / 2; off > 0; off >>= 1) {
+    sa += __shfl_xor_sync(mask, sa, off, VS);
+    sb += __shfl_xor_sync(mask, sb, off, VS);
+  }
+  acc_a = sa;
+  acc_b = sb;
+}
+
+template <class T, int VS, int UF, bool TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
   using T2 = typename Vec2<T>::type;
   __shared__ double red[2][kWarps];
@@ -468,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   const int n = static_cast<int>(k.rows0);
-  const int* __restrict__ ptr = k.s[0].rp;
+  const int* __restrict__ ptr = TL ? k.tpf : k.s[0].rp;
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
     int g = static_cast<int>(group);
@@ -487,8 +542,13 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
       T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      seg_dot2<T, VS, UF>(k.s[0].ci, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
-                          mask, da, db);
+      if (TL) {
+        seg_dot2t<T, VS, UF>(k.tif, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
+                             mask, da, db);
+      } else {
+        seg_dot2<T, VS, UF>(k.s[0].ci, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
+                            mask, da, db);
+      }
       if (lane == 0) {
         const T ra = e[0] - da, rb = e[1] - db;
         T2 wo;
@@ -524,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   }
 }
 
-template <class T, int VS, int UF>
+template <class T, int VS, int UF, bool TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
   using T2 = typename Vec2<T>::type;
   const int lane = threadIdx.x & (VS - 1);
@@ -534,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   if (!on0 && !on1) return;
   const int n = static_cast<int>(k.cols0);
-  const int* __restrict__ ptr = k.s[0].cp;
+  const int* __restrict__ ptr = TL ? k.tpb : k.s[0].cp;
   int g = static_cast<int>(group);
   int beg = 0, end = 0;
   if (g < n) {
@@ -555,8 +615,13 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
     }
     T ua, ub;
-    seg_dot2<T, VS, UF>(k.s[0].ri, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane,
-                        mask, ua, ub);
+    if (TL) {
+      seg_dot2t<T, VS, UF>(k.tib, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane, mask,
+                           ua, ub);
+    } else {
+      seg_dot2<T, VS, UF>(k.s[0].ri, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane,
+                          mask, ua, ub);
+    }
     if (lane == 0) {
       if (on0) xo.x = upd(xo.x, k.relax, ua, ci.x);
       if (on1) xo.y = upd(xo.y, k.relax, ub, ci.y);
@@ -585,6 +650,48 @@ __global__ void deinterleave_kernel(const T* xx, T* x1, T* x2, long long n) {
        j += (long long)gridDim.x * blockDim.x) {
     x1[j] = xx[2 * j];
     x2[j] = xx[2 * j + 1];
+  }
+}
+
+// Tiled paired stream of one compressed matrix (see seg_dot2t): one warp per
+// vector writes its padded, tile-permuted indices and interleaved values.
+// Padding repeats the vector's last index (an L1-hot gather) with value 0.
+template <class T>
+__global__ void tile_stream_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                   const T* __restrict__ v0, const T* __restrict__ v1,
+                                   long long nvec, const int* __restrict__ tptr,
+                                   int* __restrict__ tidx, T* __restrict__ tv2, int tile) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long s = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+       s < nvec; s += nw) {
+    const int beg = ptr[s], len = ptr[s + 1] - beg;
+    const int ob = tptr[s], lp = tptr[s + 1] - ob;
+    const int pad = len > 0 ? idx[beg + len - 1] : 0;
+    for (int p = lane; p < lp; p += 32) {
+      const int t0 = (p / tile) * tile;
+      const int r = min(tile, lp - t0) >> 2;  // quads in this tile
+      const int w = p - t0;
+      const int o = t0 + (w & 3) * r + (w >> 2);
+      int c = pad;
+      T a = T(0), b = T(0);
+      if (o < len) {
+        c = idx[beg + o];
+        a = v0[beg + o];
+        b = v1[beg + o];
+      }
+      tidx[ob + p] = c;
+      tv2[2 * static_cast<long long>(ob + p)] = a;
+      tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+    }
+  }
+}
+
+// padded vector lengths (multiple of 4) -> counts for the pointer scan
+__global__ void pad4_counts_kernel(const int* __restrict__ ptr, long long n, int* __restrict__ cnt) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    cnt[i] = i < n ? ((ptr[i + 1] - ptr[i] + 3) & ~3) : 0;
   }
 }
 
@@ -1333,6 +1440,10 @@ SartK<T> make_args(Plan& P) {
   k.cv2 = reinterpret_cast<const T*>(P.cv2.get());
   k.pe = reinterpret_cast<const T*>(P.pe.get());
   k.cc = reinterpret_cast<const T*>(P.cc.get());
+  k.tpf = P.tptr_f.get();
+  k.tif = P.tidx_f.get();
+  k.tpb = P.tptr_b.get();
+  k.tib = P.tidx_b.get();
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
@@ -1400,11 +1511,16 @@ void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
   const int vs = fwd ? P.vs_fwd : P.vs_back;
   const int uf = fwd ? P.uf_fwd : P.uf_back;
   const int blocks = fwd ? P.fwd_blocks : P.back_blocks;
-#define SSB_PAIR(V, U)                                                                     \
-  if (vs == V && uf == U) {                                                                \
-    if (fwd) sart_fwd_pair_kernel<T, V, U><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
-    else sart_back_pair_kernel<T, V, U><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
-    return;                                                                                \
+#define SSB_PAIR(V, U)                                                                         \
+  if (vs == V && uf == U) {                                                                    \
+    if (P.tiled) {                                                                             \
+      if (fwd) sart_fwd_pair_kernel<T, V, U, true><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
+      else sart_back_pair_kernel<T, V, U, true><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
+    } else {                                                                                   \
+      if (fwd) sart_fwd_pair_kernel<T, V, U, false><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
+      else sart_back_pair_kernel<T, V, U, false><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
+    }                                                                                          \
+    return;                                                                                    \
   }
   SSB_PAIR(4, 1) SSB_PAIR(8, 1) SSB_PAIR(16, 1) SSB_PAIR(32, 1)
   SSB_PAIR(4, 2) SSB_PAIR(8, 2) SSB_PAIR(16, 2) SSB_PAIR(32, 2)
@@ -1496,14 +1612,14 @@ int occupancy_pair_blocks(Plan& P, bool fwd) {
   int per_sm = 0;
   if (P.dtype == SS_F32) {
     SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_fwd_pair_kernel<float, 16, 2>, kThreads, 0)
+                       &per_sm, sart_fwd_pair_kernel<float, 16, 2, true>, kThreads, 0)
                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_back_pair_kernel<float, 4, 2>, kThreads, 0));
+                       &per_sm, sart_back_pair_kernel<float, 4, 2, true>, kThreads, 0));
   } else {
     SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_fwd_pair_kernel<double, 16, 2>, kThreads, 0)
+                       &per_sm, sart_fwd_pair_kernel<double, 16, 2, true>, kThreads, 0)
                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_back_pair_kernel<double, 4, 2>, kThreads, 0));
+                       &per_sm, sart_back_pair_kernel<double, 4, 2, true>, kThreads, 0));
   }
   return std::max(1, per_sm) * P.ctx->sm_count;
 }
@@ -1838,8 +1954,9 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
   const std::int64_t b = static_cast<std::int64_t>(tsize());
   std::int64_t f = 0, k = 0;
   if (paired) {
-    f = a[0]->nnz * (4 + 2 * b) + 4 * (rows[0] + 1);
-    k = a[0]->nnz * (4 + 2 * b) + 4 * (cols[0] + 1);
+    const std::int64_t nf = tiled ? tnnz_f : a[0]->nnz, nb = tiled ? tnnz_b : a[0]->nnz;
+    f = nf * (4 + 2 * b) + 4 * (rows[0] + 1);
+    k = nb * (4 + 2 * b) + 4 * (cols[0] + 1);
   } else {
     for (int s = 0; s < nsys; ++s) {
       f += a[s]->nnz * (4 + b) + 4 * (rows[s] + 1);
@@ -2021,12 +2138,32 @@ void setup_stream(Plan& P, int mode) {
 }  // namespace
 
 namespace {
+// padded pointer of one compressed direction; returns the padded entry count
+std::int64_t tiled_ptr(Plan& P, const int* ptr, long long n, DBuf<int>& tptr) {
+  DBuf<int> cnt(n + 1);
+  tptr.alloc(n + 1);
+  pad4_counts_kernel<<<grid1(P.ctx, n + 1), 256, 0, P.ctx->stream>>>(ptr, n, cnt.get());
+  P.ctx->check_launch("pad4_counts_kernel");
+  scan_counts(P.ctx, cnt.get(), tptr.get(), n);
+  int total = 0;
+  P.ctx->copy(&total, tptr.get() + n, sizeof(int));
+  return total;
+}
+
 template <class T>
 void build_paired_t(Plan& P) {
   const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
   const std::size_t tb = sizeof(T);
-  P.rv2.alloc(2 * nnz * tb);
-  P.cv2.alloc(2 * nnz * tb);
+  if (P.tiled) {
+    if (nnz + 3 * std::max(rows, cols) >= (1LL << 31)) {
+      P.tiled = false;  // padded offsets must stay in int32
+    } else {
+      P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
+      P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
+    }
+  }
+  P.rv2.alloc(2 * (P.tiled ? P.tnnz_f : nnz) * tb);
+  P.cv2.alloc(2 * (P.tiled ? P.tnnz_b : nnz) * tb);
   P.pe.alloc(4 * rows * tb);
   P.cc.alloc(2 * cols * tb);
   SSB_CUDA(cudaMemsetAsync(P.pe.get(), 0, 4 * rows * tb, P.ctx->stream));
@@ -2043,8 +2180,10 @@ void build_paired_t(Plan& P) {
       rv = P.a[s]->val.get();
       cv = P.a[s]->cval.get();
     }
-    interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(rv, rv2, nnz, 2, s);
-    interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(cv, cv2, nnz, 2, s);
+    if (!P.tiled) {
+      interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(rv, rv2, nnz, 2, s);
+      interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(cv, cv2, nnz, 2, s);
+    }
     interleave_kernel<T, T><<<gr, 256, 0, P.ctx->stream>>>(
         reinterpret_cast<const T*>(P.rinv[s].get()), reinterpret_cast<T*>(P.pe.get()), rows, 4,
         2 + s);
@@ -2052,6 +2191,23 @@ void build_paired_t(Plan& P) {
         reinterpret_cast<const T*>(P.cinv[s].get()), reinterpret_cast<T*>(P.cc.get()), cols, 2,
         s);
     P.ctx->check_launch("interleave_kernel");
+  }
+  if (P.tiled) {
+    const auto vals = [&](int s, bool csr) -> const T* {
+      if constexpr (sizeof(T) == 4) return csr ? P.a[s]->val32.get() : P.a[s]->cval32.get();
+      else return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
+    };
+    P.tidx_f.alloc(P.tnnz_f);
+    P.tidx_b.alloc(P.tnnz_b);
+    const int gw = static_cast<int>(std::min<long long>(P.ctx->sm_count * 16LL,
+                                                        (std::max(rows, cols) + 7) / 8));
+    tile_stream_kernel<T><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
+        P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
+        P.tptr_f.get(), P.tidx_f.get(), rv2, 4 * P.vs_fwd);
+    tile_stream_kernel<T><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
+        P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
+        P.tptr_b.get(), P.tidx_b.get(), cv2, 4 * P.vs_back);
+    P.ctx->check_launch("tile_stream_kernel");
   }
   P.ctx->sync();
 }
@@ -2084,6 +2240,7 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
       P->a[1] = P->pair_own[1];
     }
     P->paired = true;
+    P->tiled = env_int("SSB_TILED", 1) != 0;
     tr.mark("pair pattern");
   }
   for (int s = 0; s < P->nsys; ++s) {
