@@ -494,7 +494,7 @@ int ss_sart_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_opti
     check_system(A->rows, p, m, "sart_solve");
     check_options(*opts);
     if (n != A->cols) ssb::fail("sart_solve: solution length does not match columns");
-    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, A, nullptr, *opts, 1));
+    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, A, nullptr, *opts, 1, false));
     P->set_rhs_host(0, p);
     P->launch();
     ss_solve_report rep{};
@@ -617,7 +617,7 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       if (report) *report = rep;
       return;
     }
-    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1));
+    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1, false));
     tr.mark("plan (csc, norms, graph)");
     for (int s = 0; s < 2; ++s) {
       if (P->empty_rows[s]) errs[s] = "sart_solve: matrix has no nonzero rows";

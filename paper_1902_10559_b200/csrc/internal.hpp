@@ -132,8 +132,13 @@ struct PhaseTrace {
     if (!on) return;
     ctx->sync();
     const auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[ssb]     %-24s %9.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(n - t).count());
+    cudaMemPool_t pool;
+    unsigned long long reserved = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    }
+    std::fprintf(stderr, "[ssb]     %-24s %9.3f ms  (pool %llu MB)\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count(), reserved >> 20);
     t = n;
   }
 };
@@ -150,8 +155,11 @@ struct Matrix {
   DBuf<double> cval;
   bool has_f32 = false;
   DBuf<float> val32, cval32;
+  DBuf<int> csc_perm;  // CSR position of each CSC entry (kept on request)
 
-  void ensure_csc();
+  void ensure_csc(bool keep_perm = false);
+  // CSC of a matrix with ref's exact CSR pattern: ref's ordering, own values
+  void csc_like(const Matrix& ref);
   void ensure_f32();
 };
 

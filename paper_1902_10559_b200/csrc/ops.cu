@@ -287,14 +287,27 @@ __global__ void count_nonzero_kernel(const double* v, std::int64_t n, unsigned l
 // found by binary search in the mirror row, like SparseMatrix::coeff). Keeps
 // the row maximum and the smallest column reaching it — the first entry in
 // column-major order with strict '>'. One warp per row.
+constexpr int kSymCap = 1536;  // mirror-row columns staged per warp (6 KB)
+
 __global__ void symmetry_rows_kernel(const int* ptr, const int* col, const double* val,
                                      std::int64_t m, std::int64_t n, double* rmax, int* rarg) {
+  extern __shared__ int sym_sm[];
+  int* wsm = sym_sm + (threadIdx.x >> 5) * kSymCap;
   const int lane = threadIdx.x & 31;
   const std::int64_t w0 = (blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x) >> 5;
   const std::int64_t nw = ((std::int64_t)gridDim.x * blockDim.x) >> 5;
   for (std::int64_t i = w0; i < m; i += nw) {
     const std::int64_t mi = m - 1 - i;
     const int mb = ptr[mi], me = ptr[mi + 1];
+    // the mirror row's columns in shared memory when they fit: the per-entry
+    // binary searches then run at shared-memory latency
+    const int* mc = col;
+    __syncwarp();
+    if (me - mb <= kSymCap) {
+      for (int q = lane; q < me - mb; q += 32) wsm[q] = col[mb + q];
+      __syncwarp();
+      mc = wsm - mb;
+    }
     double best = 0.0;
     int arg = 0x7fffffff;
     for (int k = ptr[i] + lane; k < ptr[i + 1]; k += 32) {
@@ -303,9 +316,9 @@ __global__ void symmetry_rows_kernel(const int* ptr, const int* col, const doubl
       int lo = mb, hi = me;
       while (lo < hi) {
         const int mid = lo + ((hi - lo) >> 1);
-        if (col[mid] < target) lo = mid + 1; else hi = mid;
+        if (mc[mid] < target) lo = mid + 1; else hi = mid;
       }
-      const double mv = (lo < me && col[lo] == target) ? val[lo] : 0.0;
+      const double mv = (lo < me && mc[lo] == target) ? val[lo] : 0.0;
       const double d = fabs(sub(val[k], mv));
       if (d > best) {  // entries of a lane ascend in j: first maximum kept
         best = d;
@@ -397,8 +410,14 @@ __device__ __forceinline__ int first_at_least(const int* col, int b, int e, std:
 // count pass records per-lane counts; the fill pass writes each lane's
 // buckets at the row offset plus the exclusive prefix of the lanes before it,
 // so the output is sorted by bj exactly as a sequential merge would be.
+// Column indices of the two source rows are staged in shared memory (when
+// they fit) so the 32 per-lane merges chase indices at shared-memory latency.
+constexpr int kFoldCap = 1536;  // staged columns per warp (6 KB; 48 KB per 256-thread block)
+
 template <bool FILL>
 __global__ void fold_kernel(FoldArgs a) {
+  extern __shared__ int fold_sm[];
+  int* wsm = fold_sm + (threadIdx.x >> 5) * kFoldCap;
   const int lane = threadIdx.x & 31;
   const std::int64_t w0 = (blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x) >> 5;
   const std::int64_t nw = ((std::int64_t)gridDim.x * blockDim.x) >> 5;
@@ -407,27 +426,38 @@ __global__ void fold_kernel(FoldArgs a) {
     const std::int64_t top = bi, bot = a.m - 1 - bi;
     const int tb = a.ptr[top], te = a.ptr[top + 1];
     const int bb = a.ptr[bot], be = a.ptr[bot + 1];
-    const int tmid = first_at_least(a.col, tb, te, a.nh);  // first TR entry of top
-    const int bmid = first_at_least(a.col, bb, be, a.nh);
+    const int* ct = a.col;  // column lists of the top / bottom row
+    const int* cb = a.col;
+    const int lt = te - tb, lb = be - bb;
+    __syncwarp();  // previous row's reads of the staging area are done
+    if (lt + lb <= kFoldCap) {
+      for (int q = lane; q < lt; q += 32) wsm[q] = a.col[tb + q];
+      for (int q = lane; q < lb; q += 32) wsm[lt + q] = a.col[bb + q];
+      __syncwarp();
+      ct = wsm - tb;
+      cb = wsm + lt - bb;
+    }
+    const int tmid = first_at_least(ct, tb, te, a.nh);  // first TR entry of top
+    const int bmid = first_at_least(cb, bb, be, a.nh);
     // bucket span of the row (all four lists)
     std::int64_t lo = a.nh, hi = -1;
-    if (tmid > tb) { lo = min(lo, (std::int64_t)a.col[tb]); hi = max(hi, (std::int64_t)a.col[tmid - 1]); }
-    if (bmid > bb) { lo = min(lo, (std::int64_t)a.col[bb]); hi = max(hi, (std::int64_t)a.col[bmid - 1]); }
-    if (te > tmid) { lo = min(lo, nm1 - a.col[te - 1]); hi = max(hi, nm1 - a.col[tmid]); }
-    if (be > bmid) { lo = min(lo, nm1 - a.col[be - 1]); hi = max(hi, nm1 - a.col[bmid]); }
+    if (tmid > tb) { lo = min(lo, (std::int64_t)ct[tb]); hi = max(hi, (std::int64_t)ct[tmid - 1]); }
+    if (bmid > bb) { lo = min(lo, (std::int64_t)cb[bb]); hi = max(hi, (std::int64_t)cb[bmid - 1]); }
+    if (te > tmid) { lo = min(lo, nm1 - ct[te - 1]); hi = max(hi, nm1 - ct[tmid]); }
+    if (be > bmid) { lo = min(lo, nm1 - cb[be - 1]); hi = max(hi, nm1 - cb[bmid]); }
     int n1 = 0, n2 = 0;
     if (hi >= lo) {
       const std::int64_t span = hi - lo + 1;
       const std::int64_t s_lo = lo + span * lane / 32, s_hi = lo + span * (lane + 1) / 32;
       // TL/BL: columns in [s_lo, s_hi); TR/BR: columns in [n-s_hi, n-1-s_lo], walked down
-      int tl = first_at_least(a.col, tb, tmid, s_lo);
-      const int tl_end = first_at_least(a.col, tl, tmid, s_hi);
-      int bl = first_at_least(a.col, bb, bmid, s_lo);
-      const int bl_end = first_at_least(a.col, bl, bmid, s_hi);
-      const int tr_stop = first_at_least(a.col, tmid, te, a.n - s_hi);
-      int tr = first_at_least(a.col, tr_stop, te, a.n - s_lo) - 1;
-      const int br_stop = first_at_least(a.col, bmid, be, a.n - s_hi);
-      int br = first_at_least(a.col, br_stop, be, a.n - s_lo) - 1;
+      int tl = first_at_least(ct, tb, tmid, s_lo);
+      const int tl_end = first_at_least(ct, tl, tmid, s_hi);
+      int bl = first_at_least(cb, bb, bmid, s_lo);
+      const int bl_end = first_at_least(cb, bl, bmid, s_hi);
+      const int tr_stop = first_at_least(ct, tmid, te, a.n - s_hi);
+      int tr = first_at_least(ct, tr_stop, te, a.n - s_lo) - 1;
+      const int br_stop = first_at_least(cb, bmid, be, a.n - s_hi);
+      int br = first_at_least(cb, br_stop, be, a.n - s_lo) - 1;
       int o1 = 0, o2 = 0;
       if (FILL) {
         const int c1 = a.cnt1[bi * 32 + lane], c2 = a.cnt2[bi * 32 + lane];
@@ -446,10 +476,10 @@ __global__ void fold_kernel(FoldArgs a) {
       }
       for (;;) {
         std::int64_t bj = s_hi;
-        if (tl < tl_end) bj = min(bj, (std::int64_t)a.col[tl]);
-        if (bl < bl_end) bj = min(bj, (std::int64_t)a.col[bl]);
-        if (tr >= tr_stop) bj = min(bj, nm1 - a.col[tr]);
-        if (br >= br_stop) bj = min(bj, nm1 - a.col[br]);
+        if (tl < tl_end) bj = min(bj, (std::int64_t)ct[tl]);
+        if (bl < bl_end) bj = min(bj, (std::int64_t)cb[bl]);
+        if (tr >= tr_stop) bj = min(bj, nm1 - ct[tr]);
+        if (br >= br_stop) bj = min(bj, nm1 - cb[br]);
         if (bj == s_hi) break;
         bool have = false;
         double s1 = 0.0, s2 = 0.0;
@@ -465,10 +495,10 @@ __global__ void fold_kernel(FoldArgs a) {
             s2 = add(s2, h);
           }
         };
-        if (tl < tl_end && a.col[tl] == bj) term(a.val[tl++], false);
-        if (bl < bl_end && a.col[bl] == bj) term(a.val[bl++], true);
-        if (tr >= tr_stop && nm1 - a.col[tr] == bj) term(a.val[tr--], true);
-        if (br >= br_stop && nm1 - a.col[br] == bj) term(a.val[br--], false);
+        if (tl < tl_end && ct[tl] == bj) term(a.val[tl++], false);
+        if (bl < bl_end && cb[bl] == bj) term(a.val[bl++], true);
+        if (tr >= tr_stop && nm1 - ct[tr] == bj) term(a.val[tr--], true);
+        if (br >= br_stop && nm1 - cb[br] == bj) term(a.val[br--], false);
         if (s1 != 0.0) {
           if (FILL) {
             a.col1[o1] = static_cast<int>(bj);
@@ -891,7 +921,7 @@ Matrix* matrix_from_csc_host(Context* ctx, std::int64_t rows, std::int64_t cols,
   return a;
 }
 
-void Matrix::ensure_csc() {
+void Matrix::ensure_csc(bool keep_perm) {
   if (has_csc) return;
   Context* c = ctx;
   colptr.alloc(cols + 1);
@@ -927,7 +957,38 @@ void Matrix::ensure_csc() {
   ptr_from_sorted_kernel<<<grid_for(c, nnz + 1), kT, 0, c->stream>>>(keys_out.get(), nnz, cols,
                                                                     colptr.get());
   c->check_launch("ptr_from_sorted_kernel");
+  if (keep_perm) csc_perm = std::move(perm_out);
   c->sync();
+  has_csc = true;
+}
+
+__global__ void permute_values_kernel(const int* __restrict__ perm, const double* __restrict__ src,
+                                      std::int64_t n, double* __restrict__ dst) {
+  for (std::int64_t k = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (std::int64_t)gridDim.x * blockDim.x) {
+    dst[k] = src[perm[k]];
+  }
+}
+
+void Matrix::csc_like(const Matrix& ref) {
+  if (has_csc) return;
+  if (ref.ctx != ctx || !ref.has_csc || ref.nnz != nnz || ref.rows != rows || ref.cols != cols ||
+      ref.csc_perm.size() != static_cast<std::size_t>(std::max<std::int64_t>(nnz, 1)) ||
+      nnz == 0) {
+    ensure_csc();
+    return;
+  }
+  Context* c = ctx;
+  colptr.alloc(cols + 1);
+  rowidx.alloc(nnz);
+  cval.alloc(nnz);
+  SSB_CUDA(cudaMemcpyAsync(colptr.get(), ref.colptr.get(), (cols + 1) * sizeof(int),
+                           cudaMemcpyDeviceToDevice, c->stream));
+  SSB_CUDA(cudaMemcpyAsync(rowidx.get(), ref.rowidx.get(), nnz * sizeof(int),
+                           cudaMemcpyDeviceToDevice, c->stream));
+  permute_values_kernel<<<grid_for(c, nnz), kT, 0, c->stream>>>(ref.csc_perm.get(), val.get(),
+                                                               nnz, cval.get());
+  c->check_launch("permute_values_kernel");
   has_csc = true;
 }
 
@@ -1034,7 +1095,8 @@ ss_symmetry_report verify_symmetry(Matrix& a, double tol) {
     DBuf<double> rmax(a.rows);
     DBuf<int> rarg(a.rows);
     DBuf<Worst> w(1);
-    symmetry_rows_kernel<<<grid_for(ctx, a.rows * 32), kT, 0, ctx->stream>>>(
+    symmetry_rows_kernel<<<grid_for(ctx, a.rows * 32), kT,
+                           (kT / 32) * kSymCap * static_cast<int>(sizeof(int)), ctx->stream>>>(
         a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, rmax.get(), rarg.get());
     ctx->check_launch("symmetry_rows_kernel");
     symmetry_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(rmax.get(), rarg.get(), a.rows, w.get());
@@ -1050,6 +1112,9 @@ ss_symmetry_report verify_symmetry(Matrix& a, double tol) {
   return rep;
 }
 
+constexpr int kFoldSmem = (kT / 32) * kFoldCap * static_cast<int>(sizeof(int));
+static_assert(kFoldSmem <= 48 * 1024, "fold staging must fit the default shared memory");
+
 void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   if (a.rows % 2 != 0 || a.cols % 2 != 0) fail("split_matrix: dimensions must be even");
   Context* ctx = a.ctx;
@@ -1061,7 +1126,7 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
               nullptr, nullptr, lane1.get(), lane2.get(), c1.get(), c2.get(),
               nullptr, nullptr, nullptr, nullptr};
   if (mh > 0) {
-    fold_kernel<false><<<grid_for(ctx, mh * 32), kT, 0, ctx->stream>>>(fa);
+    fold_kernel<false><<<grid_for(ctx, mh * 32), kT, kFoldSmem, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<count>");
   }
   DBuf<int> p1(mh + 1), p2(mh + 1);
@@ -1078,7 +1143,7 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   fa.col2 = col2.get();
   fa.val2 = val2.get();
   if (mh > 0) {
-    fold_kernel<true><<<grid_for(ctx, mh * 32), kT, 0, ctx->stream>>>(fa);
+    fold_kernel<true><<<grid_for(ctx, mh * 32), kT, kFoldSmem, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<fill>");
   }
   ctx->sync();

@@ -75,7 +75,8 @@ struct Plan {
   void kernel_bytes(std::int64_t* fwd, std::int64_t* back) const;
 };
 
-Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs);
+Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs,
+                bool reusable = true);
 Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t row_begin, std::int64_t row_end,
                         const ss_solve_options& o);
 void partition_rows(const int* rowptr, std::int64_t rows, int parts, std::int64_t* bounds);

@@ -513,7 +513,7 @@ __device__ __forceinline__ void seg_dot2t(const int* __restrict__ idx, const T* 
   acc_b = sb;
 }
 
-template <class T, int VS, int UF, bool TL>
+template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
   using T2 = typename Vec2<T>::type;
   __shared__ double red[2][kWarps];
@@ -523,26 +523,27 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   const int n = static_cast<int>(k.rows0);
-  const int* __restrict__ ptr = TL ? k.tpf : k.s[0].rp;
+  const int* __restrict__ ptr = TL != 0 ? k.tpf : k.s[0].rp;
+  int g = static_cast<int>(group);
+  const int gend = n, gstep = static_cast<int>(ngroups);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    int g = static_cast<int>(group);
     int beg = 0, end = 0;
-    if (g < n) {
+    if (g < gend) {
       beg = __ldg(ptr + g);
       end = __ldg(ptr + g + 1);
     }
-    for (; g < n; g += static_cast<int>(ngroups)) {
-      const int gn = g + static_cast<int>(ngroups);
+    for (; g < gend; g += gstep) {
+      const int gn = g + gstep;
       int nbeg = 0, nend = 0;
-      if (gn < n) {  // next row's bounds, ahead of this row's dot product
+      if (gn < gend) {  // next row's bounds, ahead of this row's dot product
         nbeg = __ldg(ptr + gn);
         nend = __ldg(ptr + gn + 1);
       }
       T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      if (TL) {
+      if (TL == 1) {
         seg_dot2t<T, VS, UF>(k.tif, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
                              mask, da, db);
       } else {
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   }
 }
 
-template <class T, int VS, int UF, bool TL>
+template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
   using T2 = typename Vec2<T>::type;
   const int lane = threadIdx.x & (VS - 1);
@@ -594,17 +595,18 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   if (!on0 && !on1) return;
   const int n = static_cast<int>(k.cols0);
-  const int* __restrict__ ptr = TL ? k.tpb : k.s[0].cp;
+  const int* __restrict__ ptr = TL != 0 ? k.tpb : k.s[0].cp;
   int g = static_cast<int>(group);
+  const int gend = n, gstep = static_cast<int>(ngroups);
   int beg = 0, end = 0;
-  if (g < n) {
+  if (g < gend) {
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
   }
-  for (; g < n; g += static_cast<int>(ngroups)) {
-    const int gn = g + static_cast<int>(ngroups);
+  for (; g < gend; g += gstep) {
+    const int gn = g + gstep;
     int nbeg = 0, nend = 0;
-    if (gn < n) {
+    if (gn < gend) {
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
     }
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
     }
     T ua, ub;
-    if (TL) {
+    if (TL == 1) {
       seg_dot2t<T, VS, UF>(k.tib, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane, mask,
                            ua, ub);
     } else {
@@ -656,9 +658,9 @@ __global__ void deinterleave_kernel(const T* xx, T* x1, T* x2, long long n) {
 // Tiled paired stream of one compressed matrix (see seg_dot2t): one warp per
 // vector writes its padded, tile-permuted indices and interleaved values.
 // Padding repeats the vector's last index (an L1-hot gather) with value 0.
-template <class T>
+template <class T, class S>
 __global__ void tile_stream_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
-                                   const T* __restrict__ v0, const T* __restrict__ v1,
+                                   const S* __restrict__ v0, const S* __restrict__ v1,
                                    long long nvec, const int* __restrict__ tptr,
                                    int* __restrict__ tidx, T* __restrict__ tv2, int tile) {
   const int lane = threadIdx.x & 31;
@@ -677,8 +679,8 @@ __global__ void tile_stream_kernel(const int* __restrict__ ptr, const int* __res
       T a = T(0), b = T(0);
       if (o < len) {
         c = idx[beg + o];
-        a = v0[beg + o];
-        b = v1[beg + o];
+        a = static_cast<T>(v0[beg + o]);  // fp64 master values rounded once to the plan type
+        b = static_cast<T>(v1[beg + o]);
       }
       tidx[ob + p] = c;
       tv2[2 * static_cast<long long>(ob + p)] = a;
@@ -1507,26 +1509,33 @@ void stream_attributes() {
 }
 
 template <class T>
-void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
+using PairFn = void (*)(SartK<T>, int);
+
+// the paired kernel a plan launches (layout x VS x UF) and its
+// dynamic shared memory
+template <class T>
+PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
   const int vs = fwd ? P.vs_fwd : P.vs_back;
   const int uf = fwd ? P.uf_fwd : P.uf_back;
-  const int blocks = fwd ? P.fwd_blocks : P.back_blocks;
-#define SSB_PAIR(V, U)                                                                         \
-  if (vs == V && uf == U) {                                                                    \
-    if (P.tiled) {                                                                             \
-      if (fwd) sart_fwd_pair_kernel<T, V, U, true><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
-      else sart_back_pair_kernel<T, V, U, true><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
-    } else {                                                                                   \
-      if (fwd) sart_fwd_pair_kernel<T, V, U, false><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it); \
-      else sart_back_pair_kernel<T, V, U, false><<<blocks, kThreads, 0, P.ctx->stream>>>(k, it);    \
-    }                                                                                          \
-    return;                                                                                    \
+  *smem = 0;
+#define SSB_PAIR(V, U)                                                                        \
+  if (vs == V && uf == U) {                                                                   \
+    if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
+    return fwd ? sart_fwd_pair_kernel<T, V, U, 1> : sart_back_pair_kernel<T, V, U, 1>;        \
   }
   SSB_PAIR(4, 1) SSB_PAIR(8, 1) SSB_PAIR(16, 1) SSB_PAIR(32, 1)
   SSB_PAIR(4, 2) SSB_PAIR(8, 2) SSB_PAIR(16, 2) SSB_PAIR(32, 2)
   SSB_PAIR(4, 4) SSB_PAIR(8, 4) SSB_PAIR(16, 4) SSB_PAIR(32, 4)
 #undef SSB_PAIR
   fail("plan: unsupported paired kernel shape");
+  return nullptr;
+}
+
+template <class T>
+void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
+  int smem = 0;
+  const PairFn<T> fn = pair_kernel<T>(P, fwd, &smem);
+  fn<<<fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream>>>(k, it);
 }
 
 template <class T>
@@ -1608,20 +1617,19 @@ int occupancy_blocks(Plan& P, bool fwd) {
   return std::max(1, per_sm) * P.ctx->sm_count;
 }
 
-int occupancy_pair_blocks(Plan& P, bool fwd) {
-  int per_sm = 0;
-  if (P.dtype == SS_F32) {
-    SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_fwd_pair_kernel<float, 16, 2, true>, kThreads, 0)
-                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_back_pair_kernel<float, 4, 2, true>, kThreads, 0));
-  } else {
-    SSB_CUDA(fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_fwd_pair_kernel<double, 16, 2, true>, kThreads, 0)
-                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                       &per_sm, sart_back_pair_kernel<double, 4, 2, true>, kThreads, 0));
+template <class T>
+int occupancy_pair_t(Plan& P, bool fwd) {
+  int smem = 0, per_sm = 0;
+  const PairFn<T> fn = pair_kernel<T>(P, fwd, &smem);
+  if (smem > 0) {  // static + dynamic may pass 48 KB
+    SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
   return std::max(1, per_sm) * P.ctx->sm_count;
+}
+
+int occupancy_pair_blocks(Plan& P, bool fwd) {
+  return P.dtype == SS_F32 ? occupancy_pair_t<float>(P, fwd) : occupancy_pair_t<double>(P, fwd);
 }
 
 template <class T>
@@ -2171,16 +2179,17 @@ void build_paired_t(Plan& P) {
   T* cv2 = reinterpret_cast<T*>(P.cv2.get());
   const int gn = grid1(P.ctx, nnz), gr = grid1(P.ctx, rows), gc = grid1(P.ctx, cols);
   for (int s = 0; s < 2; ++s) {
-    const T* rv = nullptr;
-    const T* cv = nullptr;
-    if constexpr (sizeof(T) == 4) {
-      rv = P.a[s]->val32.get();
-      cv = P.a[s]->cval32.get();
-    } else {
-      rv = P.a[s]->val.get();
-      cv = P.a[s]->cval.get();
-    }
     if (!P.tiled) {
+      const T* rv = nullptr;
+      const T* cv = nullptr;
+      if constexpr (sizeof(T) == 4) {
+        P.a[s]->ensure_f32();
+        rv = P.a[s]->val32.get();
+        cv = P.a[s]->cval32.get();
+      } else {
+        rv = P.a[s]->val.get();
+        cv = P.a[s]->cval.get();
+      }
       interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(rv, rv2, nnz, 2, s);
       interleave_kernel<T, T><<<gn, 256, 0, P.ctx->stream>>>(cv, cv2, nnz, 2, s);
     }
@@ -2192,19 +2201,18 @@ void build_paired_t(Plan& P) {
         s);
     P.ctx->check_launch("interleave_kernel");
   }
-  if (P.tiled) {
-    const auto vals = [&](int s, bool csr) -> const T* {
-      if constexpr (sizeof(T) == 4) return csr ? P.a[s]->val32.get() : P.a[s]->cval32.get();
-      else return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
+  if (P.tiled) {  // straight from the fp64 CSR/CSC values (no fp32 matrix copies)
+    const auto vals = [&](int s, bool csr) -> const double* {
+      return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
     };
     P.tidx_f.alloc(P.tnnz_f);
     P.tidx_b.alloc(P.tnnz_b);
     const int gw = static_cast<int>(std::min<long long>(P.ctx->sm_count * 16LL,
                                                         (std::max(rows, cols) + 7) / 8));
-    tile_stream_kernel<T><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
+    tile_stream_kernel<T, double><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
         P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
         P.tptr_f.get(), P.tidx_f.get(), rv2, 4 * P.vs_fwd);
-    tile_stream_kernel<T><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
+    tile_stream_kernel<T, double><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
         P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
         P.tptr_b.get(), P.tidx_b.get(), cv2, 4 * P.vs_back);
     P.ctx->check_launch("tile_stream_kernel");
@@ -2213,7 +2221,8 @@ void build_paired_t(Plan& P) {
 }
 }  // namespace
 
-Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs) {
+Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs,
+                bool reusable) {
   if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
   if (o.max_iters < 1) fail("sart_solve: max_iters must be >= 1");
   if (o.dtype != SS_F64 && o.dtype != SS_F32) fail("plan: unknown dtype");
@@ -2245,13 +2254,14 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   }
   for (int s = 0; s < P->nsys; ++s) {
     Matrix* a = P->a[s];
-    if (P->paired && s == 1 && P->pair_own[1]) {
-      a->ensure_csc();  // same pattern as a[0]: the stable sort yields the same CSC order
+    if (P->paired && s == 1) {
+      a->csc_like(*P->a[0]);  // same CSR pattern: a[0]'s column ordering, own values
+      P->a[0]->csc_perm.release();
     } else {
-      a->ensure_csc();
+      a->ensure_csc(P->paired && !P->a[1]->has_csc);
     }
     tr.mark("csc");
-    if (o.dtype == SS_F32) a->ensure_f32();
+    if (o.dtype == SS_F32 && !P->paired) a->ensure_f32();  // paired streams convert on build
     tr.mark("f32 copies");
     P->rows[s] = a->rows;
     P->cols[s] = a->cols;
@@ -2321,7 +2331,9 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     tr.mark("paired streams");
   }
   if (P->nsys == 1 && P->empty_rows[0]) fail("sart_solve: matrix has no nonzero rows");
-  P->build_graph();
+  // a reusable plan replays one captured graph; a one-shot solve enqueues its
+  // launches directly (the host stays ahead of the 2*max_iters kernels)
+  if (reusable) P->build_graph();
   tr.mark("graph capture");
   return P.release();
 }

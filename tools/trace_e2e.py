@@ -10,7 +10,7 @@ s = P.build_system(w.scan_config(), ctx=ctx)
 f = P.rasterize(P.random_ellipses(w.seed(), 8), P.make_grid(w.scan_config()), ctx=ctx)
 p = P.forward_project(s.a, f)
 opts = P.SolveOptions(max_iters=w.iters, tol=0.0, relaxation=w.relaxation, dtype=w.dtypes[-1])
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     t = time.perf_counter()
     P.solve_split(P.CentroSystem(s.a, p, 0.0), opts)
     print(f"--- call {rep}: {1e3*(time.perf_counter()-t):.1f} ms", file=sys.stderr, flush=True)
