@@ -236,6 +236,9 @@ int ss_plan_stats(ss_plan_t plan, int64_t* matrix_bytes_per_iter,
 /* matrix bytes each SART kernel streams per launch in this plan's format
  * (paired plans share one index stream between the two folded systems) */
 int ss_plan_kernel_bytes(ss_plan_t plan, int64_t* fwd_bytes, int64_t* back_bytes);
+/* one-line JSON description of the plan's kernels (layout, VS, UF, grid,
+ * kernel names as ncu reports them); NUL-terminated, truncated to cap */
+int ss_plan_describe(ss_plan_t plan, char* buf, int64_t cap);
 /* time `iters` bare iterations of the loop with CUDA events on the context
  * stream (per-kernel split: fwd_ms = forward kernels, back_ms = back kernels) */
 int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms);

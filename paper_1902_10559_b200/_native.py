@@ -115,6 +115,7 @@ SIGNATURES = {
     "ss_plan_stats": (C.c_int, [vp, i64p, i64p, C.POINTER(C.c_int)]),
     "ss_plan_profile": (C.c_int, [vp, C.c_int, fp, fp]),
     "ss_plan_kernel_bytes": (C.c_int, [vp, i64p, i64p]),
+    "ss_plan_describe": (C.c_int, [vp, C.c_char_p, i64]),
     "ss_nccl_unique_id": (C.c_int, [vp]),
     "ss_ctx_attach_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
     "ss_partition_rows": (C.c_int, [i32p, i64, C.c_int, i64p]),

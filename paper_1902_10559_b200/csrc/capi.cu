@@ -846,6 +846,17 @@ int ss_plan_kernel_bytes(ss_plan_t plan, int64_t* fwd_bytes, int64_t* back_bytes
   return guarded([&] { PL(plan)->kernel_bytes(fwd_bytes, back_bytes); });
 }
 
+int ss_plan_describe(ss_plan_t plan, char* buf, int64_t cap) {
+  return guarded([&] {
+    need(buf, "buf");
+    if (cap < 1) ssb::fail("plan_describe: cap must be positive");
+    const std::string d = PL(plan)->describe();
+    const std::size_t n = std::min<std::size_t>(d.size(), static_cast<std::size_t>(cap - 1));
+    std::memcpy(buf, d.data(), n);
+    buf[n] = '\0';
+  });
+}
+
 int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms) {
   return guarded([&] {
     ssb::Plan* P = PL(plan);

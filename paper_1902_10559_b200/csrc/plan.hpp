@@ -73,6 +73,7 @@ struct Plan {
   void profile(int iters, float* fwd_ms, float* back_ms);
   void stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const;
   void kernel_bytes(std::int64_t* fwd, std::int64_t* back) const;
+  std::string describe() const;
 };
 
 Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs,

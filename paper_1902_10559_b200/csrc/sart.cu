@@ -1975,6 +1975,35 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
   if (back) *back = k;
 }
 
+std::string Plan::describe() const {
+  const char* t = dtype == SS_F32 ? "float" : "double";
+  std::string fk, bk;
+  if (sharded || nrhs > 1 || !paired) {
+    fk = nrhs > 1 ? "sart_fwd_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_fwd_kernel");
+    bk = nrhs > 1 ? "sart_back_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_back_kernel");
+  } else {
+    const int tl = tiled ? 1 : 0;
+    fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
+         std::to_string(uf_fwd) + ", " + std::to_string(tl) + ">";
+    bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
+         std::to_string(uf_back) + ", " + std::to_string(tl) + ">";
+  }
+  std::int64_t f = 0, b = 0;
+  kernel_bytes(&f, &b);
+  char buf[768];
+  std::snprintf(buf, sizeof buf,
+                "{\"layout\": \"%s\", \"dtype\": \"%s\", \"nsys\": %d, \"nrhs\": %d, "
+                "\"vs_fwd\": %d, \"uf_fwd\": %d, \"vs_back\": %d, \"uf_back\": %d, "
+                "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
+                "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
+                "\"back_bytes\": %lld, \"graph\": %s}",
+                sharded ? "row-sharded" : (paired ? (tiled ? "paired-tiled" : "paired") : "separate"),
+                t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
+                fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
+                graph ? "true" : "false");
+  return buf;
+}
+
 void Plan::stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const {
   std::int64_t f = 0, k = 0, vb = 0;
   kernel_bytes(&f, &k);

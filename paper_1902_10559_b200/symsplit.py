@@ -648,6 +648,13 @@ class SartPlan:
         _check(_lib().ss_plan_kernel_bytes(self.h, C.byref(f), C.byref(b)))
         return f.value, b.value
 
+    def describe(self) -> dict:
+        """Kernel layout, VS/UF, grid and the kernel names ncu reports."""
+        import json
+        buf = C.create_string_buffer(1024)
+        _check(_lib().ss_plan_describe(self.h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
     def profile(self, iters):
         a, b = C.c_float(), C.c_float()
         _check(_lib().ss_plan_profile(self.h, iters, C.byref(a), C.byref(b)))

@@ -1,10 +1,11 @@
 #!/bin/bash
 # Launch list + one ncu --set full capture of the paired SART kernels (config 3 fp32).
+# Each ncu command runs only after the same command exited 0 without ncu.
 mkdir -p gpurun_out
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain.log; exit 1; }
-ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-    --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --page raw \
+    $CMD > gpurun_out/launches_raw.csv 2> gpurun_out/ncu_launch.err
 ncu --set full --clock-control none --import-source on -k regex:'sart_(fwd|back)_pair' -s 40 -c 4 \
     -o gpurun_out/prof_pair $CMD > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/ncu_full.log
+tail -2 gpurun_out/ncu_full.log
