@@ -45,6 +45,12 @@ struct Plan {
   // paired + tiled: rows/columns padded to 4 entries and permuted within tiles
   // of 4*VS entries so each gather instruction covers consecutive entries
   bool tiled = false;
+  // tiled + 16-bit indices: per tile an int32 base, per entry a uint16 offset
+  bool c16 = false;
+  DBuf<unsigned short> tofs_f, tofs_b;
+  DBuf<int> tbase_f, tbase_b, tfirst_f, tfirst_b;  // per tile base, per vector first tile
+  std::int64_t ntile_f = 0, ntile_b = 0;
+  int layout_mode() const { return !tiled ? 0 : (c16 ? 2 : 1); }
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;

@@ -75,6 +75,12 @@ struct SartK {
   const int* tif;
   const int* tpb;               //               tiled: padded column pointer / indices
   const int* tib;
+  const unsigned short* tof;    //               u16 tiled: offsets / tile bases / first tile (K1)
+  const int* tbf;
+  const int* tff;
+  const unsigned short* tob;    //               u16 tiled (K2)
+  const int* tbb;
+  const int* tfb;
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
@@ -513,6 +519,66 @@ __device__ __forceinline__ void seg_dot2t(const int* __restrict__ idx, const T* 
   acc_b = sb;
 }
 
+// The tiled layout with 16-bit indices: each tile (the VS quads one step of
+// a VS-lane group covers) stores an int32 base (its smallest index) and every
+// entry a uint16 offset from it -- 2 bytes per entry instead of 4 on the
+// stream. Used when every tile of the plan spans < 65536 indices.
+__device__ __forceinline__ int4 decode16(uint2 o, int b) {
+  return make_int4(b + static_cast<int>(o.x & 0xffffu), b + static_cast<int>(o.x >> 16),
+                   b + static_cast<int>(o.y & 0xffffu), b + static_cast<int>(o.y >> 16));
+}
+
+template <class T, int VS, int UF>
+__device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off,
+                                          const int* __restrict__ tbase, int tf,
+                                          const T* __restrict__ v2,
+                                          const typename Vec2<T>::type* __restrict__ xv, int beg,
+                                          int end, int lane, unsigned mask, T& acc_a, T& acc_b) {
+  using T2 = typename Vec2<T>::type;
+  T sa = T(0), sb = T(0);
+  const int nvec = (end - beg) >> 2;
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    uint2 o[UF];
+    int b[UF];
+    T v[UF][8];
+    const int t0 = tf + (q - lane) / VS;
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = beg + ((q + u * VS) << 2);
+      o[u] = __ldg(reinterpret_cast<const uint2*>(off + k0));
+      b[u] = __ldg(tbase + t0 + u);
+      load8(v2 + 2 * k0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int4 c = decode16(o[u], b[u]);
+      const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
+               g3 = __ldg(xv + c.w);
+      sa += v[u][0] * g0.x + v[u][2] * g1.x + v[u][4] * g2.x + v[u][6] * g3.x;
+      sb += v[u][1] * g0.y + v[u][3] * g1.y + v[u][5] * g2.y + v[u][7] * g3.y;
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = beg + (q << 2);
+    const int4 c = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)),
+                            __ldg(tbase + tf + (q - lane) / VS));
+    T v[8];
+    load8(v2 + 2 * k0, v);
+    const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
+             g3 = __ldg(xv + c.w);
+    sa += v[0] * g0.x + v[2] * g1.x + v[4] * g2.x + v[6] * g3.x;
+    sb += v[1] * g0.y + v[3] * g1.y + v[5] * g2.y + v[7] * g3.y;
+  }
+#pragma unroll
+  for (int off2 = VS / 2; off2 > 0; off2 >>= 1) {
+    sa += __shfl_xor_sync(mask, sa, off2, VS);
+    sb += __shfl_xor_sync(mask, sb, off2, VS);
+  }
+  acc_a = sa;
+  acc_b = sb;
+}
+
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
   using T2 = typename Vec2<T>::type;
@@ -523,27 +589,32 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   const int n = static_cast<int>(k.rows0);
-  const int* __restrict__ ptr = TL != 0 ? k.tpf : k.s[0].rp;
+  const int* __restrict__ ptr = TL != 0 ? k.tpf : k.s[0].rp;  // tiled: padded pointer
   int g = static_cast<int>(group);
   const int gend = n, gstep = static_cast<int>(ngroups);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    int beg = 0, end = 0;
+    int beg = 0, end = 0, tf = 0;
     if (g < gend) {
       beg = __ldg(ptr + g);
       end = __ldg(ptr + g + 1);
+      if (TL == 2) tf = __ldg(k.tff + g);
     }
     for (; g < gend; g += gstep) {
       const int gn = g + gstep;
-      int nbeg = 0, nend = 0;
+      int nbeg = 0, nend = 0, ntf = 0;
       if (gn < gend) {  // next row's bounds, ahead of this row's dot product
         nbeg = __ldg(ptr + gn);
         nend = __ldg(ptr + gn + 1);
+        if (TL == 2) ntf = __ldg(k.tff + gn);
       }
       T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      if (TL == 1) {
+      if (TL == 2) {
+        seg_dot2c<T, VS, UF>(k.tof, k.tbf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end,
+                             lane, mask, da, db);
+      } else if (TL == 1) {
         seg_dot2t<T, VS, UF>(k.tif, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
                              mask, da, db);
       } else {
@@ -561,6 +632,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
       }
       beg = nbeg;
       end = nend;
+      tf = ntf;
     }
   }
 #pragma unroll
@@ -598,17 +670,19 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const int* __restrict__ ptr = TL != 0 ? k.tpb : k.s[0].cp;
   int g = static_cast<int>(group);
   const int gend = n, gstep = static_cast<int>(ngroups);
-  int beg = 0, end = 0;
+  int beg = 0, end = 0, tf = 0;
   if (g < gend) {
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
+    if (TL == 2) tf = __ldg(k.tfb + g);
   }
   for (; g < gend; g += gstep) {
     const int gn = g + gstep;
-    int nbeg = 0, nend = 0;
+    int nbeg = 0, nend = 0, ntf = 0;
     if (gn < gend) {
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
+      if (TL == 2) ntf = __ldg(k.tfb + gn);
     }
     T2 xo, ci;
     xo.x = xo.y = ci.x = ci.y = T(0);
@@ -617,7 +691,10 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
     }
     T ua, ub;
-    if (TL == 1) {
+    if (TL == 2) {
+      seg_dot2c<T, VS, UF>(k.tob, k.tbb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end,
+                           lane, mask, ua, ub);
+    } else if (TL == 1) {
       seg_dot2t<T, VS, UF>(k.tib, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane, mask,
                            ua, ub);
     } else {
@@ -633,6 +710,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     }
     beg = nbeg;
     end = nend;
+    tf = ntf;
   }
 }
 
@@ -686,6 +764,58 @@ __global__ void tile_stream_kernel(const int* __restrict__ ptr, const int* __res
       tv2[2 * static_cast<long long>(ob + p)] = a;
       tv2[2 * static_cast<long long>(ob + p) + 1] = b;
     }
+  }
+}
+
+// tiles per vector (tile = 4*VS padded entries) -> counts for the first-tile scan
+__global__ void tile_counts_kernel(const int* __restrict__ tptr, long long n, int tile,
+                                   int* __restrict__ cnt) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    cnt[i] = i < n ? (tptr[i + 1] - tptr[i] + tile - 1) / tile : 0;
+  }
+}
+
+// 16-bit tiled stream (see seg_dot2c): same permutation as tile_stream_kernel;
+// per tile base = its smallest index (the tile's first entry in sorted order),
+// per entry offset = index - base; padding repeats the base. Any offset that
+// does not fit 16 bits raises *overflow (the plan then keeps int32 indices).
+template <class T, class S>
+__global__ void tile_stream16_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                     const S* __restrict__ v0, const S* __restrict__ v1,
+                                     long long nvec, const int* __restrict__ tptr,
+                                     const int* __restrict__ tfirst, unsigned short* __restrict__ tofs,
+                                     int* __restrict__ tbase, T* __restrict__ tv2, int tile,
+                                     int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long s = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+       s < nvec; s += nw) {
+    const int beg = ptr[s], len = ptr[s + 1] - beg;
+    const int ob = tptr[s], lp = tptr[s + 1] - ob;
+    const int tf = tfirst[s];
+    for (int t = lane; t * tile < lp; t += 32) tbase[tf + t] = idx[beg + t * tile];
+    bool bad = false;
+    for (int p = lane; p < lp; p += 32) {
+      const int t0 = (p / tile) * tile;
+      const int r = min(tile, lp - t0) >> 2;
+      const int w = p - t0;
+      const int o = t0 + (w & 3) * r + (w >> 2);
+      const int base = idx[beg + t0];
+      int c = base;
+      T a = T(0), b = T(0);
+      if (o < len) {
+        c = idx[beg + o];
+        a = static_cast<T>(v0[beg + o]);
+        b = static_cast<T>(v1[beg + o]);
+      }
+      const unsigned d = static_cast<unsigned>(c - base);
+      bad |= d > 0xffffu;
+      tofs[ob + p] = static_cast<unsigned short>(d);
+      tv2[2 * static_cast<long long>(ob + p)] = a;
+      tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(overflow, 1);
   }
 }
 
@@ -1446,6 +1576,12 @@ SartK<T> make_args(Plan& P) {
   k.tif = P.tidx_f.get();
   k.tpb = P.tptr_b.get();
   k.tib = P.tidx_b.get();
+  k.tof = P.tofs_f.get();
+  k.tbf = P.tbase_f.get();
+  k.tff = P.tfirst_f.get();
+  k.tob = P.tofs_b.get();
+  k.tbb = P.tbase_b.get();
+  k.tfb = P.tfirst_b.get();
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
@@ -1521,6 +1657,7 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
 #define SSB_PAIR(V, U)                                                                        \
   if (vs == V && uf == U) {                                                                   \
     if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
+    if (P.c16) return fwd ? sart_fwd_pair_kernel<T, V, U, 2> : sart_back_pair_kernel<T, V, U, 2>; \
     return fwd ? sart_fwd_pair_kernel<T, V, U, 1> : sart_back_pair_kernel<T, V, U, 1>;        \
   }
   SSB_PAIR(4, 1) SSB_PAIR(8, 1) SSB_PAIR(16, 1) SSB_PAIR(32, 1)
@@ -1963,8 +2100,13 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
   std::int64_t f = 0, k = 0;
   if (paired) {
     const std::int64_t nf = tiled ? tnnz_f : a[0]->nnz, nb = tiled ? tnnz_b : a[0]->nnz;
-    f = nf * (4 + 2 * b) + 4 * (rows[0] + 1);
-    k = nb * (4 + 2 * b) + 4 * (cols[0] + 1);
+    if (c16) {  // uint16 offsets + int32 tile bases + padded and first-tile pointers
+      f = nf * (2 + 2 * b) + 4 * ntile_f + 8 * (rows[0] + 1);
+      k = nb * (2 + 2 * b) + 4 * ntile_b + 8 * (cols[0] + 1);
+    } else {
+      f = nf * (4 + 2 * b) + 4 * (rows[0] + 1);
+      k = nb * (4 + 2 * b) + 4 * (cols[0] + 1);
+    }
   } else {
     for (int s = 0; s < nsys; ++s) {
       f += a[s]->nnz * (4 + b) + 4 * (rows[s] + 1);
@@ -1982,11 +2124,11 @@ std::string Plan::describe() const {
     fk = nrhs > 1 ? "sart_fwd_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_fwd_kernel");
     bk = nrhs > 1 ? "sart_back_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_back_kernel");
   } else {
-    const int tl = tiled ? 1 : 0;
+    const std::string tl = ", " + std::to_string(layout_mode()) + ">";
     fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
-         std::to_string(uf_fwd) + ", " + std::to_string(tl) + ">";
+         std::to_string(uf_fwd) + tl;
     bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
-         std::to_string(uf_back) + ", " + std::to_string(tl) + ">";
+         std::to_string(uf_back) + tl;
   }
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
@@ -1997,7 +2139,9 @@ std::string Plan::describe() const {
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
                 "\"back_bytes\": %lld, \"graph\": %s}",
-                sharded ? "row-sharded" : (paired ? (tiled ? "paired-tiled" : "paired") : "separate"),
+                sharded ? "row-sharded"
+                        : (paired ? (tiled ? (c16 ? "paired-tiled-u16" : "paired-tiled") : "paired")
+                                  : "separate"),
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 graph ? "true" : "false");
@@ -2191,9 +2335,11 @@ template <class T>
 void build_paired_t(Plan& P) {
   const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
   const std::size_t tb = sizeof(T);
+  if (!P.tiled) P.c16 = false;
   if (P.tiled) {
     if (nnz + 3 * std::max(rows, cols) >= (1LL << 31)) {
       P.tiled = false;  // padded offsets must stay in int32
+      P.c16 = false;
     } else {
       P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
       P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
@@ -2234,17 +2380,64 @@ void build_paired_t(Plan& P) {
     const auto vals = [&](int s, bool csr) -> const double* {
       return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
     };
-    P.tidx_f.alloc(P.tnnz_f);
-    P.tidx_b.alloc(P.tnnz_b);
-    const int gw = static_cast<int>(std::min<long long>(P.ctx->sm_count * 16LL,
-                                                        (std::max(rows, cols) + 7) / 8));
-    tile_stream_kernel<T, double><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
-        P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
-        P.tptr_f.get(), P.tidx_f.get(), rv2, 4 * P.vs_fwd);
-    tile_stream_kernel<T, double><<<std::max(gw, 1), 256, 0, P.ctx->stream>>>(
-        P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
-        P.tptr_b.get(), P.tidx_b.get(), cv2, 4 * P.vs_back);
-    P.ctx->check_launch("tile_stream_kernel");
+    const int gw = std::max(1, static_cast<int>(std::min<long long>(
+                                   P.ctx->sm_count * 16LL, (std::max(rows, cols) + 7) / 8)));
+    if (P.c16) {
+      // per-vector first tile, then 16-bit offsets + per-tile bases; any tile
+      // spanning >= 65536 indices sends the plan back to int32 indices
+      const auto first_tiles = [&](const DBuf<int>& tptr, long long n, int tile,
+                                   DBuf<int>& tfirst) -> std::int64_t {
+        DBuf<int> cnt(n + 1);
+        tfirst.alloc(n + 1);
+        tile_counts_kernel<<<grid1(P.ctx, n + 1), 256, 0, P.ctx->stream>>>(tptr.get(), n, tile,
+                                                                          cnt.get());
+        P.ctx->check_launch("tile_counts_kernel");
+        scan_counts(P.ctx, cnt.get(), tfirst.get(), n);
+        int total = 0;
+        P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
+        return total;
+      };
+      P.ntile_f = first_tiles(P.tptr_f, rows, 4 * P.vs_fwd, P.tfirst_f);
+      P.ntile_b = first_tiles(P.tptr_b, cols, 4 * P.vs_back, P.tfirst_b);
+      P.tofs_f.alloc(P.tnnz_f);
+      P.tofs_b.alloc(P.tnnz_b);
+      P.tbase_f.alloc(P.ntile_f);
+      P.tbase_b.alloc(P.ntile_b);
+      DBuf<int> overflow(1);
+      SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
+      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
+          P.tptr_f.get(), P.tfirst_f.get(), P.tofs_f.get(), P.tbase_f.get(), rv2, 4 * P.vs_fwd,
+          overflow.get());
+      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
+          P.tptr_b.get(), P.tfirst_b.get(), P.tofs_b.get(), P.tbase_b.get(), cv2, 4 * P.vs_back,
+          overflow.get());
+      P.ctx->check_launch("tile_stream16_kernel");
+      int bad = 0;
+      P.ctx->copy(&bad, overflow.get(), sizeof(int));
+      if (bad) {
+        P.c16 = false;
+        P.tofs_f.release();
+        P.tofs_b.release();
+        P.tbase_f.release();
+        P.tbase_b.release();
+        P.tfirst_f.release();
+        P.tfirst_b.release();
+        P.ntile_f = P.ntile_b = 0;
+      }
+    }
+    if (!P.c16) {
+      P.tidx_f.alloc(P.tnnz_f);
+      P.tidx_b.alloc(P.tnnz_b);
+      tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
+          P.tptr_f.get(), P.tidx_f.get(), rv2, 4 * P.vs_fwd);
+      tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
+          P.tptr_b.get(), P.tidx_b.get(), cv2, 4 * P.vs_back);
+      P.ctx->check_launch("tile_stream_kernel");
+    }
   }
   P.ctx->sync();
 }
@@ -2279,6 +2472,7 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     }
     P->paired = true;
     P->tiled = env_int("SSB_TILED", 1) != 0;
+    P->c16 = env_int("SSB_U16", 1) != 0;
     tr.mark("pair pattern");
   }
   for (int s = 0; s < P->nsys; ++s) {
