@@ -46,11 +46,11 @@ struct Plan {
   // of 4*VS entries so each gather instruction covers consecutive entries
   bool tiled = false;
   // tiled + 16-bit indices: per tile an int32 base, per entry a uint16 offset
-  bool c16 = false;
+  bool c16f = false, c16b = false;  // per direction (K1 rows / K2 columns)
   DBuf<unsigned short> tofs_f, tofs_b;
   DBuf<int> tbase_f, tbase_b, tfirst_f, tfirst_b;  // per tile base, per vector first tile
   std::int64_t ntile_f = 0, ntile_b = 0;
-  int layout_mode() const { return !tiled ? 0 : (c16 ? 2 : 1); }
+  int layout_mode(bool fwd) const { return !tiled ? 0 : ((fwd ? c16f : c16b) ? 2 : 1); }
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;

@@ -1657,7 +1657,8 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
 #define SSB_PAIR(V, U)                                                                        \
   if (vs == V && uf == U) {                                                                   \
     if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
-    if (P.c16) return fwd ? sart_fwd_pair_kernel<T, V, U, 2> : sart_back_pair_kernel<T, V, U, 2>; \
+    if (fwd ? P.c16f : P.c16b)                                                                \
+      return fwd ? sart_fwd_pair_kernel<T, V, U, 2> : sart_back_pair_kernel<T, V, U, 2>;      \
     return fwd ? sart_fwd_pair_kernel<T, V, U, 1> : sart_back_pair_kernel<T, V, U, 1>;        \
   }
   SSB_PAIR(4, 1) SSB_PAIR(8, 1) SSB_PAIR(16, 1) SSB_PAIR(32, 1)
@@ -2100,13 +2101,11 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
   std::int64_t f = 0, k = 0;
   if (paired) {
     const std::int64_t nf = tiled ? tnnz_f : a[0]->nnz, nb = tiled ? tnnz_b : a[0]->nnz;
-    if (c16) {  // uint16 offsets + int32 tile bases + padded and first-tile pointers
-      f = nf * (2 + 2 * b) + 4 * ntile_f + 8 * (rows[0] + 1);
-      k = nb * (2 + 2 * b) + 4 * ntile_b + 8 * (cols[0] + 1);
-    } else {
-      f = nf * (4 + 2 * b) + 4 * (rows[0] + 1);
-      k = nb * (4 + 2 * b) + 4 * (cols[0] + 1);
-    }
+    // uint16 offsets + int32 tile bases + padded and first-tile pointers, or int32 indices
+    f = c16f ? nf * (2 + 2 * b) + 4 * ntile_f + 8 * (rows[0] + 1)
+             : nf * (4 + 2 * b) + 4 * (rows[0] + 1);
+    k = c16b ? nb * (2 + 2 * b) + 4 * ntile_b + 8 * (cols[0] + 1)
+             : nb * (4 + 2 * b) + 4 * (cols[0] + 1);
   } else {
     for (int s = 0; s < nsys; ++s) {
       f += a[s]->nnz * (4 + b) + 4 * (rows[s] + 1);
@@ -2124,11 +2123,10 @@ std::string Plan::describe() const {
     fk = nrhs > 1 ? "sart_fwd_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_fwd_kernel");
     bk = nrhs > 1 ? "sart_back_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_back_kernel");
   } else {
-    const std::string tl = ", " + std::to_string(layout_mode()) + ">";
     fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
-         std::to_string(uf_fwd) + tl;
+         std::to_string(uf_fwd) + ", " + std::to_string(layout_mode(true)) + ">";
     bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
-         std::to_string(uf_back) + tl;
+         std::to_string(uf_back) + ", " + std::to_string(layout_mode(false)) + ">";
   }
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
@@ -2140,7 +2138,7 @@ std::string Plan::describe() const {
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
                 "\"back_bytes\": %lld, \"graph\": %s}",
                 sharded ? "row-sharded"
-                        : (paired ? (tiled ? (c16 ? "paired-tiled-u16" : "paired-tiled") : "paired")
+                        : (paired ? (tiled ? (c16f || c16b ? "paired-tiled-u16" : "paired-tiled") : "paired")
                                   : "separate"),
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
@@ -2335,11 +2333,11 @@ template <class T>
 void build_paired_t(Plan& P) {
   const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
   const std::size_t tb = sizeof(T);
-  if (!P.tiled) P.c16 = false;
+  if (!P.tiled) P.c16f = P.c16b = false;
   if (P.tiled) {
     if (nnz + 3 * std::max(rows, cols) >= (1LL << 31)) {
       P.tiled = false;  // padded offsets must stay in int32
-      P.c16 = false;
+      P.c16f = P.c16b = false;
     } else {
       P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
       P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
@@ -2382,12 +2380,24 @@ void build_paired_t(Plan& P) {
     };
     const int gw = std::max(1, static_cast<int>(std::min<long long>(
                                    P.ctx->sm_count * 16LL, (std::max(rows, cols) + 7) / 8)));
-    if (P.c16) {
-      // per-vector first tile, then 16-bit offsets + per-tile bases; any tile
-      // spanning >= 65536 indices sends the plan back to int32 indices
-      const auto first_tiles = [&](const DBuf<int>& tptr, long long n, int tile,
-                                   DBuf<int>& tfirst) -> std::int64_t {
-        DBuf<int> cnt(n + 1);
+    // per direction: 16-bit offsets + per-tile bases when every tile spans
+    // < 65536 indices (overflow flag from the build), else int32 indices
+    const auto build_dir = [&](bool fwd) {
+      const Matrix& m = *P.a[0];
+      const int* ptr = fwd ? m.rowptr.get() : m.colptr.get();
+      const int* idx = fwd ? m.colidx.get() : m.rowidx.get();
+      const long long n = fwd ? rows : cols;
+      const int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
+      const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
+      const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
+      T* v2 = fwd ? rv2 : cv2;
+      bool& u16 = fwd ? P.c16f : P.c16b;
+      if (u16) {
+        DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
+        DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
+        DBuf<int>& tbase = fwd ? P.tbase_f : P.tbase_b;
+        std::int64_t& ntile = fwd ? P.ntile_f : P.ntile_b;
+        DBuf<int> cnt(n + 1), overflow(1);
         tfirst.alloc(n + 1);
         tile_counts_kernel<<<grid1(P.ctx, n + 1), 256, 0, P.ctx->stream>>>(tptr.get(), n, tile,
                                                                           cnt.get());
@@ -2395,49 +2405,31 @@ void build_paired_t(Plan& P) {
         scan_counts(P.ctx, cnt.get(), tfirst.get(), n);
         int total = 0;
         P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
-        return total;
-      };
-      P.ntile_f = first_tiles(P.tptr_f, rows, 4 * P.vs_fwd, P.tfirst_f);
-      P.ntile_b = first_tiles(P.tptr_b, cols, 4 * P.vs_back, P.tfirst_b);
-      P.tofs_f.alloc(P.tnnz_f);
-      P.tofs_b.alloc(P.tnnz_b);
-      P.tbase_f.alloc(P.ntile_f);
-      P.tbase_b.alloc(P.ntile_b);
-      DBuf<int> overflow(1);
-      SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
-      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
-          P.tptr_f.get(), P.tfirst_f.get(), P.tofs_f.get(), P.tbase_f.get(), rv2, 4 * P.vs_fwd,
-          overflow.get());
-      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
-          P.tptr_b.get(), P.tfirst_b.get(), P.tofs_b.get(), P.tbase_b.get(), cv2, 4 * P.vs_back,
-          overflow.get());
-      P.ctx->check_launch("tile_stream16_kernel");
-      int bad = 0;
-      P.ctx->copy(&bad, overflow.get(), sizeof(int));
-      if (bad) {
-        P.c16 = false;
-        P.tofs_f.release();
-        P.tofs_b.release();
-        P.tbase_f.release();
-        P.tbase_b.release();
-        P.tfirst_f.release();
-        P.tfirst_b.release();
-        P.ntile_f = P.ntile_b = 0;
+        ntile = total;
+        tofs.alloc(tn);
+        tbase.alloc(ntile);
+        SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
+        tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
+            tbase.get(), v2, tile, overflow.get());
+        P.ctx->check_launch("tile_stream16_kernel");
+        int bad = 0;
+        P.ctx->copy(&bad, overflow.get(), sizeof(int));
+        if (!bad) return;
+        u16 = false;
+        tofs.release();
+        tbase.release();
+        tfirst.release();
+        ntile = 0;
       }
-    }
-    if (!P.c16) {
-      P.tidx_f.alloc(P.tnnz_f);
-      P.tidx_b.alloc(P.tnnz_b);
+      DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
+      tidx.alloc(tn);
       tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          P.a[0]->rowptr.get(), P.a[0]->colidx.get(), vals(0, true), vals(1, true), rows,
-          P.tptr_f.get(), P.tidx_f.get(), rv2, 4 * P.vs_fwd);
-      tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          P.a[0]->colptr.get(), P.a[0]->rowidx.get(), vals(0, false), vals(1, false), cols,
-          P.tptr_b.get(), P.tidx_b.get(), cv2, 4 * P.vs_back);
+          ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tidx.get(), v2, tile);
       P.ctx->check_launch("tile_stream_kernel");
-    }
+    };
+    build_dir(true);
+    build_dir(false);
   }
   P.ctx->sync();
 }
@@ -2472,7 +2464,7 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     }
     P->paired = true;
     P->tiled = env_int("SSB_TILED", 1) != 0;
-    P->c16 = env_int("SSB_U16", 1) != 0;
+    P->c16f = P->c16b = env_int("SSB_U16", 1) != 0;
     tr.mark("pair pattern");
   }
   for (int s = 0; s < P->nsys; ++s) {

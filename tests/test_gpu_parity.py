@@ -328,3 +328,40 @@ def test_sharded_plan_single_rank_nccl():
         tol = 1e-12 if dtype == "f64" else 1e-5
         assert rel_err(sh.solution(0), ref.solution(0)) <= tol
         assert np.allclose(sh.history(0), ref.history(0), rtol=tol)
+
+
+# ------------------------------------------------------------------ paired-stream layouts
+def _wide_centro(seed, mh, nh, per_row, span):
+    """Random centrosymmetric sparse system whose rows reach `span` columns apart
+    (forces the 16-bit tiled index stream back to int32 when span >= 65536)."""
+    rng = np.random.default_rng(seed)
+    m, n = 2 * mh, 2 * nh
+    r, c, v = [], [], []
+    for i in range(mh):
+        lo = int(rng.integers(0, max(1, n - span)))
+        cols = np.unique(rng.integers(lo, min(n, lo + span), per_row))
+        vals = rng.uniform(0.1, 1.0, len(cols))
+        r += [i] * len(cols) + [m - 1 - i] * len(cols)
+        c += list(cols) + list(n - 1 - cols)
+        v += list(vals) + list(vals)
+    p = rng.uniform(0.5, 1.5, m)
+    return m, n, np.array(r), np.array(c), np.array(v), p
+
+
+@pytest.mark.parametrize("span,per_row", [(3000, 150), (200000, 8)])
+def test_paired_tiled_layouts_match_oracle(span, per_row):
+    m, n, r, c, v, p = _wide_centro(7 + span, 96, 120000, per_row, span)
+    a = P.Matrix.from_triplets(m, n, r, c, v)
+    sys_ = P.CentroSystem(a, p, 0.0)
+    split = P.split_system(sys_)
+    plan = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0))
+    d = plan.describe()
+    assert d["layout"].startswith("paired-tiled")
+    # K2 (columns list rows < 96) always fits 16 bits; K1 falls back for wide rows
+    assert d["back_kernel"].endswith(", 2>")
+    assert d["fwd_kernel"].endswith(", 2>" if span < 65536 else ", 1>")
+    got = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
+    ref = O.solve_split(O.Matrix.triplets(m, n, r, c, v), p, 0.0, 12, 0.0, 1.0)
+    assert rel_err(got.f, ref.f) <= TOL_F64
+    got32 = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0, dtype="f32"))
+    assert rel_err(got32.f, ref.f) <= TOL_F32
