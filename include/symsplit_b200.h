@@ -67,6 +67,7 @@ typedef struct {
 /* iterative methods on the device (reference Method, solvers.hpp:14) */
 #define SS_METHOD_SART 0
 #define SS_METHOD_CGLS 1
+#define SS_METHOD_DENSE 2 /* Method::dense_minnorm (pseudo_solve_dense) */
 
 /* replaces SolveOptions (solvers.hpp:19-27) */
 typedef struct {
@@ -75,7 +76,8 @@ typedef struct {
   double relaxation;  /* default 1.0, in (0, 2] (SART only)    */
   int parallelism;    /* accepted for parity; results never depend on it */
   int dtype;          /* SS_F64 (reference) or SS_F32          */
-  int method;         /* SS_METHOD_SART (default) or SS_METHOD_CGLS */
+  int method;         /* SS_METHOD_SART (default), SS_METHOD_CGLS or SS_METHOD_DENSE */
+  int64_t dense_cap;  /* rows*cols guard of the dense path; 0 = reference default 5e7 */
 } ss_solve_options;
 
 /* replaces SolveReport scalars (solvers.hpp:29-45) */
@@ -176,7 +178,12 @@ int ss_sart_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_opti
  * for max_iters entries */
 int ss_cgls_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
                   double* f, int64_t n, ss_solve_report* report, double* history);
-/* replaces solve_split (solvers.cpp:207-269) with method = sart or cgls */
+/* replaces pseudo_solve_dense (solvers.cpp:81-97): minimum-norm solution via
+ * the SVD pseudo-inverse at the reference threshold max(m,n)*eps; refuses
+ * rows*cols > dense_cap with the reference message */
+int ss_pseudo_solve_dense(ss_matrix_t a, const double* p, int64_t m, int64_t dense_cap,
+                          double* f, int64_t n);
+/* replaces solve_split (solvers.cpp:207-269) with method = sart, cgls or dense */
 int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_tol,
                    const ss_solve_options* opts, double* f, int64_t n,
                    ss_solve_report* report);

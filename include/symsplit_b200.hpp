@@ -9,9 +9,10 @@
 //    std::vector<double>; Matrix is a device-resident sparse matrix handle
 //    (construct from compressed-column arrays, triplets or a dense
 //    column-major array);
-//  * only Method::sart is available (dense min-norm and CGLS are not on the
-//    B200 path); SolveOptions gains `dtype` (fp64 = reference arithmetic,
-//    fp32 = the bandwidth-halving variant);
+//  * Method::sart (the default here; the reference defaults to dense_minnorm),
+//    Method::cgls and Method::dense_minnorm all run on the device;
+//    SolveOptions gains `dtype` (fp64 = reference arithmetic, fp32 = the
+//    bandwidth-halving variant; SART only);
 //  * every call runs on the GPU of the Context it was created on.
 #pragma once
 
@@ -241,11 +242,11 @@ struct SolveReport {
 
 namespace detail {
 inline ss_solve_options to_c(const SolveOptions& o) {
-  if (o.method == Method::dense_minnorm) {
-    throw Error("Method::dense_minnorm is not on the B200 path (use sart or cgls)");
-  }
-  return ss_solve_options{o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype,
-                          o.method == Method::cgls ? SS_METHOD_CGLS : SS_METHOD_SART};
+  const int m = o.method == Method::cgls ? SS_METHOD_CGLS
+                                         : (o.method == Method::dense_minnorm ? SS_METHOD_DENSE
+                                                                              : SS_METHOD_SART);
+  return ss_solve_options{o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype, m,
+                          o.dense_cap};
 }
 inline SolveReport from_c(Vector f, const ss_solve_report& r, Mode mode) {
   SolveReport rep;
@@ -346,9 +347,28 @@ inline SolveReport cgls_solve(const Matrix& a, const Vector& p, const SolveOptio
   return rep;
 }
 
+// reference pseudo_solve_dense (solvers.cpp:81-97)
+inline Vector pseudo_solve_dense(const Matrix& a, const Vector& p,
+                                 std::int64_t dense_cap = 50'000'000) {
+  Vector f(static_cast<std::size_t>(a.cols()));
+  detail::check(ss_pseudo_solve_dense(a.get(), p.data(), static_cast<int64_t>(p.size()),
+                                      dense_cap, f.data(), static_cast<int64_t>(f.size())));
+  return f;
+}
+
 inline SolveReport solve_direct(const CentroSystem& sys, const SolveOptions& opts) {
-  return opts.method == Method::cgls ? cgls_solve(sys.a, sys.p, opts)
-                                     : sart_solve(sys.a, sys.p, opts);
+  if (opts.method == Method::cgls) return cgls_solve(sys.a, sys.p, opts);
+  if (opts.method == Method::dense_minnorm) {
+    const ss_solve_options c = detail::to_c(opts);
+    Vector f(static_cast<std::size_t>(sys.a.cols()));
+    ss_solve_report r{};
+    detail::check(ss_solve_direct(sys.a.get(), sys.p.data(), static_cast<int64_t>(sys.p.size()),
+                                  &c, f.data(), static_cast<int64_t>(f.size()), &r));
+    SolveReport rep = detail::from_c(std::move(f), r, Mode::direct);
+    rep.method = Method::dense_minnorm;
+    return rep;
+  }
+  return sart_solve(sys.a, sys.p, opts);
 }
 
 inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts) {

@@ -391,6 +391,35 @@ def solve_split_prepared(a1: Matrix, a2: Matrix, p1, p2, max_iters, tol, relaxat
     return f, it.value, t4
 
 
+# ----------------------------------------------------------------- dense min-norm
+def pinv_solve(a, b):
+    """tests/support/oracles.hpp:101-113 restated with numpy's SVD: the reference's
+    own oracle for pseudo_solve_dense (test_solvers.cpp:72-84 pins the
+    implementation to it within 1e-10). Cutoff max(m,n)*eps*s_0."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    m, n = a.shape
+    if m == 0 or n == 0:
+        return np.zeros(n)
+    u, s, vt = np.linalg.svd(a, full_matrices=False)
+    cutoff = max(m, n) * np.finfo(np.float64).eps * (s[0] if s.size else 0.0)
+    y = u.T @ b
+    y = np.where(s > cutoff, y / np.where(s > cutoff, s, 1.0), 0.0)
+    return vt.T @ y
+
+
+def random_with_rank(m, n, rank, rng):
+    """tests/support/oracles.hpp:70-85 (numpy Generator instead of the Rng):
+    Q_u diag(sigma, sigma ~ U[0.5,1.5] on `rank` entries) Q_v^T."""
+    qu, _ = np.linalg.qr(rng.uniform(-1, 1, (m, m)))
+    qv, _ = np.linalg.qr(rng.uniform(-1, 1, (n, n)))
+    k = min(m, n)
+    s = np.zeros((m, n))
+    r = min(rank, k)
+    s[np.arange(r), np.arange(r)] = rng.uniform(0.5, 1.5, r)
+    return qu @ s @ qv.T
+
+
 # ----------------------------------------------------------------- geometry
 def scan_config(k, gamma, h_e, h_m, l_m, n_p, obj_size, grid_nx, grid_ny, a_e=7e-4):
     return ScanConfigC(k, gamma, h_e, h_m, l_m, n_p, a_e, obj_size, grid_nx, grid_ny)

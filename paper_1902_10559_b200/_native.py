@@ -40,7 +40,8 @@ class GridSpec(C.Structure):
 
 class SolveOptionsC(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("tol", C.c_double), ("relaxation", C.c_double),
-                ("parallelism", C.c_int), ("dtype", C.c_int), ("method", C.c_int)]
+                ("parallelism", C.c_int), ("dtype", C.c_int), ("method", C.c_int),
+                ("dense_cap", C.c_int64)]
 
 
 class SolveReportC(C.Structure):
@@ -92,6 +93,7 @@ SIGNATURES = {
     "ss_recombine_solution": (C.c_int, [vp, dp, dp, i64, dp]),
     "ss_sart_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
                                 C.POINTER(SolveReportC), dp]),
+    "ss_pseudo_solve_dense": (C.c_int, [vp, dp, i64, i64, dp, i64]),
     "ss_cgls_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
                                 C.POINTER(SolveReportC), dp]),
     "ss_solve_split": (C.c_int, [vp, dp, i64, C.c_double, C.POINTER(SolveOptionsC), dp, i64,

@@ -92,6 +92,11 @@ void check_system(std::int64_t rows, const double* p, std::int64_t m, const char
   }
 }
 
+// reference SolveOptions::dense_cap default (solvers.hpp:26); 0 = that default
+std::int64_t effective_dense_cap(const ss_solve_options& o) {
+  return o.dense_cap > 0 ? o.dense_cap : 50000000;
+}
+
 void check_options(const ss_solve_options& o) {
   if (o.relaxation <= 0 || o.relaxation > 2) ssb::fail("sart_solve: relaxation must be in (0, 2]");
   if (o.max_iters < 1) ssb::fail("sart_solve: max_iters must be >= 1");
@@ -234,6 +239,7 @@ int ss_ctx_destroy(ss_ctx_t h) {
     ssb::alloc_stream() = ctx->stream;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) ssb::nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+    ssb::release_solver(ctx);
     ctx->scratch.release();
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -529,9 +535,44 @@ int ss_cgls_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_opti
   });
 }
 
+int ss_pseudo_solve_dense(ss_matrix_t a, const double* p, int64_t m, int64_t dense_cap,
+                          double* f, int64_t n) {
+  return guarded([&] {
+    ssb::Matrix* A = M(a);
+    ssb::Context* c = A->ctx;
+    use_device(c);
+    need(f, "f");
+    check_system(A->rows, p, m, "pseudo_solve_dense");
+    if (n != A->cols) ssb::fail("pseudo_solve_dense: solution length does not match columns");
+    auto dp = to_device(c, p, m);
+    ssb::DBuf<double> fd(std::max<int64_t>(n, 1));
+    ssb::pseudo_solve_dense_dev(*A, dp.get(), fd.get(), dense_cap);
+    to_host(c, f, fd.get(), n);
+  });
+}
+
 int ss_solve_direct(ss_matrix_t a, const double* p, int64_t m, const ss_solve_options* opts,
                     double* f, int64_t n, ss_solve_report* report) {
   if (opts && opts->method == SS_METHOD_CGLS) return ss_cgls_solve(a, p, m, opts, f, n, report, nullptr);
+  if (opts && opts->method == SS_METHOD_DENSE) {
+    // run_method's dense branch (solvers.cpp:40-48): f, wall time, residual, norms
+    return guarded([&] {
+      ssb::Matrix* A = M(a);
+      ssb::Context* c = A->ctx;
+      use_device(c);
+      check_system(A->rows, p, m, "pseudo_solve_dense");
+      if (n != A->cols) ssb::fail("pseudo_solve_dense: solution length does not match columns");
+      auto dp = to_device(c, p, m);
+      ssb::DBuf<double> fd(std::max<int64_t>(n, 1));
+      const double t0 = now();
+      ssb::pseudo_solve_dense_dev(*A, dp.get(), fd.get(), effective_dense_cap(*opts));
+      ss_solve_report rep{};
+      rep.wall_time_seconds = now() - t0;
+      to_host(c, f, fd.get(), n);
+      fill_report(*A, fd.get(), dp.get(), &rep);
+      if (report) *report = rep;
+    });
+  }
   return ss_sart_solve(a, p, m, opts, f, n, report, nullptr);
 }
 
@@ -567,11 +608,15 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     const std::int64_t mh = m / 2;
     std::vector<double> hp(static_cast<std::size_t>(mh));
     const bool cgls = opts->method == SS_METHOD_CGLS;
+    const bool dense = opts->method == SS_METHOD_DENSE;
     for (int s = 0; s < 2; ++s) {
       to_host(c, hp.data(), (s ? o.p2 : o.p1).get(), mh);
       try {
-        check_system(o.a1->rows, hp.data(), mh, cgls ? "cgls_solve" : "sart_solve");
-        if (cgls) {
+        check_system(o.a1->rows, hp.data(), mh,
+                     cgls ? "cgls_solve" : (dense ? "pseudo_solve_dense" : "sart_solve"));
+        if (dense) {
+          // no options to validate (solvers.cpp:81-97)
+        } else if (cgls) {
           if (opts->tol <= 0) ssb::fail("cgls_solve: tol must be positive");
           if (opts->max_iters < 1) ssb::fail("cgls_solve: max_iters must be >= 1");
         } else {
@@ -583,15 +628,22 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     }
     raise_if_failed(SS_ERR_INVALID);
     tr.mark("branch validation");
-    if (cgls) {
+    if (cgls || dense) {
       // both branches on the device, failures aggregated like the reference
-      ssb::DBuf<double> f1(n / 2), f2(n / 2);
+      ssb::DBuf<double> f1(std::max<int64_t>(n / 2, 1)), f2(std::max<int64_t>(n / 2, 1));
       ss_solve_report rb[2] = {};
       int code = SS_OK;
       for (int s = 0; s < 2; ++s) {
         try {
-          ssb::cgls_device(s ? *o.a2 : *o.a1, (s ? o.p2 : o.p1).get(), *opts,
-                           (s ? f2 : f1).get(), &rb[s], nullptr);
+          if (dense) {
+            const double tb = now();
+            ssb::pseudo_solve_dense_dev(s ? *o.a2 : *o.a1, (s ? o.p2 : o.p1).get(),
+                                        (s ? f2 : f1).get(), effective_dense_cap(*opts));
+            rb[s].wall_time_seconds = now() - tb;
+          } else {
+            ssb::cgls_device(s ? *o.a2 : *o.a1, (s ? o.p2 : o.p1).get(), *opts,
+                             (s ? f2 : f1).get(), &rb[s], nullptr);
+          }
         } catch (const ssb::Failure& e) {
           errs[s] = e.what();
           code = e.code;

@@ -102,6 +102,7 @@ struct Context {
   // NCCL (row-sharded plans); opaque to avoid the header here
   void* comm = nullptr;
   int nranks = 1, rank = 0;
+  void* solver = nullptr;  // cuSOLVER handle (dense min-norm path), created on first use
 
   void* temp(std::size_t bytes) {
     if (scratch.size() < bytes) scratch.alloc(bytes + bytes / 4);
@@ -213,6 +214,9 @@ ss_symmetry_report verify_symmetry(Matrix& a, double tol);
 void fold(Matrix& a, Matrix*& a1, Matrix*& a2);
 bool same_pattern(Matrix& a, Matrix& b);
 void scan_counts(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n);
+// dense minimum-norm solve of a (reference pseudo_solve_dense), p and f on the device
+void pseudo_solve_dense_dev(Matrix& a, const double* p, double* f, std::int64_t dense_cap);
+void release_solver(Context* ctx);
 void union_pattern(Matrix& a, Matrix& b, Matrix*& ua, Matrix*& ub);
 void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh);
 void recombine_dev(Context* ctx, const double* f1, const double* f2, double* f,

@@ -299,25 +299,25 @@ class SolutionPair:
 
 @dataclass
 class SolveOptions:
-    """reference SolveOptions (solvers.hpp:19-27); method is SART."""
+    """reference SolveOptions (solvers.hpp:19-27). The default method here is
+    SART (the B200 product path); the reference's default is dense_minnorm."""
     max_iters: int = 200
     tol: float = 1e-10
     relaxation: float = 1.0
     parallelism: int = 0
     dtype: str = "f64"  # "f64" (reference arithmetic) or "f32"
-    method: str = "sart"
+    method: str = "sart"  # "sart", "cgls", "dense" / "dense_minnorm"
+    dense_cap: int = 50_000_000
 
     def _c(self):
-        if self.method not in ("sart", "cgls"):
-            # solvers.cpp:28-33 method_from_name; dense min-norm is not on the B200 path
-            raise Error(f"unknown method name: {self.method}" if self.method not in
-                        ("dense", "dense_minnorm") else
-                        f"method {self.method} is not on the B200 path")
+        codes = {"sart": 0, "cgls": 1, "dense": 2, "dense_minnorm": 2}
+        if self.method not in codes:
+            raise Error(f"unknown method name: {self.method}")  # solvers.cpp:73-78
         if self.dtype not in ("f64", "f32"):
             raise Error("dtype must be 'f64' or 'f32'")
         return N.SolveOptionsC(int(self.max_iters), float(self.tol), float(self.relaxation),
                                int(self.parallelism), N.SS_F64 if self.dtype == "f64" else N.SS_F32,
-                               1 if self.method == "cgls" else 0)
+                               codes[self.method], int(self.dense_cap))
 
 
 @dataclass
@@ -431,11 +431,30 @@ def cgls_solve(a: Matrix, p, opts: Optional[SolveOptions] = None) -> SolveReport
     return rep
 
 
+def pseudo_solve_dense(a: Matrix, p, dense_cap: int = 50_000_000):
+    """solvers.cpp:81-97: minimum-norm solution (device SVD pseudo-inverse at the
+    reference threshold max(m,n)*eps); refuses rows*cols > dense_cap."""
+    p = _f64(p)
+    f = np.empty(a.shape[1])
+    _check(_lib().ss_pseudo_solve_dense(a.h, _dp(p), len(p), int(dense_cap), _dp(f), len(f)))
+    return f
+
+
 def solve_direct(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> SolveReport:
-    """solvers.cpp:201-205 (method = sart or cgls)"""
+    """solvers.cpp:201-205 (method = sart, cgls or dense)"""
     opts = opts or SolveOptions()
     if opts.method == "cgls":
         return cgls_solve(sys.a, sys.p, opts)
+    if opts.method in ("dense", "dense_minnorm"):
+        p = _f64(sys.p)
+        f = np.empty(sys.a.shape[1])
+        r = N.SolveReportC()
+        o = opts._c()
+        _check(_lib().ss_solve_direct(sys.a.h, _dp(p), len(p), C.byref(o), _dp(f), len(f),
+                                      C.byref(r)))
+        rep = _report(f, r, "direct")
+        rep.method = "dense"
+        return rep
     return sart_solve(sys.a, sys.p, opts)
 
 
@@ -454,7 +473,7 @@ def solve_split(sys: CentroSystem, opts: Optional[SolveOptions] = None) -> Solve
         raise SymmetryError(msg, verify_symmetry(sys.a, sys.symmetry_tol))
     _check(rc)
     rep = _report(f, r, "split")
-    rep.method = opts.method
+    rep.method = "dense" if opts.method == "dense_minnorm" else opts.method
     return rep
 
 
