@@ -18,13 +18,7 @@ struct Plan {
   bool sharded = false;
   bool paired = false;  // folded pair on one shared index stream
   Matrix* pair_own[2] = {nullptr, nullptr};  // union-pattern copies (when patterns differ)
-  bool stream = false;  // work-table kernels (mode 1 TMA ring, mode 2 flat stream)
-  int mode = 0;
-  int q_fwd = 4, q_back = 4;  // flat kernels: entries per lane per batch
   int sys_blocks_f = 0x7fffffff, sys_blocks_b = 0x7fffffff;  // first CTA of system 1
-  int u_fwd = 4, u_back = 4;
-  int nwork_f = 0, nwork_b = 0;
-  DBuf<int2> work_f, work_b;  // per-warp [begin, end) vector ranges
   std::int64_t row_begin = 0, row_end = 0;  // sharded: rows kept by this rank
   ss_solve_options opts{};
   Matrix* a[2] = {nullptr, nullptr};

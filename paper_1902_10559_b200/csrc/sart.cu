@@ -64,7 +64,7 @@ struct SartK {
   int hstride;
   int* state;                   // [nsys*nrhs][4]
   unsigned* ticket;
-  int sys_blocks[2];            // flat kernels: first CTA of system 1 (fwd, back)
+  int sys_blocks[2];            // CTA-uniform dispatch: first CTA of system 1 (fwd, back)
   T* xx;                        // paired plans: iterates interleaved [cols][2]
   T* ww;                        //               weighted residuals [rows][2]
   const T* rv2;                 //               CSR values interleaved [nnz][2]
@@ -827,436 +827,6 @@ __global__ void pad4_counts_kernel(const int* __restrict__ ptr, long long n, int
   }
 }
 
-// ------------------------------------------------------------ TMA-streamed kernels
-// Each warp owns a contiguous, nnz-balanced range of compressed vectors (rows
-// for K1, columns for K2), hence one contiguous byte range of the index and
-// value arrays. Lane 0 streams that range into a per-warp shared-memory ring
-// of kChunks chunks with 1-D bulk TMA (cp.async.bulk ... complete_tx on an
-// mbarrier per slot), kChunks-1 chunks ahead of consumption, so the DRAM
-// stream never waits on the dependent x/w gathers. Lanes read the ring
-// lane-strided (conflict-free), gather the dense vector through L1/L2 and
-// reduce each compressed vector with a fixed-order butterfly.
-constexpr int kStreamWarps = 16;   // warps per CTA (512 threads, 1 CTA per SM)
-constexpr int kChunk = 256;        // entries per TMA chunk (power of two)
-constexpr int kChunks = 4;         // ring slots per warp
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// 1-D bulk copy global -> shared, completion counted in bytes on `bar`;
-// evict-first in L2 so the streamed matrix does not displace the gathered
-// vectors.
-__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-template <class T>
-struct StreamSmem {
-  static constexpr int kRingBytes = kChunks * kChunk * (4 + static_cast<int>(sizeof(T)));
-  static constexpr int kBytes = kStreamWarps * (kChunks * 8 + kRingBytes);
-};
-
-template <class T, bool FWD, int U>
-__global__ void __launch_bounds__(kStreamWarps * 32, 1)
-    sart_stream_kernel(SartK<T> k, const int2* __restrict__ work, int nwork, int it) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double red[2][kStreamWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kStreamWarps + warp;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * kChunks;
-  int* ring_i = reinterpret_cast<int*>(smem + kStreamWarps * kChunks * 8 +
-                                       warp * StreamSmem<T>::kRingBytes);
-  T* ring_v = reinterpret_cast<T*>(ring_i + kChunks * kChunk);
-  double r2 = 0.0;
-  int sys = 0;
-  if (gw < nwork) {
-    const int2 wk = work[gw];
-    const long long split = FWD ? k.rows0 : k.cols0;
-    sys = wk.x >= split ? 1 : 0;
-    const SysK<T>& S = k.s[sys];
-    if (wk.y > wk.x && sys_on(k.state, sys)) {
-      const int i0 = static_cast<int>(wk.x - (sys ? split : 0));
-      const int i1 = static_cast<int>(wk.y - (sys ? split : 0));
-      const int* __restrict__ ptr = FWD ? S.rp : S.cp;
-      const int* __restrict__ idx = FWD ? S.ci : S.ri;
-      const T* __restrict__ val = FWD ? S.rv : S.cv;
-      const T* __restrict__ vec = FWD ? S.x : S.w;
-      const int kfirst = __ldg(ptr + i0), klast = __ldg(ptr + i1);
-      const int kb = kfirst & ~3;
-      const int ke = (klast + 3) & ~3;
-      const int nch = (ke - kb + kChunk - 1) / kChunk;
-      const uint64_t pol = evict_first_policy();
-      if (lane == 0) {
-        for (int c = 0; c < kChunks; ++c) mbar_init(&bars[c], 1);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      }
-      __syncwarp();
-      auto issue = [&](int c) {  // lane 0 only
-        const int slot = c % kChunks;
-        const int start = kb + c * kChunk;
-        const int len = min(kChunk, ke - start);
-        const uint32_t bi = static_cast<uint32_t>(len) * 4u;
-        const uint32_t bv = static_cast<uint32_t>(len) * static_cast<uint32_t>(sizeof(T));
-        mbar_expect_tx(&bars[slot], bi + bv);
-        tma_load(ring_i + slot * kChunk, idx + start, bi, &bars[slot], pol);
-        tma_load(ring_v + slot * kChunk, val + start, bv, &bars[slot], pol);
-      };
-      if (lane == 0) {
-        for (int c = 0; c < min(kChunks, nch); ++c) issue(c);
-      }
-      int ready = 0;  // chunks known complete
-      int freed = 0;  // chunks released back to the producer
-      for (int b0 = i0; b0 < i1; b0 += 31) {
-        const int nb = min(31, i1 - b0);
-        const int pv = lane <= nb ? __ldg(ptr + b0 + lane) : 0;
-        // epilogue operands of row/column b0+lane, prefetched for the batch
-        T e1 = T(0), e2 = T(0);
-        if (lane < nb) {
-          if (FWD) {
-            e1 = S.p[b0 + lane];
-            e2 = S.rinv[b0 + lane];
-          } else {
-            e1 = k.bp_out ? T(0) : S.x[b0 + lane];
-            e2 = S.cinv[b0 + lane];
-          }
-        }
-        for (int t = 0; t < nb; ++t) {
-          const int k0 = __shfl_sync(0xffffffffu, pv, t);
-          const int k1 = __shfl_sync(0xffffffffu, pv, t + 1);
-          T acc = T(0);
-          for (int s0 = k0; s0 < k1; s0 += 32 * U) {
-            const int nxt = min(s0 + 32 * U, k1);
-            const int chi = (nxt - 1 - kb) / kChunk;
-            while (ready <= chi) {
-              mbar_wait(&bars[ready % kChunks], (ready / kChunks) & 1);
-              ++ready;
-            }
-            int ci[U];
-            T cv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int e = s0 + u * 32 + lane;
-              const int o = e - kb;
-              const int pos = ((o / kChunk) % kChunks) * kChunk + (o & (kChunk - 1));
-              const bool in = e < k1;
-              ci[u] = in ? ring_i[pos] : 0;
-              cv[u] = in ? ring_v[pos] : T(0);
-            }
-            T g[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) g[u] = __ldg(vec + ci[u]);
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc += cv[u] * g[u];
-            const int clo = (nxt - kb) / kChunk;  // chunks below are fully consumed
-            if (clo > freed) {
-              __syncwarp();
-              if (lane == 0) {
-                for (int f = freed; f < clo; ++f) {
-                  if (f + kChunks < nch) issue(f + kChunks);
-                }
-              }
-              freed = clo;
-            }
-          }
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-          if (lane == t) {
-            const int i = b0 + t;
-            if (FWD) {
-              const T r = e1 - acc;
-              S.w[i] = e2 * r;
-              r2 += static_cast<double>(r) * static_cast<double>(r);
-            } else if (k.bp_out) {
-              k.bp_out[i] = acc;
-            } else {
-              const T xn = upd(e1, k.relax, acc, e2);
-              S.x[i] = xn;
-              if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * sys + 2], 0, it + 1);
-            }
-          }
-        }
-      }
-    }
-  }
-  if (!FWD) return;
-  // per-system ||r||^2: warp -> block partial -> last block (fixed order)
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, off);
-  if (lane == 0) {
-    red[0][warp] = sys == 0 ? r2 : 0.0;
-    red[1][warp] = sys == 1 ? r2 : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < k.nsys) {
-    double t = 0.0;
-    for (int q = 0; q < kStreamWarps; ++q) t += red[threadIdx.x][q];
-    k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
-  }
-  if (k.bp_out) return;
-  if (last_block(k.ticket)) {
-    finish_norms(k.partial, gridDim.x, k.nsys, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
-    if (threadIdx.x == 0) *k.ticket = 0;
-  }
-}
-
-// ------------------------------------------------------------ flat-stream kernels
-// Each warp owns a contiguous, nnz-balanced range of compressed vectors
-// [v0, v1) (rows for K1, columns for K2) and walks its byte range of the
-// index/value arrays as a flat sequence of 128-entry batches: lane l loads
-// entries [B+4l, B+4l+4) with one int4 + one 4-value load. Batch t+1 is
-// loaded before batch t's gathers are consumed (software pipeline), so the
-// matrix stream keeps flowing while gathers wait on L2. Vector boundaries
-// are applied with per-lane masks; a vector's lane partials are combined by
-// a fixed-order butterfly when it completes, and its epilogue runs on the
-// lane that prefetched its operands (windows of 32 vectors). Summation
-// order depends only on the static partition, so results are reproducible.
-constexpr int kFlatThreads = 256;
-constexpr int kFlatWarps = kFlatThreads / 32;
-
-// Lane-strided batches of 32*Q entries: lane l holds entries B + l + 32q,
-// so each warp-wide load reads 32 consecutive entries and each warp-wide
-// gather touches the dense-vector lines of 32 consecutive entries of a
-// vector (a few short snake-order runs: few L1 wavefronts).
-// One warp's share: vectors [v0, v1) of system SYS. Everything that can be
-// re-read from the kernel-parameter bank is, so the loop fits 32 registers
-// (8 CTAs x 256 threads per SM: the occupancy the streaming probe needs to
-// reach the copy roofline, tools/stream_probe.cu).
-template <class T, bool FWD, int Q, int SYS>
-__device__ __forceinline__ double flat_warp(const SartK<T>& k, int v0, int v1, int lane, int it) {
-  const SysK<T>& S = k.s[SYS];
-  const int* __restrict__ ptr = FWD ? S.rp : S.cp;
-  const bool bp = !FWD && k.bp_out != nullptr;
-  const int hi = __ldg(ptr + v1);
-  double r2 = 0.0;
-  int wbase = v0;
-  int wend = (wbase + lane < v1) ? __ldg(ptr + wbase + lane + 1) : hi;
-  T w1 = T(0), w2 = T(0);
-  if (wbase + lane < v1) {
-    w1 = FWD ? S.p[wbase + lane] : (bp ? T(0) : S.x[wbase + lane]);
-    w2 = FWD ? S.rinv[wbase + lane] : S.cinv[wbase + lane];
-  }
-  int r = v0;
-  int er = __shfl_sync(0xffffffffu, wend, 0);
-  T acc = T(0);
-  for (int B = __ldg(ptr + v0); r < v1; B += 32 * Q) {
-    const int bend = B + 32 * Q;
-    T pr[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int e = B + lane + 32 * q;
-      const bool in = e < hi;
-      const int c = in ? __ldg((FWD ? S.ci : S.ri) + e) : 0;
-      const T v = in ? __ldg((FWD ? S.rv : S.cv) + e) : T(0);
-      pr[q] = v * __ldg((FWD ? S.x : S.w) + c);
-    }
-    int seg_lo = B;
-    for (;;) {
-      const int seg_hi = min(er, bend);
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int e = B + lane + 32 * q;
-        if (e >= seg_lo && e < seg_hi) acc += pr[q];
-      }
-      if (er > bend) break;  // vector continues in the next batch
-      T tot = acc;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-      acc = T(0);
-      if (lane == r - wbase) {
-        if (FWD) {
-          const T res = w1 - tot;
-          S.w[r] = w2 * res;
-          r2 += static_cast<double>(res) * static_cast<double>(res);
-        } else if (bp) {
-          k.bp_out[r] = tot;
-        } else {
-          const T xn = upd(w1, k.relax, tot, w2);
-          S.x[r] = xn;
-          if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * SYS + 2], 0, it + 1);
-        }
-      }
-      seg_lo = er;
-      ++r;
-      if (r >= v1) break;
-      if (r - wbase == 32) {  // slide the windows
-        wbase = r;
-        wend = (wbase + lane < v1) ? __ldg(ptr + wbase + lane + 1) : hi;
-        if (wbase + lane < v1) {
-          w1 = FWD ? S.p[wbase + lane] : (bp ? T(0) : S.x[wbase + lane]);
-          w2 = FWD ? S.rinv[wbase + lane] : S.cinv[wbase + lane];
-        }
-      }
-      er = __shfl_sync(0xffffffffu, wend, r - wbase);
-      if (seg_lo >= bend) break;
-    }
-  }
-  return r2;
-}
-
-// Contiguous variant: lane l holds the aligned quad [B+4l, B+4l+4) of each
-// of the Q 128-entry sub-batches; its four gathers usually fall in one
-// snake-order run (one sector), so L1 absorbs three of them.
-template <class T, bool FWD, int Q, int SYS>
-__device__ __forceinline__ double flat_warp_v4(const SartK<T>& k, int v0, int v1, int lane,
-                                               int it) {
-  const SysK<T>& S = k.s[SYS];
-  const int* __restrict__ ptr = FWD ? S.rp : S.cp;
-  const bool bp = !FWD && k.bp_out != nullptr;
-  const int lo = __ldg(ptr + v0), hi = __ldg(ptr + v1);
-  double r2 = 0.0;
-  int wbase = v0;
-  int wend = (wbase + lane < v1) ? __ldg(ptr + wbase + lane + 1) : hi;
-  T w1 = T(0), w2 = T(0);
-  if (wbase + lane < v1) {
-    w1 = FWD ? S.p[wbase + lane] : (bp ? T(0) : S.x[wbase + lane]);
-    w2 = FWD ? S.rinv[wbase + lane] : S.cinv[wbase + lane];
-  }
-  int r = v0;
-  int er = __shfl_sync(0xffffffffu, wend, 0);
-  T acc = T(0);
-  for (int B = lo & ~3; r < v1; B += 128 * Q) {
-    const int bend = B + 128 * Q;
-    T pr[Q][4];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int e = B + 128 * q + 4 * lane;
-      if (e < hi) {  // quads are aligned; entries past hi are masked below
-        const int4 c = ld_stream(reinterpret_cast<const int4*>((FWD ? S.ci : S.ri) + e));
-        T v[4];
-        ld_stream4((FWD ? S.rv : S.cv) + e, v);
-        const T* __restrict__ vec = FWD ? S.x : S.w;
-        pr[q][0] = (e >= lo) ? v[0] * __ldg(vec + c.x) : T(0);
-        pr[q][1] = (e + 1 >= lo && e + 1 < hi) ? v[1] * __ldg(vec + c.y) : T(0);
-        pr[q][2] = (e + 2 >= lo && e + 2 < hi) ? v[2] * __ldg(vec + c.z) : T(0);
-        pr[q][3] = (e + 3 < hi) ? v[3] * __ldg(vec + c.w) : T(0);
-      } else {
-        pr[q][0] = pr[q][1] = pr[q][2] = pr[q][3] = T(0);
-      }
-    }
-    int seg_lo = B;
-    for (;;) {
-      const int seg_hi = min(er, bend);
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int e = B + 128 * q + 4 * lane + t;
-          if (e >= seg_lo && e < seg_hi) acc += pr[q][t];
-        }
-      }
-      if (er > bend) break;
-      T tot = acc;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-      acc = T(0);
-      if (lane == r - wbase) {
-        if (FWD) {
-          const T res = w1 - tot;
-          S.w[r] = w2 * res;
-          r2 += static_cast<double>(res) * static_cast<double>(res);
-        } else if (bp) {
-          k.bp_out[r] = tot;
-        } else {
-          const T xn = upd(w1, k.relax, tot, w2);
-          S.x[r] = xn;
-          if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * SYS + 2], 0, it + 1);
-        }
-      }
-      seg_lo = er;
-      ++r;
-      if (r >= v1) break;
-      if (r - wbase == 32) {
-        wbase = r;
-        wend = (wbase + lane < v1) ? __ldg(ptr + wbase + lane + 1) : hi;
-        if (wbase + lane < v1) {
-          w1 = FWD ? S.p[wbase + lane] : (bp ? T(0) : S.x[wbase + lane]);
-          w2 = FWD ? S.rinv[wbase + lane] : S.cinv[wbase + lane];
-        }
-      }
-      er = __shfl_sync(0xffffffffu, wend, r - wbase);
-      if (seg_lo >= bend) break;
-    }
-  }
-  return r2;
-}
-
-// CTAs [0, sys_blocks) serve system 0, the rest system 1 (work table built
-// with CTA-aligned system boundaries). Q > 0: lane-strided batches of 32*Q;
-// Q < 0: contiguous quads, 128*|Q| entries per batch.
-template <class T, bool FWD, int Q>
-__global__ void __launch_bounds__(kFlatThreads, 8)
-    sart_flat_kernel(SartK<T> k, const int2* __restrict__ work, int nwork, int it) {
-  __shared__ double red[2][kFlatWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kFlatWarps + warp;
-  const int sys = blockIdx.x >= k.sys_blocks[FWD ? 0 : 1] ? 1 : 0;
-  double r2 = 0.0;
-  if (gw < nwork && sys_on(k.state, sys)) {
-    const int2 wk = work[gw];
-    if (wk.y > wk.x) {
-      const int off = sys ? static_cast<int>(FWD ? k.rows0 : k.cols0) : 0;
-      if constexpr (Q > 0) {
-        r2 = sys == 0 ? flat_warp<T, FWD, Q, 0>(k, wk.x, wk.y, lane, it)
-                      : flat_warp<T, FWD, Q, 1>(k, wk.x - off, wk.y - off, lane, it);
-      } else {
-        r2 = sys == 0 ? flat_warp_v4<T, FWD, -Q, 0>(k, wk.x, wk.y, lane, it)
-                      : flat_warp_v4<T, FWD, -Q, 1>(k, wk.x - off, wk.y - off, lane, it);
-      }
-    }
-  }
-  if (!FWD) return;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, off);
-  if (lane == 0) {
-    red[0][warp] = sys == 0 ? r2 : 0.0;
-    red[1][warp] = sys == 1 ? r2 : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < k.nsys) {
-    double t = 0.0;
-    for (int q = 0; q < kFlatWarps; ++q) t += red[threadIdx.x][q];
-    k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
-  }
-  if (k.bp_out) return;
-  if (last_block(k.ticket)) {
-    finish_norms(k.partial, gridDim.x, k.nsys, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
-    if (threadIdx.x == 0) *k.ticket = 0;
-  }
-}
-
 // ------------------------------------------------------------ multi-RHS kernels
 // Slices share A; X/W/P are [n][S] so one warp's 32 lanes read 32 consecutive
 // slices of a gathered row (coalesced 128 B for fp32) while the matrix entry
@@ -1505,14 +1075,6 @@ __global__ void sqrt_kernel(double* v, int n) {
   if (threadIdx.x < n) v[threadIdx.x] = sqrt(v[threadIdx.x]);
 }
 
-// Kernel family for single-RHS plans: 0 = vector-per-group direct loads
-// (default, fastest measured), 1 = TMA ring, 2 = flat warp stream
-// (SSB_KERNEL_MODE overrides; A/B experiments, profiles/r01_notes.md).
-int kernel_mode() {
-  const char* v = std::getenv("SSB_KERNEL_MODE");
-  return v && *v ? std::atoi(v) : 0;
-}
-
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
@@ -1601,49 +1163,6 @@ void launch_back1(Plan& P, const SartK<T>& k, int it) {
   fn<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
 }
 
-template <class T, bool FWD>
-void launch_stream(Plan& P, const SartK<T>& k, int it) {
-  const std::size_t sh = StreamSmem<T>::kBytes;
-  const int2* wk = FWD ? P.work_f.get() : P.work_b.get();
-  const int nw = FWD ? P.nwork_f : P.nwork_b;
-  const int blocks = FWD ? P.fwd_blocks : P.back_blocks;
-  if (P.mode == 2) {
-    const int q = FWD ? P.q_fwd : P.q_back;
-    auto* fn = q >= 8 ? sart_flat_kernel<T, FWD, 8>
-             : q >= 4 ? sart_flat_kernel<T, FWD, 4>
-             : q >= 2 ? sart_flat_kernel<T, FWD, 2>
-             : q == -2 ? sart_flat_kernel<T, FWD, -2>
-                       : sart_flat_kernel<T, FWD, -1>;
-    fn<<<blocks, kFlatThreads, 0, P.ctx->stream>>>(k, wk, nw, it);
-    return;
-  }
-  switch (FWD ? P.u_fwd : P.u_back) {
-    case 8:
-      sart_stream_kernel<T, FWD, 8><<<blocks, kStreamWarps * 32, sh, P.ctx->stream>>>(k, wk, nw, it);
-      break;
-    case 2:
-      sart_stream_kernel<T, FWD, 2><<<blocks, kStreamWarps * 32, sh, P.ctx->stream>>>(k, wk, nw, it);
-      break;
-    default:
-      sart_stream_kernel<T, FWD, 4><<<blocks, kStreamWarps * 32, sh, P.ctx->stream>>>(k, wk, nw, it);
-      break;
-  }
-}
-
-template <class T>
-void stream_attributes() {
-  static bool done = false;
-  if (done) return;
-  const int sh = StreamSmem<T>::kBytes;
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  SSB_CUDA(cudaFuncSetAttribute(sart_stream_kernel<T, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh));
-  done = true;
-}
-
 template <class T>
 using PairFn = void (*)(SartK<T>, int);
 
@@ -1682,10 +1201,6 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
     launch_pair<T>(P, k, it, true);
     return;
   }
-  if (P.stream) {
-    launch_stream<T, true>(P, k, it);
-    return;
-  }
   if (P.nrhs > 1) {
     const int spl = (P.nrhs + 31) / 32;
     const std::size_t sh = sizeof(double) * kWarps * P.nsys * P.nrhs;
@@ -1710,10 +1225,6 @@ template <class T>
 void launch_back(Plan& P, const SartK<T>& k, int it) {
   if (P.paired) {
     launch_pair<T>(P, k, it, false);
-    return;
-  }
-  if (P.stream) {
-    launch_stream<T, false>(P, k, it);
     return;
   }
   if (P.nrhs > 1) {
@@ -2120,8 +1631,8 @@ std::string Plan::describe() const {
   const char* t = dtype == SS_F32 ? "float" : "double";
   std::string fk, bk;
   if (sharded || nrhs > 1 || !paired) {
-    fk = nrhs > 1 ? "sart_fwd_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_fwd_kernel");
-    bk = nrhs > 1 ? "sart_back_multi_kernel" : (stream ? "sart_stream_kernel" : "sart_back_kernel");
+    fk = nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel";
+    bk = nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel";
   } else {
     fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
          std::to_string(uf_fwd) + ", " + std::to_string(layout_mode(true)) + ">";
@@ -2216,105 +1727,6 @@ void normalisers(Plan& P, int s, double* max_row_sum) {
 }
 }  // namespace
 
-namespace {
-int pick_unroll(double avg) {
-  if (avg >= 192) return 8;
-  if (avg >= 48) return 4;
-  return 2;
-}
-
-// Static nnz-balanced warp ranges over the compressed vectors (rows when
-// fwd, columns otherwise) of every system; each vector costs len + 16
-// entry-equivalents (per-vector epilogue). Ranges never straddle systems.
-void build_work(Plan& P, bool fwd, int warps_per_block, long long max_warps, DBuf<int2>& out,
-                int& nwork, int& blocks, int& unroll, int* sys_blocks = nullptr) {
-  std::vector<std::vector<int>> ptr(P.nsys);
-  double wsum[2] = {0, 0};
-  long long nvec_total = 0, nnz_total = 0;
-  for (int s = 0; s < P.nsys; ++s) {
-    Matrix* a = P.a[s];
-    const long long n = fwd ? P.rows[s] : P.cols[s];
-    ptr[s].resize(n + 1);
-    P.ctx->copy(ptr[s].data(), fwd ? a->rowptr.get() : a->colptr.get(),
-                        (n + 1) * sizeof(int));
-    wsum[s] = static_cast<double>(ptr[s][n]) + 16.0 * n;
-    nvec_total += n;
-    nnz_total += ptr[s][n];
-  }
-  long long W = std::min<long long>(max_warps, std::max<long long>(warps_per_block, nvec_total / 2));
-  W = (W + warps_per_block - 1) / warps_per_block * warps_per_block;
-  W = std::max<long long>(W, static_cast<long long>(P.nsys) * warps_per_block);
-  long long Ws[2] = {W, 0};
-  if (P.nsys == 2) {
-    const double tot = wsum[0] + wsum[1];
-    Ws[0] = tot > 0 ? std::llround(W * wsum[0] / tot) : W / 2;
-    // system 0 ends on a CTA boundary (kernels pick the system per CTA)
-    Ws[0] = (Ws[0] + warps_per_block / 2) / warps_per_block * warps_per_block;
-    Ws[0] = std::max<long long>(warps_per_block, std::min<long long>(W - warps_per_block, Ws[0]));
-    Ws[1] = W - Ws[0];
-  }
-  if (sys_blocks) {
-    *sys_blocks = P.nsys == 2 ? static_cast<int>(Ws[0] / warps_per_block) : 0x7fffffff;
-  }
-  std::vector<int2> wk;
-  wk.reserve(W);
-  long long off = 0;
-  for (int s = 0; s < P.nsys; ++s) {
-    const auto& pp = ptr[s];
-    const long long n = static_cast<long long>(pp.size()) - 1;
-    long long r = 0;
-    for (long long j = 0; j < Ws[s]; ++j) {
-      const double target = wsum[s] * static_cast<double>(j + 1) / static_cast<double>(Ws[s]);
-      long long e = r;
-      if (j + 1 == Ws[s]) {
-        e = n;
-      } else {
-        while (e < n && static_cast<double>(pp[e + 1]) + 16.0 * (e + 1) <= target) ++e;
-      }
-      wk.push_back(make_int2(static_cast<int>(off + r), static_cast<int>(off + e)));
-      r = e;
-    }
-    off += n;
-  }
-  out.alloc(wk.size());
-  P.ctx->copy(out.get(), wk.data(), wk.size() * sizeof(int2));
-  nwork = static_cast<int>(wk.size());
-  blocks = static_cast<int>((wk.size() + warps_per_block - 1) / warps_per_block);
-  unroll = pick_unroll(nvec_total > 0 ? static_cast<double>(nnz_total) / nvec_total : 0.0);
-}
-
-template <class T>
-int flat_blocks_per_sm() {
-  int a = 0, b = 0;
-  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, sart_flat_kernel<T, true, 8>,
-                                                         kFlatThreads, 0));
-  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sart_flat_kernel<T, false, 8>,
-                                                         kFlatThreads, 0));
-  return std::max(1, std::min(a, b));
-}
-
-// mode 1: TMA-ring kernels; mode 2: flat-stream kernels
-void setup_stream(Plan& P, int mode) {
-  P.mode = mode;
-  if (mode == 1) {
-    if (P.dtype == SS_F32) stream_attributes<float>();
-    else stream_attributes<double>();
-    const long long mw = static_cast<long long>(P.ctx->sm_count) * kStreamWarps;
-    build_work(P, true, kStreamWarps, mw, P.work_f, P.nwork_f, P.fwd_blocks, P.u_fwd);
-    build_work(P, false, kStreamWarps, mw, P.work_b, P.nwork_b, P.back_blocks, P.u_back);
-  } else {
-    const int per_sm = P.dtype == SS_F32 ? flat_blocks_per_sm<float>() : flat_blocks_per_sm<double>();
-    const long long mw = static_cast<long long>(P.ctx->sm_count) * per_sm * kFlatWarps;
-    build_work(P, true, kFlatWarps, mw, P.work_f, P.nwork_f, P.fwd_blocks, P.u_fwd,
-               &P.sys_blocks_f);
-    build_work(P, false, kFlatWarps, mw, P.work_b, P.nwork_b, P.back_blocks, P.u_back,
-               &P.sys_blocks_b);
-    P.q_fwd = env_int("SSB_Q_FWD", -1);
-    P.q_back = env_int("SSB_Q_BACK", -1);
-  }
-  P.stream = true;
-}
-}  // namespace
 
 namespace {
 // padded pointer of one compressed direction; returns the padded entry count
@@ -2531,7 +1943,6 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->sys_blocks_f = split(P->fwd_blocks, n0 + 16.0 * a1->rows, n1 + 16.0 * a2->rows);
     P->sys_blocks_b = split(P->back_blocks, n0 + 16.0 * a1->cols, n1 + 16.0 * a2->cols);
   }
-  if (nrhs == 1 && kernel_mode() != 0) setup_stream(*P, kernel_mode());
   alloc_common(*P);
   tr.mark("occupancy + alloc");
   for (int s = 0; s < P->nsys; ++s) {
@@ -2614,7 +2025,6 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
     P->fwd_blocks = occupancy_blocks<double>(*P, true);
     P->back_blocks = occupancy_blocks<double>(*P, false);
   }
-  if (kernel_mode() != 0) setup_stream(*P, kernel_mode());
   alloc_common(*P);
   P->bp.alloc((a->cols + 1) * P->tsize());
   // normalisers: rows from the local block, columns from the full matrix
