@@ -102,7 +102,9 @@ struct Context {
   // NCCL (row-sharded plans); opaque to avoid the header here
   void* comm = nullptr;
   int nranks = 1, rank = 0;
-  void* solver = nullptr;  // cuSOLVER handle (dense min-norm path), created on first use
+  void* solver = nullptr;   // cuSOLVER handle (dense min-norm path), created on first use
+  void* solver2 = nullptr;  // second handle + stream: the concurrent folded branch
+  cudaStream_t side = nullptr;
 
   void* temp(std::size_t bytes) {
     if (scratch.size() < bytes) scratch.alloc(bytes + bytes / 4);
@@ -121,6 +123,13 @@ struct Context {
     ++launches;
   }
 };
+
+// Second stream of a context: the concurrent folded branch of solve_split
+// (dense and CGLS methods), created on first use and destroyed with the context.
+inline cudaStream_t side_stream(Context* ctx) {
+  if (!ctx->side) SSB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  return ctx->side;
+}
 
 // Phase timing for diagnostics (SSB_TRACE=1 prints to stderr).
 struct PhaseTrace {
@@ -216,6 +225,11 @@ bool same_pattern(Matrix& a, Matrix& b);
 void scan_counts(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n);
 // dense minimum-norm solve of a (reference pseudo_solve_dense), p and f on the device
 void pseudo_solve_dense_dev(Matrix& a, const double* p, double* f, std::int64_t dense_cap);
+// both folded branches concurrently (main + side stream, two host threads);
+// per-branch wall seconds; a failing branch leaves its message and code
+void pseudo_solve_dense_pair(Matrix* a[2], const double* p[2], double* f[2],
+                             std::int64_t dense_cap, double seconds[2], std::string errs[2],
+                             int codes[2]);
 void release_solver(Context* ctx);
 void union_pattern(Matrix& a, Matrix& b, Matrix*& ua, Matrix*& ub);
 void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh);
@@ -232,6 +246,8 @@ bool all_finite_dev(Context* ctx, const double* v, std::int64_t n);
 void rasterize_dev(Context* ctx, const double* ell6, int count, const Grid& g, double* out);
 void forward_project_dev(Matrix& a, const double* f, double* p);
 // CGLS (cgls.cu): f_dev receives x in fp64; report gets iterations/history/time
+void cgls_device_pair(Matrix* a[2], const double* p[2], const ss_solve_options& o, double* f[2],
+                      ss_solve_report rep[2], std::string errs[2], int codes[2]);
 void cgls_device(Matrix& a, const double* p_dev, const ss_solve_options& o, double* f_dev,
                  ss_solve_report* rep, double* hist_host);
 

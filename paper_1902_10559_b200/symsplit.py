@@ -559,6 +559,17 @@ def write_vector_csv(v, path: str) -> None:
 
 
 # ----------------------------------------------------------------- phantom
+def shepp_logan_ellipses():
+    """phantom.cpp:18-32: the 10-ellipse Shepp-Logan table, rows
+    (x0, y0, a, b, angle [rad], density)."""
+    t = [(0.0, 0.0, 0.69, 0.92, 0.0, 2.0), (0.0, -0.0184, 0.6624, 0.874, 0.0, -0.98),
+         (0.22, 0.0, 0.11, 0.31, -18.0, -0.02), (-0.22, 0.0, 0.16, 0.41, 18.0, -0.02),
+         (0.0, 0.35, 0.21, 0.25, 0.0, 0.01), (0.0, 0.1, 0.046, 0.046, 0.0, 0.01),
+         (0.0, -0.1, 0.046, 0.046, 0.0, 0.01), (-0.08, -0.605, 0.046, 0.023, 0.0, 0.01),
+         (0.0, -0.606, 0.023, 0.023, 0.0, 0.01), (0.06, -0.605, 0.023, 0.046, 0.0, 0.01)]
+    return np.array([(x, y, a, b, degrees_to_radians(d), rho) for x, y, a, b, d, rho in t])
+
+
 def random_ellipses(seed: int, count: int = 8):
     out = np.empty((count, 6))
     _check(_lib().ss_random_ellipses(seed, count, _dp(out)))
