@@ -714,6 +714,157 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   }
 }
 
+// ------------------------------------------------------------ single-system tiled kernels
+// One system (sart_solve, the per-rank system of a 2-GPU run, a row shard) on
+// the same tiled stream layout as the folded pair: quads padded, entries
+// permuted within 4*VS-entry tiles, 16-bit offsets + tile bases when they fit.
+template <class T, int VS, int UF, bool U16>
+__device__ __forceinline__ T seg_dot1(const int* __restrict__ idx,
+                                      const unsigned short* __restrict__ off,
+                                      const int* __restrict__ tbase, int tf,
+                                      const T* __restrict__ val, const T* __restrict__ vec, int beg,
+                                      int end, int lane, unsigned mask) {
+  T acc = T(0);
+  const int nvec = (end - beg) >> 2;
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    int4 c[UF];
+    T v[UF][4];
+    const int t0 = tf + (q - lane) / VS;
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = beg + ((q + u * VS) << 2);
+      if (U16) {
+        c[u] = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)), __ldg(tbase + t0 + u));
+      } else {
+        c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
+      }
+      load4(val + k0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      acc += v[u][0] * __ldg(vec + c[u].x) + v[u][1] * __ldg(vec + c[u].y) +
+             v[u][2] * __ldg(vec + c[u].z) + v[u][3] * __ldg(vec + c[u].w);
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = beg + (q << 2);
+    const int4 c = U16 ? decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)),
+                                  __ldg(tbase + tf + (q - lane) / VS))
+                       : __ldg(reinterpret_cast<const int4*>(idx + k0));
+    T v[4];
+    load4(val + k0, v);
+    acc += v[0] * __ldg(vec + c.x) + v[1] * __ldg(vec + c.y) + v[2] * __ldg(vec + c.z) +
+           v[3] * __ldg(vec + c.w);
+  }
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, VS);
+  return acc;
+}
+
+template <class T, int VS, int UF, bool U16>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_kernel(SartK<T> k, int it) {
+  __shared__ double red[kWarps];
+  const SysK<T>& S = k.s[0];
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.rows0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
+  double r2 = 0.0;
+  if (sys_on(k.state, 0)) {
+    int beg = 0, end = 0, tf = 0;
+    if (g < n) {
+      beg = __ldg(k.tpf + g);
+      end = __ldg(k.tpf + g + 1);
+      if (U16) tf = __ldg(k.tff + g);
+    }
+    for (; g < n; g += gstep) {
+      const int gn = g + gstep;
+      int nbeg = 0, nend = 0, ntf = 0;
+      if (gn < n) {
+        nbeg = __ldg(k.tpf + gn);
+        nend = __ldg(k.tpf + gn + 1);
+        if (U16) ntf = __ldg(k.tff + gn);
+      }
+      T pv = T(0), ri = T(0);
+      if (lane == 0) {
+        pv = S.p[g];
+        ri = S.rinv[g];
+      }
+      const T dot = seg_dot1<T, VS, UF, U16>(k.tif, k.tof, k.tbf, tf, k.rv2, S.x, beg, end,
+                                             lane, mask);
+      if (lane == 0) {
+        const T r = pv - dot;
+        S.w[g] = ri * r;
+        r2 += static_cast<double>(r) * static_cast<double>(r);
+      }
+      beg = nbeg;
+      end = nend;
+      tf = ntf;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kWarps; ++q) t += red[q];
+    k.partial[blockIdx.x] = t;
+  }
+  if (k.bp_out) return;  // sharded plans reduce ||r||^2 across ranks instead
+  if (last_block(k.ticket)) {
+    finish_norms(k.partial, gridDim.x, 1, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
+template <class T, int VS, int UF, bool U16>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_tiled_kernel(SartK<T> k, int it) {
+  const SysK<T>& S = k.s[0];
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.cols0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
+  if (!sys_on(k.state, 0)) return;
+  int beg = 0, end = 0, tf = 0;
+  if (g < n) {
+    beg = __ldg(k.tpb + g);
+    end = __ldg(k.tpb + g + 1);
+    if (U16) tf = __ldg(k.tfb + g);
+  }
+  for (; g < n; g += gstep) {
+    const int gn = g + gstep;
+    int nbeg = 0, nend = 0, ntf = 0;
+    if (gn < n) {
+      nbeg = __ldg(k.tpb + gn);
+      nend = __ldg(k.tpb + gn + 1);
+      if (U16) ntf = __ldg(k.tfb + gn);
+    }
+    T xo = T(0), ci = T(0);
+    if (lane == 0 && !k.bp_out) {
+      xo = S.x[g];
+      ci = S.cinv[g];
+    }
+    const T u = seg_dot1<T, VS, UF, U16>(k.tib, k.tob, k.tbb, tf, k.cv2, S.w, beg, end, lane,
+                                         mask);
+    if (lane == 0) {
+      if (k.bp_out) {
+        k.bp_out[g] = u;
+      } else {
+        const T xn = upd(xo, k.relax, u, ci);
+        S.x[g] = xn;
+        if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[2], 0, it + 1);
+      }
+    }
+    beg = nbeg;
+    end = nend;
+    tf = ntf;
+  }
+}
+
 // dst[stride*i + slot] = src[i] (building interleaved paired streams)
 template <class T, class S>
 __global__ void interleave_kernel(const S* src, T* dst, long long n, int stride, int slot) {
@@ -758,11 +909,15 @@ __global__ void tile_stream_kernel(const int* __restrict__ ptr, const int* __res
       if (o < len) {
         c = idx[beg + o];
         a = static_cast<T>(v0[beg + o]);  // fp64 master values rounded once to the plan type
-        b = static_cast<T>(v1[beg + o]);
+        if (v1) b = static_cast<T>(v1[beg + o]);
       }
       tidx[ob + p] = c;
-      tv2[2 * static_cast<long long>(ob + p)] = a;
-      tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+      if (v1) {  // folded pair: {a1, a2} interleaved
+        tv2[2 * static_cast<long long>(ob + p)] = a;
+        tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+      } else {   // one system
+        tv2[ob + p] = a;
+      }
     }
   }
 }
@@ -807,13 +962,17 @@ __global__ void tile_stream16_kernel(const int* __restrict__ ptr, const int* __r
       if (o < len) {
         c = idx[beg + o];
         a = static_cast<T>(v0[beg + o]);
-        b = static_cast<T>(v1[beg + o]);
+        if (v1) b = static_cast<T>(v1[beg + o]);
       }
       const unsigned d = static_cast<unsigned>(c - base);
       bad |= d > 0xffffu;
       tofs[ob + p] = static_cast<unsigned short>(d);
-      tv2[2 * static_cast<long long>(ob + p)] = a;
-      tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+      if (v1) {
+        tv2[2 * static_cast<long long>(ob + p)] = a;
+        tv2[2 * static_cast<long long>(ob + p) + 1] = b;
+      } else {
+        tv2[ob + p] = a;
+      }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(overflow, 1);
   }
@@ -1188,6 +1347,26 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
   return nullptr;
 }
 
+// single-system tiled kernel of a plan
+template <class T>
+PairFn<T> single_kernel(const Plan& P, bool fwd) {
+  const int vs = fwd ? P.vs_fwd : P.vs_back;
+  const int uf = fwd ? P.uf_fwd : P.uf_back;
+  const bool u16 = fwd ? P.c16f : P.c16b;
+#define SSB_ONE(V, U)                                                                          \
+  if (vs == V && uf == U) {                                                                    \
+    if (u16) return fwd ? sart_fwd_tiled_kernel<T, V, U, true> : sart_back_tiled_kernel<T, V, U, true>; \
+    return fwd ? sart_fwd_tiled_kernel<T, V, U, false> : sart_back_tiled_kernel<T, V, U, false>; \
+  }
+  SSB_ONE(4, 2) SSB_ONE(8, 2) SSB_ONE(16, 2) SSB_ONE(32, 2)
+  SSB_ONE(4, 4) SSB_ONE(8, 4) SSB_ONE(16, 4) SSB_ONE(32, 4)
+#undef SSB_ONE
+  fail("plan: unsupported single-system kernel shape");
+  return nullptr;
+}
+
+bool single_tiled(const Plan& P) { return !P.paired && P.tiled && P.nrhs == 1 && P.nsys == 1; }
+
 template <class T>
 void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
   int smem = 0;
@@ -1199,6 +1378,10 @@ template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
   if (P.paired) {
     launch_pair<T>(P, k, it, true);
+    return;
+  }
+  if (single_tiled(P)) {
+    single_kernel<T>(P, true)<<<P.fwd_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
     return;
   }
   if (P.nrhs > 1) {
@@ -1225,6 +1408,10 @@ template <class T>
 void launch_back(Plan& P, const SartK<T>& k, int it) {
   if (P.paired) {
     launch_pair<T>(P, k, it, false);
+    return;
+  }
+  if (single_tiled(P)) {
+    single_kernel<T>(P, false)<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
     return;
   }
   if (P.nrhs > 1) {
@@ -1275,6 +1462,31 @@ int occupancy_pair_t(Plan& P, bool fwd) {
   }
   SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
   return std::max(1, per_sm) * P.ctx->sm_count;
+}
+
+// resident-CTA grids of a single-system tiled plan (never more blocks than groups)
+template <class T>
+void size_single_grid_t(Plan& P) {
+  for (int f = 0; f < 2; ++f) {
+    const bool fwd = f == 0;
+    int per_sm = 0;
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, single_kernel<T>(P, fwd),
+                                                           kThreads, 0));
+    const long long groups = static_cast<long long>(fwd ? P.rows[0] : P.cols[0]) *
+                             (fwd ? P.vs_fwd : P.vs_back);
+    const int b = static_cast<int>(std::max<long long>(1, std::min<long long>(
+        std::max(1, per_sm) * static_cast<long long>(P.ctx->sm_count),
+        (groups + kThreads - 1) / kThreads)));
+    (fwd ? P.fwd_blocks : P.back_blocks) = b;
+  }
+}
+
+void size_single_grid(Plan& P) {
+  if (P.dtype == SS_F32) size_single_grid_t<float>(P);
+  else size_single_grid_t<double>(P);
+  if (static_cast<std::size_t>(P.fwd_blocks) * P.nsys * P.nrhs > P.partial.size()) {
+    P.partial.alloc(static_cast<std::size_t>(P.fwd_blocks) * P.nsys * P.nrhs);
+  }
 }
 
 int occupancy_pair_blocks(Plan& P, bool fwd) {
@@ -1617,6 +1829,11 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
              : nf * (4 + 2 * b) + 4 * (rows[0] + 1);
     k = c16b ? nb * (2 + 2 * b) + 4 * ntile_b + 8 * (cols[0] + 1)
              : nb * (4 + 2 * b) + 4 * (cols[0] + 1);
+  } else if (tiled && nsys == 1 && nrhs == 1) {
+    f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
+             : tnnz_f * (4 + b) + 4 * (rows[0] + 1);
+    k = c16b ? tnnz_b * (2 + b) + 4 * ntile_b + 8 * (cols[0] + 1)
+             : tnnz_b * (4 + b) + 4 * (cols[0] + 1);
   } else {
     for (int s = 0; s < nsys; ++s) {
       f += a[s]->nnz * (4 + b) + 4 * (rows[s] + 1);
@@ -1630,7 +1847,12 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
 std::string Plan::describe() const {
   const char* t = dtype == SS_F32 ? "float" : "double";
   std::string fk, bk;
-  if (sharded || nrhs > 1 || !paired) {
+  if (!paired && tiled && nrhs == 1 && nsys == 1) {
+    fk = "sart_fwd_tiled_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
+         std::to_string(uf_fwd) + ", " + (c16f ? "true" : "false") + ">";
+    bk = "sart_back_tiled_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
+         std::to_string(uf_back) + ", " + (c16b ? "true" : "false") + ">";
+  } else if (sharded || nrhs > 1 || !paired) {
     fk = nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel";
     bk = nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel";
   } else {
@@ -1648,9 +1870,9 @@ std::string Plan::describe() const {
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
                 "\"back_bytes\": %lld, \"graph\": %s}",
-                sharded ? "row-sharded"
+                sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
                         : (paired ? (tiled ? (c16f || c16b ? "paired-tiled-u16" : "paired-tiled") : "paired")
-                                  : "separate"),
+                                  : (tiled ? "single-tiled" : "separate")),
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 graph ? "true" : "false");
@@ -1741,22 +1963,91 @@ std::int64_t tiled_ptr(Plan& P, const int* ptr, long long n, DBuf<int>& tptr) {
   return total;
 }
 
+// Tiled streams (see seg_dot2t / seg_dot1) of a[0]'s pattern in both
+// directions, with the values of w systems (2 = the folded pair interleaved):
+// padded pointers, then per direction 16-bit offsets + tile bases when every
+// tile spans < 65536 indices, else int32 indices. Returns false if the padded
+// offsets would overflow int32 (the plan then keeps the plain layout).
+template <class T>
+bool build_tiled_streams(Plan& P, int w) {
+  const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
+  if (nnz + 3 * std::max(rows, cols) >= (1LL << 31)) return false;
+  P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
+  P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
+  const std::size_t tb = sizeof(T);
+  P.rv2.alloc(w * P.tnnz_f * tb);
+  P.cv2.alloc(w * P.tnnz_b * tb);
+  T* rv2 = reinterpret_cast<T*>(P.rv2.get());
+  T* cv2 = reinterpret_cast<T*>(P.cv2.get());
+  // straight from the fp64 CSR/CSC values (no fp32 matrix copies)
+  const auto vals = [&](int s, bool csr) -> const double* {
+    if (s >= w) return nullptr;
+    return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
+  };
+  const int gw = std::max(1, static_cast<int>(std::min<long long>(
+                                 P.ctx->sm_count * 16LL, (std::max(rows, cols) + 7) / 8)));
+  const auto build_dir = [&](bool fwd) {
+    const Matrix& m = *P.a[0];
+    const int* ptr = fwd ? m.rowptr.get() : m.colptr.get();
+    const int* idx = fwd ? m.colidx.get() : m.rowidx.get();
+    const long long n = fwd ? rows : cols;
+    const int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
+    const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
+    const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
+    T* v2 = fwd ? rv2 : cv2;
+    bool& u16 = fwd ? P.c16f : P.c16b;
+    if (u16) {
+      DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
+      DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
+      DBuf<int>& tbase = fwd ? P.tbase_f : P.tbase_b;
+      std::int64_t& ntile = fwd ? P.ntile_f : P.ntile_b;
+      DBuf<int> cnt(n + 1), overflow(1);
+      tfirst.alloc(n + 1);
+      tile_counts_kernel<<<grid1(P.ctx, n + 1), 256, 0, P.ctx->stream>>>(tptr.get(), n, tile,
+                                                                        cnt.get());
+      P.ctx->check_launch("tile_counts_kernel");
+      scan_counts(P.ctx, cnt.get(), tfirst.get(), n);
+      int total = 0;
+      P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
+      ntile = total;
+      tofs.alloc(tn);
+      tbase.alloc(ntile);
+      SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
+      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
+          tbase.get(), v2, tile, overflow.get());
+      P.ctx->check_launch("tile_stream16_kernel");
+      int bad = 0;
+      P.ctx->copy(&bad, overflow.get(), sizeof(int));
+      if (!bad) return;
+      u16 = false;
+      tofs.release();
+      tbase.release();
+      tfirst.release();
+      ntile = 0;
+    }
+    DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
+    tidx.alloc(tn);
+    tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+        ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tidx.get(), v2, tile);
+    P.ctx->check_launch("tile_stream_kernel");
+  };
+  build_dir(true);
+  build_dir(false);
+  P.ctx->sync();
+  return true;
+}
+
 template <class T>
 void build_paired_t(Plan& P) {
   const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
   const std::size_t tb = sizeof(T);
-  if (!P.tiled) P.c16f = P.c16b = false;
-  if (P.tiled) {
-    if (nnz + 3 * std::max(rows, cols) >= (1LL << 31)) {
-      P.tiled = false;  // padded offsets must stay in int32
-      P.c16f = P.c16b = false;
-    } else {
-      P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
-      P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
-    }
+  if (P.tiled && !build_tiled_streams<T>(P, 2)) P.tiled = false;
+  if (!P.tiled) {
+    P.c16f = P.c16b = false;
+    P.rv2.alloc(2 * nnz * tb);
+    P.cv2.alloc(2 * nnz * tb);
   }
-  P.rv2.alloc(2 * (P.tiled ? P.tnnz_f : nnz) * tb);
-  P.cv2.alloc(2 * (P.tiled ? P.tnnz_b : nnz) * tb);
   P.pe.alloc(4 * rows * tb);
   P.cc.alloc(2 * cols * tb);
   SSB_CUDA(cudaMemsetAsync(P.pe.get(), 0, 4 * rows * tb, P.ctx->stream));
@@ -1786,64 +2077,16 @@ void build_paired_t(Plan& P) {
         s);
     P.ctx->check_launch("interleave_kernel");
   }
-  if (P.tiled) {  // straight from the fp64 CSR/CSC values (no fp32 matrix copies)
-    const auto vals = [&](int s, bool csr) -> const double* {
-      return csr ? P.a[s]->val.get() : P.a[s]->cval.get();
-    };
-    const int gw = std::max(1, static_cast<int>(std::min<long long>(
-                                   P.ctx->sm_count * 16LL, (std::max(rows, cols) + 7) / 8)));
-    // per direction: 16-bit offsets + per-tile bases when every tile spans
-    // < 65536 indices (overflow flag from the build), else int32 indices
-    const auto build_dir = [&](bool fwd) {
-      const Matrix& m = *P.a[0];
-      const int* ptr = fwd ? m.rowptr.get() : m.colptr.get();
-      const int* idx = fwd ? m.colidx.get() : m.rowidx.get();
-      const long long n = fwd ? rows : cols;
-      const int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
-      const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
-      const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
-      T* v2 = fwd ? rv2 : cv2;
-      bool& u16 = fwd ? P.c16f : P.c16b;
-      if (u16) {
-        DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
-        DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
-        DBuf<int>& tbase = fwd ? P.tbase_f : P.tbase_b;
-        std::int64_t& ntile = fwd ? P.ntile_f : P.ntile_b;
-        DBuf<int> cnt(n + 1), overflow(1);
-        tfirst.alloc(n + 1);
-        tile_counts_kernel<<<grid1(P.ctx, n + 1), 256, 0, P.ctx->stream>>>(tptr.get(), n, tile,
-                                                                          cnt.get());
-        P.ctx->check_launch("tile_counts_kernel");
-        scan_counts(P.ctx, cnt.get(), tfirst.get(), n);
-        int total = 0;
-        P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
-        ntile = total;
-        tofs.alloc(tn);
-        tbase.alloc(ntile);
-        SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
-        tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
-            tbase.get(), v2, tile, overflow.get());
-        P.ctx->check_launch("tile_stream16_kernel");
-        int bad = 0;
-        P.ctx->copy(&bad, overflow.get(), sizeof(int));
-        if (!bad) return;
-        u16 = false;
-        tofs.release();
-        tbase.release();
-        tfirst.release();
-        ntile = 0;
-      }
-      DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
-      tidx.alloc(tn);
-      tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tidx.get(), v2, tile);
-      P.ctx->check_launch("tile_stream_kernel");
-    };
-    build_dir(true);
-    build_dir(false);
-  }
   P.ctx->sync();
+}
+
+// single-system plans: tiled streams when enabled (else the plain CSR/CSC kernels)
+void build_single(Plan& P) {
+  if (!P.tiled) return;
+  const bool ok = P.dtype == SS_F32 ? build_tiled_streams<float>(P, 1)
+                                    : build_tiled_streams<double>(P, 1);
+  if (!ok) P.tiled = false;
+  if (!P.tiled) P.c16f = P.c16b = false;
 }
 }  // namespace
 
@@ -1955,6 +2198,12 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);
     tr.mark("paired streams");
+  } else if (P->nsys == 1 && nrhs == 1) {
+    P->tiled = env_int("SSB_TILED", 1) != 0;
+    P->c16f = P->c16b = env_int("SSB_U16", 1) != 0;
+    build_single(*P);
+    if (P->tiled) size_single_grid(*P);
+    tr.mark("tiled streams");
   }
   if (P->nsys == 1 && P->empty_rows[0]) fail("sart_solve: matrix has no nonzero rows");
   // a reusable plan replays one captured graph; a one-shot solve enqueues its
@@ -2050,6 +2299,10 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   }
   ctx->check_launch("inv_kernel");
   if (!(max_dev(ctx, rs_full.get(), a->rows) > 0.0)) fail("sart_solve: matrix has no nonzero rows");
+  P->tiled = env_int("SSB_TILED", 1) != 0;  // the row block on the tiled streams
+  P->c16f = P->c16b = env_int("SSB_U16", 1) != 0;
+  build_single(*P);
+  if (P->tiled) size_single_grid(*P);
   ctx->sync();
   return P.release();
 }

@@ -365,3 +365,20 @@ def test_paired_tiled_layouts_match_oracle(span, per_row):
     assert rel_err(got.f, ref.f) <= TOL_F64
     got32 = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0, dtype="f32"))
     assert rel_err(got32.f, ref.f) <= TOL_F32
+
+
+@pytest.mark.parametrize("span,per_row", [(3000, 150), (200000, 8)])
+def test_single_tiled_layouts_match_oracle(span, per_row):
+    """sart_solve on one system: single-system tiled streams (16-bit or int32)."""
+    m, n, r, c, v, p = _wide_centro(11 + span, 64, 90000, per_row, span)
+    a = P.Matrix.from_triplets(m, n, r, c, v)
+    plan = P.SartPlan(a, None, P.SolveOptions(max_iters=9, tol=0.0))
+    d = plan.describe()
+    assert d["layout"] == "single-tiled"
+    assert d["fwd_kernel"].endswith("true>" if span < 65536 else "false>")
+    got = P.sart_solve(a, p, P.SolveOptions(max_iters=9, tol=0.0))
+    ref = O.sart_solve(O.Matrix.triplets(m, n, r, c, v), p, max_iters=9, tol=0.0)
+    assert rel_err(got.f, ref.f) <= TOL_F64
+    h, hr = np.asarray(got.residual_history), np.asarray(ref.residual_history)
+    # late residuals are differences of O(|p|) quantities: compare at |p|*1e-12
+    assert h.shape == hr.shape and np.allclose(h, hr, rtol=1e-10, atol=1e-12 * hr[0])
