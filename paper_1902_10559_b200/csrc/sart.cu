@@ -987,17 +987,37 @@ __global__ void pad4_counts_kernel(const int* __restrict__ ptr, long long n, int
 }
 
 // ------------------------------------------------------------ multi-RHS kernels
-// Slices share A; X/W/P are [n][S] so one warp's 32 lanes read 32 consecutive
-// slices of a gathered row (coalesced 128 B for fp32) while the matrix entry
-// is loaded once per warp and broadcast: matrix bytes amortise over S.
-// One compressed vector against S slices: the warp loads 32 (index, value)
-// pairs coalesced, then broadcasts them 8 at a time so 8 independent
-// slice-row gathers (128 B each for fp32, S = 32) are in flight per lane.
-// Entries past `end` carry value 0 and index 0 (a harmless gather).
-template <class T, int SPL>
+// Slices share A; X/W/P are [n][S] so a warp reads the S slices of one
+// gathered row contiguously while the matrix entry is loaded once per warp and
+// broadcast: matrix bytes amortise over S. Lane l owns the V consecutive slices
+// q*32V + l*V .. +V-1 (q < Q) and moves them with one vector load, so a warp
+// covers 32*V slices per gather instruction.
+// The warp loads 32 (index, value) pairs coalesced, then broadcasts them 8 at
+// a time so 8 independent slice-row gathers are in flight per lane. Entries
+// past `end` carry value 0 and index 0 (a harmless gather).
+template <class T, int V>
+__device__ __forceinline__ void loadv(const T* __restrict__ p, T (&o)[V]) {
+  if constexpr (V == 1) {
+    o[0] = __ldg(p);
+  } else if constexpr (V == 2 && sizeof(T) == 4) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    o[0] = t.x; o[1] = t.y;
+  } else if constexpr (V == 4 && sizeof(T) == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else {
+#pragma unroll
+    for (int h = 0; h < V; h += 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p) + h / 2);
+      o[h] = t.x; o[h + 1] = t.y;
+    }
+  }
+}
+
+template <class T, int V, int Q>
 __device__ __forceinline__ void multi_row_dot(const int* __restrict__ idx, const T* __restrict__ val,
                                               const T* __restrict__ X, int beg, int end,
-                                              int lane, int S, T (&acc)[SPL]) {
+                                              int lane, int S, T (&acc)[Q][V]) {
   for (int base = beg; base < end; base += 32) {
     const int kk = base + lane;
     const int c = kk < end ? __ldg(idx + kk) : 0;
@@ -1016,65 +1036,80 @@ __device__ __forceinline__ void multi_row_dot(const int* __restrict__ idx, const
         }
       }
 #pragma unroll
-      for (int q = 0; q < SPL; ++q) {
-        const int sl = lane + 32 * q;
+      for (int q = 0; q < Q; ++q) {
+        const int sl = (q * 32 + lane) * V;
         if (sl < S) {
-          T g[8];
+          T g[8][V];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) g[u] = __ldg(X + static_cast<long long>(ce[u]) * S + sl);
+          for (int u = 0; u < 8; ++u) loadv<T, V>(X + static_cast<long long>(ce[u]) * S + sl, g[u]);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[q] += ve[u] * g[u];
+          for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc[q][t] += ve[u] * g[u][t];
+          }
         }
       }
     }
   }
 }
 
-template <class T, int SPL>
+template <class T, int V, int Q>
 __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, int it) {
   extern __shared__ double mred[];  // [kWarps][nsys*S]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = k.nrhs;
   const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kThreads) >> 5;
-  double r2a[SPL], r2b[SPL];
-  bool ona[SPL], onb[SPL];
+  double r2a[Q][V], r2b[Q][V];
+  bool ona[Q][V], onb[Q][V];
 #pragma unroll
-  for (int q = 0; q < SPL; ++q) {
-    const int sl = lane + 32 * q;
-    r2a[q] = r2b[q] = 0.0;
-    ona[q] = sl < S && sys_on(k.state, sl);
-    onb[q] = sl < S && k.nsys > 1 && sys_on(k.state, S + sl);
+  for (int q = 0; q < Q; ++q) {
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      const int sl = (q * 32 + lane) * V + t;
+      r2a[q][t] = r2b[q][t] = 0.0;
+      ona[q][t] = sl < S && sys_on(k.state, sl);
+      onb[q][t] = sl < S && k.nsys > 1 && sys_on(k.state, S + sl);
+    }
   }
   for (long long g = gw; g < k.rows_total; g += nw) {
     const int s = g >= k.rows0 ? 1 : 0;
     const SysK<T>& Sy = k.s[s];
     const int i = static_cast<int>(g - (s ? k.rows0 : 0));
-    T acc[SPL];
+    T acc[Q][V];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) acc[q] = T(0);
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int t = 0; t < V; ++t) acc[q][t] = T(0);
+    }
     const int beg = Sy.rp[i], end = Sy.rp[i + 1];
-    multi_row_dot<T, SPL>(Sy.ci, Sy.rv, Sy.x, beg, end, lane, S, acc);
+    multi_row_dot<T, V, Q>(Sy.ci, Sy.rv, Sy.x, beg, end, lane, S, acc);
     const T ri = Sy.rinv[i];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) {
-      const int sl = lane + 32 * q;
-      if (s ? onb[q] : ona[q]) {
-        const long long o = static_cast<long long>(i) * S + sl;
-        const T r = Sy.p[o] - acc[q];
-        Sy.w[o] = ri * r;
-        const double r2 = static_cast<double>(r) * static_cast<double>(r);
-        if (s) r2b[q] += r2; else r2a[q] += r2;
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int t = 0; t < V; ++t) {
+        const int sl = (q * 32 + lane) * V + t;
+        if (s ? onb[q][t] : ona[q][t]) {
+          const long long o = static_cast<long long>(i) * S + sl;
+          const T r = Sy.p[o] - acc[q][t];
+          Sy.w[o] = ri * r;
+          const double r2 = static_cast<double>(r) * static_cast<double>(r);
+          if (s) r2b[q][t] += r2; else r2a[q][t] += r2;
+        }
       }
     }
   }
   const int nsr = k.nsys * S;
 #pragma unroll
-  for (int q = 0; q < SPL; ++q) {
-    const int sl = lane + 32 * q;
-    if (sl < S) {
-      mred[warp * nsr + sl] = r2a[q];
-      if (k.nsys > 1) mred[warp * nsr + S + sl] = r2b[q];
+  for (int q = 0; q < Q; ++q) {
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      const int sl = (q * 32 + lane) * V + t;
+      if (sl < S) {
+        mred[warp * nsr + sl] = r2a[q][t];
+        if (k.nsys > 1) mred[warp * nsr + S + sl] = r2b[q][t];
+      }
     }
   }
   __syncthreads();
@@ -1090,37 +1125,48 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
   }
 }
 
-template <class T, int SPL>
+template <class T, int V, int Q>
 __global__ void __launch_bounds__(kThreads) sart_back_multi_kernel(SartK<T> k, int it) {
   const int lane = threadIdx.x & 31;
   const int S = k.nrhs;
   const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kThreads) >> 5;
-  bool ona[SPL], onb[SPL];
+  bool ona[Q][V], onb[Q][V];
 #pragma unroll
-  for (int q = 0; q < SPL; ++q) {
-    const int sl = lane + 32 * q;
-    ona[q] = sl < S && sys_on(k.state, sl);
-    onb[q] = sl < S && k.nsys > 1 && sys_on(k.state, S + sl);
+  for (int q = 0; q < Q; ++q) {
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      const int sl = (q * 32 + lane) * V + t;
+      ona[q][t] = sl < S && sys_on(k.state, sl);
+      onb[q][t] = sl < S && k.nsys > 1 && sys_on(k.state, S + sl);
+    }
   }
   for (long long g = gw; g < k.cols_total; g += nw) {
     const int s = g >= k.cols0 ? 1 : 0;
     const SysK<T>& Sy = k.s[s];
     const int j = static_cast<int>(g - (s ? k.cols0 : 0));
-    T acc[SPL];
+    T acc[Q][V];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) acc[q] = T(0);
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int t = 0; t < V; ++t) acc[q][t] = T(0);
+    }
     const int beg = Sy.cp[j], end = Sy.cp[j + 1];
-    multi_row_dot<T, SPL>(Sy.ri, Sy.cv, Sy.w, beg, end, lane, S, acc);
+    multi_row_dot<T, V, Q>(Sy.ri, Sy.cv, Sy.w, beg, end, lane, S, acc);
     const T ci = Sy.cinv[j];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) {
-      const int sl = lane + 32 * q;
-      if (s ? onb[q] : ona[q]) {
-        const long long o = static_cast<long long>(j) * S + sl;
-        const T xn = upd(Sy.x[o], k.relax, acc[q], ci);
-        Sy.x[o] = xn;
-        if (!isfinite(static_cast<double>(xn))) atomicCAS(&k.state[4 * (s * S + sl) + 2], 0, it + 1);
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int t = 0; t < V; ++t) {
+        const int sl = (q * 32 + lane) * V + t;
+        if (s ? onb[q][t] : ona[q][t]) {
+          const long long o = static_cast<long long>(j) * S + sl;
+          const T xn = upd(Sy.x[o], k.relax, acc[q][t], ci);
+          Sy.x[o] = xn;
+          if (!isfinite(static_cast<double>(xn))) {
+            atomicCAS(&k.state[4 * (s * S + sl) + 2], 0, it + 1);
+          }
+        }
       }
     }
   }
@@ -1374,6 +1420,21 @@ void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
   fn<<<fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream>>>(k, it);
 }
 
+// multi-RHS kernel: V consecutive slices per lane (vector loads; S % V == 0),
+// Q passes of 32*V slices
+template <class T>
+PairFn<T> multi_kernel(const Plan& P, bool fwd) {
+  const int S = P.nrhs;
+  const int v = S % 4 == 0 && S >= 128 ? 4 : (S % 2 == 0 && S >= 64 ? 2 : 1);
+  const int q = (S + 32 * v - 1) / (32 * v);
+#define SSB_MULTI(V, Q) \
+  if (v == V && q <= Q) return fwd ? sart_fwd_multi_kernel<T, V, Q> : sart_back_multi_kernel<T, V, Q>;
+  SSB_MULTI(1, 1) SSB_MULTI(1, 2) SSB_MULTI(2, 1) SSB_MULTI(2, 2) SSB_MULTI(4, 1) SSB_MULTI(4, 2)
+#undef SSB_MULTI
+  fail("plan: unsupported multi-RHS shape");
+  return nullptr;
+}
+
 template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
   if (P.paired) {
@@ -1385,15 +1446,8 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (P.nrhs > 1) {
-    const int spl = (P.nrhs + 31) / 32;
     const std::size_t sh = sizeof(double) * kWarps * P.nsys * P.nrhs;
-    switch (spl) {
-      case 1: sart_fwd_multi_kernel<T, 1><<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it); break;
-      case 2: sart_fwd_multi_kernel<T, 2><<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it); break;
-      case 3:
-      case 4: sart_fwd_multi_kernel<T, 4><<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it); break;
-      default: sart_fwd_multi_kernel<T, 8><<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it); break;
-    }
+    multi_kernel<T>(P, true)<<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it);
     return;
   }
   switch (P.vs_fwd) {
@@ -1415,14 +1469,7 @@ void launch_back(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (P.nrhs > 1) {
-    const int spl = (P.nrhs + 31) / 32;
-    switch (spl) {
-      case 1: sart_back_multi_kernel<T, 1><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it); break;
-      case 2: sart_back_multi_kernel<T, 2><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it); break;
-      case 3:
-      case 4: sart_back_multi_kernel<T, 4><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it); break;
-      default: sart_back_multi_kernel<T, 8><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it); break;
-    }
+    multi_kernel<T>(P, false)<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
     return;
   }
   switch (P.vs_back) {
@@ -1439,10 +1486,8 @@ int occupancy_blocks(Plan& P, bool fwd) {
   cudaError_t e;
   if (P.nrhs > 1) {
     const std::size_t sh = fwd ? sizeof(double) * kWarps * P.nsys * P.nrhs : 0;
-    e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_fwd_multi_kernel<T, 8>,
-                                                            kThreads, sh)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_back_multi_kernel<T, 8>,
-                                                            kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, multi_kernel<T>(P, fwd), kThreads,
+                                                      sh);
   } else {
     e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_fwd_kernel<T, 32, 4, false>,
                                                             kThreads, 0)

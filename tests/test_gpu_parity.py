@@ -165,10 +165,10 @@ def test_determinism_and_parallelism_invariance():
     assert r1.f.tobytes() == r8.f.tobytes() == r8b.f.tobytes()
 
 
-def test_multi_rhs_plan_matches_single():
+@pytest.mark.parametrize("S", [5, 64, 128, 200])  # 1, 2 and 4 slices per lane (+ a 2nd pass)
+def test_multi_rhs_plan_matches_single(S):
     w, cfg, a, csr, f_true, p, s = workload(1)
     gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
-    S = 5
     rng = np.random.default_rng(7)
     ps1 = np.stack([gs.p1 * (1 + 0.1 * k) + rng.standard_normal(len(gs.p1)) * 0.01 for k in range(S)])
     ps2 = np.stack([gs.p2 * (1 - 0.05 * k) for k in range(S)])
@@ -178,7 +178,7 @@ def test_multi_rhs_plan_matches_single():
     multi.set_rhs(1, ps2.reshape(-1))
     multi.run()
     m1, m2 = multi.solution(0), multi.solution(1)
-    for k in range(S):
+    for k in sorted({0, 1, S // 2, S - 1}):
         single = P.SartPlan(gs.a1, gs.a2, opts)
         single.set_rhs(0, ps1[k])
         single.set_rhs(1, ps2[k])
