@@ -48,6 +48,9 @@ struct Plan {
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphConditionalHandle cond = 0;  // WHILE node of the captured loop
+  DBuf<int> iter_dev;                     // pass counter of the captured loop
+  bool while_capture = false;             // make_args: kernels read / advance iter_dev
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;
   bool launched = false;

@@ -84,7 +84,45 @@ struct SartK {
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
+  // graph WHILE-loop mode: the iteration index lives on the device; the last
+  // block of K1 advances it and decides whether the loop body runs again
+  int* iter;
+  cudaGraphConditionalHandle cond;
+  int max_iters;
 };
+
+// iteration index of this launch: K1 reads the counter K1's last block then
+// advances, so K2 of the same pass sees it + 1. iter[1] != 0 once the loop is
+// over (max_iters reached or every system stopped): the remaining unrolled
+// passes of the WHILE body return at once.
+template <class T>
+__device__ __forceinline__ int pass_index(const SartK<T>& k, int it, bool fwd) {
+  if (!k.iter) return it;
+  const int c = *(volatile const int*)k.iter;
+  return fwd ? c : c - 1;
+}
+
+template <class T>
+__device__ __forceinline__ bool loop_over(const SartK<T>& k) {
+  return k.iter && *(volatile const int*)(k.iter + 1) != 0;
+}
+
+// last block of K1 in WHILE-loop mode: advance the pass counter and run
+// another pass while iterations remain and some system / slice is still on
+template <class T>
+__device__ __forceinline__ void loop_next(const SartK<T>& k, int it) {
+  if (!k.iter || threadIdx.x != 0) return;
+  const int nit = it + 1;
+  k.iter[0] = nit;
+  bool any = false;
+  for (int q = 0; q < k.nsys * k.nrhs && !any; ++q) {
+    const volatile int* st = k.state + 4 * q;  // not stopped, not diverged
+    any = st[0] == 0 && st[2] == 0;
+  }
+  const bool more = nit < k.max_iters && any;
+  k.iter[1] = more ? 0 : 1;
+  cudaGraphSetConditional(k.cond, more ? 1u : 0u);
+}
 
 // ------------------------------------------------------------ loads
 __device__ __forceinline__ void load4(const float* p, float (&v)[4]) {
@@ -323,6 +361,8 @@ __device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, lo
 
 template <class T, int VS, int UF, bool NA>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
   __shared__ double red[2][kWarps];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -353,12 +393,15 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(Sa
   if (last_block(k.ticket)) {
     finish_norms(k.partial, gridDim.x, k.nsys, k.pnorm, k.tol, k.history, k.hstride,
                  k.state, it);
+    loop_next(k, it);
     if (threadIdx.x == 0) *k.ticket = 0;
   }
 }
 
 template <class T, int VS, int UF, bool NA>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, false);
+  if (loop_over(k)) return;
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
   const int split = k.sys_blocks[1];
@@ -581,6 +624,8 @@ __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off
 
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
   using T2 = typename Vec2<T>::type;
   __shared__ double red[2][kWarps];
   const int lane = threadIdx.x & (VS - 1);
@@ -653,12 +698,15 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   }
   if (last_block(k.ticket)) {
     finish_norms(k.partial, gridDim.x, 2, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    loop_next(k, it);
     if (threadIdx.x == 0) *k.ticket = 0;
   }
 }
 
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, false);
+  if (loop_over(k)) return;
   using T2 = typename Vec2<T>::type;
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -764,6 +812,8 @@ __device__ __forceinline__ T seg_dot1(const int* __restrict__ idx,
 
 template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
   __shared__ double red[kWarps];
   const SysK<T>& S = k.s[0];
   const int lane = threadIdx.x & (VS - 1);
@@ -816,12 +866,15 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_ker
   if (k.bp_out) return;  // sharded plans reduce ||r||^2 across ranks instead
   if (last_block(k.ticket)) {
     finish_norms(k.partial, gridDim.x, 1, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    loop_next(k, it);
     if (threadIdx.x == 0) *k.ticket = 0;
   }
 }
 
 template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_tiled_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, false);
+  if (loop_over(k)) return;
   const SysK<T>& S = k.s[0];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -1055,6 +1108,8 @@ __device__ __forceinline__ void multi_row_dot(const int* __restrict__ idx, const
 
 template <class T, int V, int Q>
 __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
   extern __shared__ double mred[];  // [kWarps][nsys*S]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = k.nrhs;
@@ -1121,12 +1176,15 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
   if (last_block(k.ticket)) {
     finish_norms(k.partial, gridDim.x, nsr, k.pnorm, k.tol, k.history, k.hstride,
                  k.state, it);
+    loop_next(k, it);
     if (threadIdx.x == 0) *k.ticket = 0;
   }
 }
 
 template <class T, int V, int Q>
 __global__ void __launch_bounds__(kThreads) sart_back_multi_kernel(SartK<T> k, int it) {
+  it = pass_index(k, it, false);
+  if (loop_over(k)) return;
   const int lane = threadIdx.x & 31;
   const int S = k.nrhs;
   const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
@@ -1352,6 +1410,11 @@ SartK<T> make_args(Plan& P) {
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
+  if (P.while_capture) {
+    k.iter = P.iter_dev.get();
+    k.cond = P.cond;
+  }
+  k.max_iters = P.opts.max_iters;
   return k;
 }
 
@@ -1620,23 +1683,82 @@ void Plan::enqueue_epilogue() {
   ctx->check_launch("deinterleave_kernel");
 }
 
+// passes unrolled per WHILE-body execution (amortises the per-body scheduling)
+constexpr int kPassesPerBody = 8;
+
 void Plan::build_graph() {
   if (graph || sharded) return;  // NCCL calls stay out of the captured graph
+  if (!(opts.tol > 0.0)) {
+    // fixed iteration count (tol = 0 can never stop early): every pass
+    // unrolled into the graph, the cheapest replay (a WHILE node's per-pass
+    // scheduling costs ~5% on config 3)
+    cudaGraph_t g = nullptr;
+    SSB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const std::int64_t before = ctx->launches;
+    try {
+      enqueue_reset();
+      enqueue_iterations(0, opts.max_iters);
+      enqueue_epilogue();
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      ctx->launches = before;
+      throw;
+    }
+    ctx->launches = before;  // captured, not launched
+    SSB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    SSB_CUDA(cudaGraphInstantiate(&graph, g, 0));
+    cudaGraphDestroy(g);
+    return;
+  }
+  // tol > 0: reset nodes, then a WHILE node whose body is one pass (K1 + K2) and whose
+  // condition K1's last block sets, then the epilogue: the loop stops on the
+  // device at the reference's stop test (tol > 0) or after max_iters passes
   cudaGraph_t g = nullptr;
-  SSB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  SSB_CUDA(cudaGraphCreate(&g, 0));
   const std::int64_t before = ctx->launches;
+  cudaStreamCaptureStatus cs;
   try {
+    SSB_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    SSB_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, g, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
     enqueue_reset();
-    enqueue_iterations(0, opts.max_iters);
+    SSB_CUDA(cudaMemsetAsync(iter_dev.get(), 0, 2 * sizeof(int), ctx->stream));
+    const cudaGraphNode_t* deps = nullptr;
+    std::size_t nd = 0;
+    SSB_CUDA(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, nullptr, &deps, &nd));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    SSB_CUDA(cudaGraphAddNode(&cnode, g, deps, nd, &cp));
+    SSB_CUDA(cudaStreamUpdateCaptureDependencies(ctx->stream, &cnode, 1,
+                                                 cudaStreamSetCaptureDependencies));
     enqueue_epilogue();
+    SSB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SSB_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    while_capture = true;
+    enqueue_iterations(0, std::min(opts.max_iters, kPassesPerBody));
+    while_capture = false;
+    SSB_CUDA(cudaStreamEndCapture(ctx->stream, &body));
+    SSB_CUDA(cudaGraphInstantiate(&graph, g, 0));
   } catch (...) {
-    cudaStreamEndCapture(ctx->stream, &g);
-    if (g) cudaGraphDestroy(g);
+    while_capture = false;
+    if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(ctx->stream, &junk);
+      if (junk && junk != g) cudaGraphDestroy(junk);
+    }
+    cudaGraphDestroy(g);
+    ctx->launches = before;
     throw;
   }
   ctx->launches = before;  // captured, not launched
-  SSB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-  SSB_CUDA(cudaGraphInstantiate(&graph, g, 0));
   cudaGraphDestroy(g);
 }
 
@@ -1958,6 +2080,7 @@ void alloc_common(Plan& P) {
   P.history.alloc(static_cast<std::size_t>(nsr) * (P.opts.max_iters + 1));
   P.state.alloc(4 * nsr);
   P.ticket.alloc(1);
+  P.iter_dev.alloc(2);  // WHILE loop: pass counter, loop-over flag
   SSB_CUDA(cudaMemsetAsync(P.state.get(), 0, 4 * nsr * sizeof(int), P.ctx->stream));
   SSB_CUDA(cudaMemsetAsync(P.ticket.get(), 0, sizeof(unsigned), P.ctx->stream));
   SSB_CUDA(cudaEventCreate(&P.ev0));

@@ -382,3 +382,28 @@ def test_single_tiled_layouts_match_oracle(span, per_row):
     h, hr = np.asarray(got.residual_history), np.asarray(ref.residual_history)
     # late residuals are differences of O(|p|) quantities: compare at |p|*1e-12
     assert h.shape == hr.shape and np.allclose(h, hr, rtol=1e-10, atol=1e-12 * hr[0])
+
+
+def test_reusable_plan_stops_on_device_like_the_oracle():
+    """tol > 0: the captured graph is a WHILE loop whose condition K1's last block
+    sets; it must stop at the oracle's iteration with the oracle's history."""
+    rng = np.random.default_rng(31)
+    h1 = 3 * np.eye(40, 30) + rng.uniform(0, 0.1, (40, 30))  # well conditioned: stops
+    h2 = 2 * np.eye(40, 30) + rng.uniform(0, 0.2, (40, 30))  # at ~30 / ~100 passes
+    a = O.reconstruct_matrix(O.Matrix.dense(h1), O.Matrix.dense(h2)).to_dense()
+    p = a @ rng.uniform(0.5, 1.5, 60)
+    split = P.split_system(P.CentroSystem(P.Matrix.dense(a), p, 0.0))
+    opts = P.SolveOptions(max_iters=5000, tol=1e-6)
+    plan = P.SartPlan(split.a1, split.a2, opts)
+    plan.set_rhs(0, split.p1)
+    plan.set_rhs(1, split.p2)
+    for rep in range(2):  # replays reset the loop state
+        r = plan.run()
+        o1 = O.sart_solve(O.Matrix.dense(h1), split.p1, max_iters=5000, tol=1e-6)
+        o2 = O.sart_solve(O.Matrix.dense(h2), split.p2, max_iters=5000, tol=1e-6)
+        assert 0 < o1.iterations < 5000 and 0 < o2.iterations < 5000
+        assert r.iterations == max(o1.iterations, o2.iterations)
+        assert np.allclose(plan.history(0), o1.residual_history, rtol=1e-9, atol=0)
+        assert np.allclose(plan.history(1), o2.residual_history, rtol=1e-9, atol=0)
+        assert rel_err(plan.solution(0), o1.f) <= TOL_F64
+        assert rel_err(plan.solution(1), o2.f) <= TOL_F64
