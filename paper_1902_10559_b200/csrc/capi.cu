@@ -156,15 +156,13 @@ void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double to
                   ss_symmetry_report* rep) {
   if (m != a.rows) ssb::fail("split_system: right-hand side length does not match rows");
   Trace tr(a.ctx);
-  const ss_symmetry_report r = ssb::verify_symmetry(a, tol);
-  tr.mark("  verify_symmetry");
+  ssb::Matrix *x = nullptr, *y = nullptr;
+  const ss_symmetry_report r = ssb::fold_checked(a, tol, x, y);  // verify + fold, one pass
+  tr.mark("  verify_symmetry + fold");
   if (!r.holds) {
     if (rep) *rep = r;
     throw ssb::Failure(SS_ERR_SYMMETRY, symmetry_message("split_system", r, tol));
   }
-  ssb::Matrix *x = nullptr, *y = nullptr;
-  ssb::fold(a, x, y);
-  tr.mark("  fold");
   o.a1.reset(x);
   o.a2.reset(y);
   o.p1.alloc(m / 2);
@@ -606,14 +604,15 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       throw ssb::Failure(code, msg.str());
     };
     const std::int64_t mh = m / 2;
-    std::vector<double> hp(static_cast<std::size_t>(mh));
     const bool cgls = opts->method == SS_METHOD_CGLS;
     const bool dense = opts->method == SS_METHOD_DENSE;
     for (int s = 0; s < 2; ++s) {
-      to_host(c, hp.data(), (s ? o.p2 : o.p1).get(), mh);
       try {
-        check_system(o.a1->rows, hp.data(), mh,
-                     cgls ? "cgls_solve" : (dense ? "pseudo_solve_dense" : "sart_solve"));
+        // check_system on the device-resident folded rhs (lengths match by construction)
+        const char* op = cgls ? "cgls_solve" : (dense ? "pseudo_solve_dense" : "sart_solve");
+        if (!ssb::all_finite_dev(c, (s ? o.p2 : o.p1).get(), mh)) {
+          ssb::fail(std::string(op) + ": non-finite rhs");
+        }
         if (dense) {
           // no options to validate (solvers.cpp:81-97)
         } else if (cgls) {

@@ -221,6 +221,8 @@ void check_finite(Matrix& a);
 std::int64_t nonzeros(Matrix& a);
 ss_symmetry_report verify_symmetry(Matrix& a, double tol);
 void fold(Matrix& a, Matrix*& a1, Matrix*& a2);
+// fold with the symmetry check fused in; !holds -> a1 = a2 = nullptr
+ss_symmetry_report fold_checked(Matrix& a, double tol, Matrix*& a1, Matrix*& a2);
 bool same_pattern(Matrix& a, Matrix& b);
 void scan_counts(Context* ctx, const int* counts_np1, int* ptr, std::int64_t n);
 // dense minimum-norm solve of a (reference pseudo_solve_dense), p and f on the device

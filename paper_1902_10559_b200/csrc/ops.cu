@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 
 #include "internal.hpp"
@@ -374,6 +375,28 @@ __global__ void symmetry_reduce_kernel(const double* rmax, const int* rarg, std:
   if (threadIdx.x == 0) *out = sh[0];
 }
 
+// worst (value, column, row) over the fold's per-output-row candidates
+__global__ void symmetry_reduce3_kernel(const double* d, const int* j, const int* i,
+                                        std::int64_t n, Worst* out) {
+  __shared__ Worst sh[1024];
+  Worst w{0.0, 0x7fffffff, 0x7fffffffffffffffLL};
+  for (std::int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    if (j[t] >= 0) {
+      Worst c{d[t], j[t], i[t]};
+      if (better(c, w)) w = c;
+    }
+  }
+  sh[threadIdx.x] = w;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s && better(sh[threadIdx.x + s], sh[threadIdx.x])) {
+      sh[threadIdx.x] = sh[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
 // ------------------------------------------------------------------ fold
 struct FoldArgs {
   const int* ptr;
@@ -390,6 +413,11 @@ struct FoldArgs {
   double* val1;
   int* col2;
   double* val2;
+  // count pass, optional: the symmetry check fused into the merge (per output
+  // row bi the worst violation of rows bi and M-1-bi: value, column, row)
+  double* sym_d;
+  int* sym_j;
+  int* sym_i;
 };
 
 __device__ __forceinline__ int first_at_least(const int* col, int b, int e, std::int64_t v) {
@@ -446,6 +474,8 @@ __global__ void fold_kernel(FoldArgs a) {
     if (te > tmid) { lo = min(lo, nm1 - ct[te - 1]); hi = max(hi, nm1 - ct[tmid]); }
     if (be > bmid) { lo = min(lo, nm1 - cb[be - 1]); hi = max(hi, nm1 - cb[bmid]); }
     int n1 = 0, n2 = 0;
+    double wd = 0.0;  // fused symmetry check: worst (value, column, row) of this lane
+    std::int64_t wj = 0x7fffffff, wi = 0x7fffffffffffffffLL;
     if (hi >= lo) {
       const std::int64_t span = hi - lo + 1;
       const std::int64_t s_lo = lo + span * lane / 32, s_hi = lo + span * (lane + 1) / 32;
@@ -495,10 +525,33 @@ __global__ void fold_kernel(FoldArgs a) {
             s2 = add(s2, h);
           }
         };
-        if (tl < tl_end && ct[tl] == bj) term(a.val[tl++], false);
-        if (bl < bl_end && cb[bl] == bj) term(a.val[bl++], true);
-        if (tr >= tr_stop && nm1 - ct[tr] == bj) term(a.val[tr--], true);
-        if (br >= br_stop && nm1 - cb[br] == bj) term(a.val[br--], false);
+        const bool hTL = tl < tl_end && ct[tl] == bj;
+        const bool hBL = bl < bl_end && cb[bl] == bj;
+        const bool hTR = tr >= tr_stop && nm1 - ct[tr] == bj;
+        const bool hBR = br >= br_stop && nm1 - cb[br] == bj;
+        const double vTL = hTL ? a.val[tl++] : 0.0, vBL = hBL ? a.val[bl++] : 0.0;
+        const double vTR = hTR ? a.val[tr--] : 0.0, vBR = hBR ? a.val[br--] : 0.0;
+        if (hTL) term(vTL, false);
+        if (hBL) term(vBL, true);
+        if (hTR) term(vTR, true);
+        if (hBR) term(vBR, false);
+        if (!FILL && a.sym_d) {
+          // verify_symmetry's per-entry test (centro.cpp:27-42): every stored
+          // entry against its mirror (absent = 0); TL<->BR and BL<->TR pair up
+          const auto cand = [&](bool h, double v, double mv, std::int64_t j, std::int64_t i) {
+            if (!h) return;
+            const double d = fabs(sub(v, mv));
+            if (d > 0.0 && (d > wd || (d == wd && (j < wj || (j == wj && i < wi))))) {
+              wd = d;
+              wj = j;
+              wi = i;
+            }
+          };
+          cand(hTL, vTL, vBR, bj, top);
+          cand(hBR, vBR, vTL, nm1 - bj, bot);
+          cand(hBL, vBL, vTR, bj, bot);
+          cand(hTR, vTR, vBL, nm1 - bj, top);
+        }
         if (s1 != 0.0) {
           if (FILL) {
             a.col1[o1] = static_cast<int>(bj);
@@ -515,6 +568,24 @@ __global__ void fold_kernel(FoldArgs a) {
           }
           ++n2;
         }
+      }
+    }
+    if (!FILL && a.sym_d) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, wd, off);
+        const long long oj = __shfl_xor_sync(0xffffffffu, static_cast<long long>(wj), off);
+        const long long oi = __shfl_xor_sync(0xffffffffu, static_cast<long long>(wi), off);
+        if (od > wd || (od == wd && (oj < wj || (oj == wj && oi < wi)))) {
+          wd = od;
+          wj = oj;
+          wi = oi;
+        }
+      }
+      if (lane == 0) {
+        a.sym_d[bi] = wd;
+        a.sym_j[bi] = wd > 0.0 ? static_cast<int>(wj) : -1;
+        a.sym_i[bi] = static_cast<int>(wi);
       }
     }
     if (!FILL) {
@@ -1115,20 +1186,49 @@ ss_symmetry_report verify_symmetry(Matrix& a, double tol) {
 constexpr int kFoldSmem = (kT / 32) * kFoldCap * static_cast<int>(sizeof(int));
 static_assert(kFoldSmem <= 48 * 1024, "fold staging must fit the default shared memory");
 
-void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
-  if (a.rows % 2 != 0 || a.cols % 2 != 0) fail("split_matrix: dimensions must be even");
+// The fold with verify_symmetry fused into its count pass (one read of A
+// instead of two): the count pass also reports, per output row, the worst
+// mirror violation of the two source rows; if the reduced maximum exceeds tol
+// the report is returned before the fill pass (a1 = a2 = nullptr), with the
+// same value and first column-major arg-max verify_symmetry gives.
+ss_symmetry_report fold_checked(Matrix& a, double tol, Matrix*& a1, Matrix*& a2) {
+  if (tol < 0) fail("verify_symmetry: tol must be non-negative");
+  ss_symmetry_report rep{};
+  rep.status = a.rows % 2 != 0 ? 1 : (a.cols % 2 != 0 ? 2 : 0);
+  rep.max_violation = 0.0;
+  rep.worst_row = 1;
+  rep.worst_col = 1;
+  a1 = a2 = nullptr;
+  if (rep.status != 0) {
+    rep.holds = 0;
+    return rep;
+  }
   Context* ctx = a.ctx;
   const std::int64_t mh = a.rows / 2, nh = a.cols / 2;
   DBuf<int> lane1(mh * 32), lane2(mh * 32), c1(mh + 1), c2(mh + 1);
+  DBuf<double> sd(std::max<std::int64_t>(mh, 1));
+  DBuf<int> sj(std::max<std::int64_t>(mh, 1)), si(std::max<std::int64_t>(mh, 1));
   SSB_CUDA(cudaMemsetAsync(c1.get() + mh, 0, sizeof(int), ctx->stream));
   SSB_CUDA(cudaMemsetAsync(c2.get() + mh, 0, sizeof(int), ctx->stream));
   FoldArgs fa{a.rowptr.get(), a.colidx.get(), a.val.get(), a.rows, a.cols, mh, nh,
               nullptr, nullptr, lane1.get(), lane2.get(), c1.get(), c2.get(),
-              nullptr, nullptr, nullptr, nullptr};
+              nullptr, nullptr, nullptr, nullptr, sd.get(), sj.get(), si.get()};
   if (mh > 0) {
     fold_kernel<false><<<grid_for(ctx, mh * 32), kT, kFoldSmem, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<count>");
+    DBuf<Worst> w(1);
+    symmetry_reduce3_kernel<<<1, 1024, 0, ctx->stream>>>(sd.get(), sj.get(), si.get(), mh,
+                                                         w.get());
+    ctx->check_launch("symmetry_reduce3_kernel");
+    const Worst hw = read_scalar(ctx, w.get());
+    if (hw.j != 0x7fffffff && hw.d > 0.0) {
+      rep.max_violation = hw.d;
+      rep.worst_row = hw.i + 1;
+      rep.worst_col = hw.j + 1;
+    }
   }
+  rep.holds = rep.max_violation <= tol ? 1 : 0;
+  if (!rep.holds) return rep;
   DBuf<int> p1(mh + 1), p2(mh + 1);
   counts_to_ptr(ctx, c1.get(), p1.get(), mh);
   counts_to_ptr(ctx, c2.get(), p2.get(), mh);
@@ -1142,6 +1242,7 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   fa.val1 = val1.get();
   fa.col2 = col2.get();
   fa.val2 = val2.get();
+  fa.sym_d = nullptr;
   if (mh > 0) {
     fold_kernel<true><<<grid_for(ctx, mh * 32), kT, kFoldSmem, ctx->stream>>>(fa);
     ctx->check_launch("fold_kernel<fill>");
@@ -1149,6 +1250,14 @@ void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
   ctx->sync();
   a1 = matrix_from_csr_device(ctx, mh, nh, n1, std::move(p1), std::move(col1), std::move(val1));
   a2 = matrix_from_csr_device(ctx, mh, nh, n2, std::move(p2), std::move(col2), std::move(val2));
+  return rep;
+}
+
+void fold(Matrix& a, Matrix*& a1, Matrix*& a2) {
+  if (a.rows % 2 != 0 || a.cols % 2 != 0) fail("split_matrix: dimensions must be even");
+  // no tolerance: the fold of any even-sized matrix (split_matrix semantics)
+  const ss_symmetry_report r = fold_checked(a, std::numeric_limits<double>::infinity(), a1, a2);
+  (void)r;
 }
 
 void split_rhs_dev(Context* ctx, const double* p, double* p1, double* p2, std::int64_t mh) {

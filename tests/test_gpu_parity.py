@@ -407,3 +407,44 @@ def test_reusable_plan_stops_on_device_like_the_oracle():
         assert np.allclose(plan.history(1), o2.residual_history, rtol=1e-9, atol=0)
         assert rel_err(plan.solution(0), o1.f) <= TOL_F64
         assert rel_err(plan.solution(1), o2.f) <= TOL_F64
+
+
+def test_fused_fold_symmetry_report_matches_verify_symmetry():
+    """split_system checks symmetry inside the fold's count pass; its report
+    (value, first column-major arg-max, 1-based) must equal verify_symmetry's,
+    including ties, missing mirrors and stored zeros."""
+    rng = np.random.default_rng(77)
+    for trial in range(40):
+        mh, nh = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        h1, h2 = rng.uniform(-1, 1, (mh, nh)), rng.uniform(-1, 1, (mh, nh))
+        a = O.reconstruct_matrix(O.Matrix.dense(h1), O.Matrix.dense(h2)).to_dense()
+        a[np.abs(a) < 0.3] = 0.0
+        r, c = np.nonzero(a)
+        v = a[r, c].copy()
+        kind = trial % 4
+        if kind == 0 and len(v):      # one perturbed entry
+            v[int(rng.integers(len(v)))] += 0.25
+        elif kind == 1 and len(v) > 1:  # two equal violations (tie -> column-major first)
+            idx = rng.choice(len(v), 2, replace=False)
+            v[idx] += 0.5
+        elif kind == 2 and len(v):    # a stored zero where the mirror is non-zero
+            v[int(rng.integers(len(v)))] = 0.0
+        else:                         # an entry whose mirror is absent
+            zr, zc = np.nonzero(a == 0)
+            if len(zr):
+                t = int(rng.integers(len(zr)))
+                r, c, v = np.append(r, zr[t]), np.append(c, zc[t]), np.append(v, 0.75)
+        m = P.Matrix.from_triplets(2 * mh, 2 * nh, r, c, v)
+        want = P.verify_symmetry(m, 0.0)
+        p = np.ones(2 * mh)
+        if want.holds:
+            P.split_system(P.CentroSystem(m, p, 0.0))
+            continue
+        with pytest.raises(P.SymmetryError) as ei:
+            P.split_system(P.CentroSystem(m, p, 0.0))
+        got = ei.value.report
+        assert (got.max_violation, got.worst_row, got.worst_col, got.status) == \
+            (want.max_violation, want.worst_row, want.worst_col, want.status)
+        ref = O.verify_symmetry(O.Matrix.triplets(2 * mh, 2 * nh, r, c, v), 0.0)
+        assert (ref.max_violation, ref.worst_row, ref.worst_col) == \
+            (want.max_violation, want.worst_row, want.worst_col)
