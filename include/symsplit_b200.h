@@ -147,6 +147,15 @@ int ss_snake_inverse(int j, const ss_grid_spec* grid, int* c, int* r);
  * pass rays4 = NULL to query the count */
 int ss_enumerate_rays(const ss_scan_config* cfg, double* rays4, int64_t* count,
                       int* samples, double* pitch);
+/* replaces emitter_angles (geometry.cpp:107-117): k angles, most negative first */
+int ss_emitter_angles(const ss_scan_config* cfg, double* angles);
+/* replaces emitter_positions (geometry.cpp:119-130): k sources as (x, y) pairs */
+int ss_emitter_positions(const ss_scan_config* cfg, double center_x, double* xy);
+/* replaces ray_weights (geometry.cpp:175-225) for one ray (source x, y,
+ * detector x, y), walked on the device with the build's tracer: 1-based snake
+ * columns and lengths in path order; pass capacity 0 to query the count */
+int ss_ray_weights(ss_ctx_t ctx, const double ray4[4], const ss_grid_spec* grid, int64_t capacity,
+                   int* cols, double* lens, int64_t* count);
 /* replaces build_system (geometry.cpp:227-275): GPU Siddon trace of rays
  * 0..M/2-1, mirror rows by reflection; returns A (M x N) on the device */
 int ss_build_system(ss_ctx_t ctx, const ss_scan_config* cfg, int parallelism,

@@ -416,6 +416,44 @@ inline int snake_index(int c, int r, const GridSpec& g) {
   return j;
 }
 
+// reference geometry.hpp:74-88 (Point, Ray)
+struct Point {
+  double x = 0.0, y = 0.0;
+};
+struct Ray {
+  Point source, detector;
+};
+
+// reference geometry.cpp:107-117
+inline std::vector<double> emitter_angles(const ScanConfig& c) {
+  std::vector<double> a(static_cast<std::size_t>(c.k > 0 ? c.k : 0));
+  detail::check(ss_emitter_angles(&c, a.data()));
+  return a;
+}
+
+// reference geometry.cpp:119-130
+inline std::vector<Point> emitter_positions(const ScanConfig& c, double center_x = 0.0) {
+  std::vector<double> xy(2 * static_cast<std::size_t>(c.k > 0 ? c.k : 0));
+  detail::check(ss_emitter_positions(&c, center_x, xy.data()));
+  std::vector<Point> out(xy.size() / 2);
+  for (std::size_t i = 0; i < out.size(); ++i) out[i] = Point{xy[2 * i], xy[2 * i + 1]};
+  return out;
+}
+
+// reference geometry.cpp:175-225 (1-based snake columns, path order), device tracer
+inline std::vector<std::pair<int, double>> ray_weights(
+    const Ray& ray, const GridSpec& g, const Context& ctx = Context::default_context()) {
+  const double r4[4] = {ray.source.x, ray.source.y, ray.detector.x, ray.detector.y};
+  int64_t n = 0;
+  detail::check(ss_ray_weights(ctx.get(), r4, &g, 0, nullptr, nullptr, &n));
+  std::vector<int> cols(static_cast<std::size_t>(n));
+  Vector lens(static_cast<std::size_t>(n));
+  detail::check(ss_ray_weights(ctx.get(), r4, &g, n, cols.data(), lens.data(), &n));
+  std::vector<std::pair<int, double>> out(cols.size());
+  for (std::size_t q = 0; q < cols.size(); ++q) out[q] = {cols[q], lens[q]};
+  return out;
+}
+
 // reference geometry.hpp:118: A on the GPU, p = 0, symmetry_tol = 0
 inline CentroSystem build_system(const ScanConfig& cfg, int parallelism = 0,
                                  const Context& ctx = Context::default_context()) {

@@ -6,7 +6,8 @@ is its Python mirror of the reference API. No CPU fallback exists.
 """
 from .symsplit import (  # noqa: F401
     CentroSystem, Context, DeviceError, Error, Matrix, SartPlan, SolutionPair, SolveOptions,
-    IoError, cgls_solve, pseudo_solve_dense, shepp_logan_ellipses, read_matrix_market, read_vector_csv, write_matrix_market,
+    IoError, cgls_solve, emitter_angles, emitter_positions, pseudo_solve_dense, ray_weights,
+    shepp_logan_ellipses, read_matrix_market, read_vector_csv, write_matrix_market,
     write_vector_csv,
     SolveReport, SplitSystem, SymmetryError, SymmetryReport, SymsplitError, build_system,
     decompose_solution, default_context, degrees_to_radians, enumerate_rays, forward_project,

@@ -94,6 +94,9 @@ SIGNATURES = {
     "ss_sart_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
                                 C.POINTER(SolveReportC), dp]),
     "ss_pseudo_solve_dense": (C.c_int, [vp, dp, i64, i64, dp, i64]),
+    "ss_emitter_angles": (C.c_int, [C.POINTER(ScanConfig), dp]),
+    "ss_emitter_positions": (C.c_int, [C.POINTER(ScanConfig), C.c_double, dp]),
+    "ss_ray_weights": (C.c_int, [vp, dp, C.POINTER(GridSpec), i64, i32p, dp, i64p]),
     "ss_cgls_solve": (C.c_int, [vp, dp, i64, C.POINTER(SolveOptionsC), dp, i64,
                                 C.POINTER(SolveReportC), dp]),
     "ss_solve_split": (C.c_int, [vp, dp, i64, C.c_double, C.POINTER(SolveOptionsC), dp, i64,

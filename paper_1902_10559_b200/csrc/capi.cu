@@ -533,6 +533,48 @@ int ss_cgls_solve(ss_matrix_t a, const double* p, int64_t m, const ss_solve_opti
   });
 }
 
+int ss_emitter_angles(const ss_scan_config* cfg, double* angles) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(angles, "angles");
+    const std::vector<double> a = ssb::emitter_angles(*cfg);
+    std::copy(a.begin(), a.end(), angles);
+  });
+}
+
+int ss_emitter_positions(const ss_scan_config* cfg, double center_x, double* xy) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(xy, "xy");
+    std::vector<double> x, y;
+    ssb::emitter_positions(*cfg, center_x, x, y);
+    for (std::size_t i = 0; i < x.size(); ++i) {
+      xy[2 * i] = x[i];
+      xy[2 * i + 1] = y[i];
+    }
+  });
+}
+
+int ss_ray_weights(ss_ctx_t h, const double ray4[4], const ss_grid_spec* grid, int64_t capacity,
+                   int* cols, double* lens, int64_t* count) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(ray4, "ray4");
+    need(count, "count");
+    use_device(ctx);
+    std::vector<int> c;
+    std::vector<double> l;
+    ssb::ray_weights_dev(ctx, ray4[0], ray4[1], ray4[2], ray4[3], to_grid(grid), c, l);
+    *count = static_cast<int64_t>(c.size());
+    if (capacity <= 0) return;
+    if (capacity < *count) ssb::fail("ray_weights: capacity too small");
+    need(cols, "cols");
+    need(lens, "lens");
+    std::copy(c.begin(), c.end(), cols);
+    std::copy(l.begin(), l.end(), lens);
+  });
+}
+
 int ss_pseudo_solve_dense(ss_matrix_t a, const double* p, int64_t m, int64_t dense_cap,
                           double* f, int64_t n) {
   return guarded([&] {

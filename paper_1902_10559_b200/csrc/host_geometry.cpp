@@ -84,9 +84,9 @@ std::pair<int, int> snake_inverse(int j, const Grid& g) {
 // mirrored list reversed so ray M-1-i reflects ray i. Only the traced half
 // (i < M/2) is kept in SoA form, with the exact clip range and hypot length
 // the device walk needs.
-RayTable enumerate_rays(const ss_scan_config& c, const Grid& g, bool keep_all) {
+// reference geometry.cpp:107-117: most negative first, upper half exact sign flips
+std::vector<double> emitter_angles(const ss_scan_config& c) {
   validate_geometry(c);
-  g.validate();
   const int k = c.k;
   std::vector<double> ang(k);
   const double step = 2.0 * c.gamma / (k - 1);
@@ -94,14 +94,37 @@ RayTable enumerate_rays(const ss_scan_config& c, const Grid& g, bool keep_all) {
     ang[i] = -c.gamma + i * step;
     ang[k - 1 - i] = -ang[i];
   }
-  const double cx = g.center_x;
-  std::vector<double> srcx(k), srcy(k);
+  return ang;
+}
+
+// reference geometry.cpp:119-130: sources on the circle of radius h_e about
+// (cx, h_m); the upper half reflected about x = cx (bitwise mirror pairs)
+void emitter_positions(const ss_scan_config& c, double cx, std::vector<double>& srcx,
+                       std::vector<double>& srcy) {
+  const std::vector<double> ang = emitter_angles(c);
+  const int k = c.k;
+  srcx.assign(k, 0.0);
+  srcy.assign(k, 0.0);
   for (int i = 0; i < k / 2; ++i) {
     srcx[i] = cx + c.h_e * std::sin(ang[i]);
     srcy[i] = c.h_m + c.h_e * std::cos(ang[i]);
     srcx[k - 1 - i] = 2.0 * cx - srcx[i];
     srcy[k - 1 - i] = srcy[i];
   }
+}
+
+bool clip_ray(double sx, double sy, double ex, double ey, const Grid& g, double& t_in,
+              double& t_out) {
+  return clip_segment(sx, sy, ex, ey, g, t_in, t_out);
+}
+
+RayTable enumerate_rays(const ss_scan_config& c, const Grid& g, bool keep_all) {
+  validate_geometry(c);
+  g.validate();
+  const int k = c.k;
+  const double cx = g.center_x;
+  std::vector<double> srcx, srcy;
+  emitter_positions(c, cx, srcx, srcy);
   const double native = c.l_m / c.n_p;
   const double pitch = std::max(native, 0.5 * g.voxel_size);
   const int samples = std::max(1, static_cast<int>(std::floor(c.l_m / pitch)));

@@ -197,6 +197,15 @@ struct RayTable {  // traced half, structure of arrays (host)
 void validate_geometry(const ss_scan_config& c);
 Grid make_grid(const ss_scan_config& c);
 RayTable enumerate_rays(const ss_scan_config& c, const Grid& g, bool keep_all);
+std::vector<double> emitter_angles(const ss_scan_config& c);
+void emitter_positions(const ss_scan_config& c, double center_x, std::vector<double>& x,
+                       std::vector<double>& y);
+bool clip_ray(double sx, double sy, double ex, double ey, const Grid& g, double& t_in,
+              double& t_out);
+// reference ray_weights (geometry.cpp:175-225) for one ray, walked on the
+// device with the build's tracer: (1-based snake column, length) in path order
+void ray_weights_dev(Context* ctx, double sx, double sy, double ex, double ey, const Grid& g,
+                     std::vector<int>& cols, std::vector<double>& lens);
 ss_scan_config parse_scan_config(const std::string& text);
 int snake_index(int c, int r, const Grid& g);
 std::pair<int, int> snake_inverse(int j, const Grid& g);

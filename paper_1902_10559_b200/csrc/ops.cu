@@ -1098,6 +1098,51 @@ std::int64_t nonzeros(Matrix& a) {
 // GPU build_system (geometry.cpp:227-275): count -> scan -> fill of the
 // traced half, stable (row,col) radix sort (repeats collapse in traversal
 // order, as setFromTriplets would sum them), then the mirror half.
+void ray_weights_dev(Context* ctx, double sx, double sy, double ex, double ey, const Grid& g,
+                     std::vector<int>& cols, std::vector<double>& lens) {
+  g.validate();
+  cols.clear();
+  lens.clear();
+  const double dx = ex - sx, dy = ey - sy;
+  const double seg = std::hypot(dx, dy);
+  if (seg == 0.0) fail("ray_weights: degenerate ray");
+  double tin = 0.0, tout = 0.0;
+  if (!clip_ray(sx, sy, ex, ey, g, tin, tout)) return;
+  std::vector<double> xb(g.n_x + 1), yb(g.n_y + 1);
+  for (int k = 0; k <= g.n_x; ++k) xb[k] = g.center_x + (k - g.n_x / 2) * g.voxel_size;
+  for (int k = 0; k <= g.n_y; ++k) yb[k] = g.y_bottom + k * g.voxel_size;
+  const double ray7[7] = {sx, sy, dx, dy, seg, tin, tout};
+  DBuf<double> d_ray(7), d_xb(xb.size()), d_yb(yb.size());
+  upload(ctx, d_ray.get(), ray7, 7);
+  upload(ctx, d_xb.get(), xb.data(), xb.size());
+  upload(ctx, d_yb.get(), yb.data(), yb.size());
+  TraceArgs ta{d_ray.get(),     d_ray.get() + 1, d_ray.get() + 2, d_ray.get() + 3,
+               d_ray.get() + 4, d_ray.get() + 5, d_ray.get() + 6, d_xb.get(),
+               d_yb.get(),      g.n_x,           g.n_y,           g.voxel_size,
+               g.x_left(),      g.y_bottom,      1};
+  DBuf<int> count(1);
+  trace_count_kernel<<<1, 32, 0, ctx->stream>>>(ta, count.get());
+  ctx->check_launch("trace_count_kernel");
+  const int n = read_scalar(ctx, count.get());
+  DBuf<std::int64_t> off(1);
+  SSB_CUDA(cudaMemsetAsync(off.get(), 0, sizeof(std::int64_t), ctx->stream));
+  DBuf<unsigned long long> keys(std::max(n, 1));
+  DBuf<double> vals(std::max(n, 1));
+  trace_fill_kernel<<<1, 32, 0, ctx->stream>>>(ta, off.get(), keys.get(), vals.get());
+  ctx->check_launch("trace_fill_kernel");
+  std::vector<unsigned long long> hk(n);
+  lens.resize(n);
+  if (n) {
+    SSB_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    SSB_CUDA(cudaMemcpyAsync(lens.data(), vals.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  }
+  ctx->sync();
+  cols.resize(n);
+  for (int q = 0; q < n; ++q) cols[q] = static_cast<int>(hk[q] & 0xffffffffull) + 1;
+}
+
 Matrix* build_system(Context* ctx, const ss_scan_config& cfg) {
   const Grid g = make_grid(cfg);
   const RayTable rt = enumerate_rays(cfg, g, false);

@@ -508,6 +508,34 @@ def snake_inverse(j, grid: N.GridSpec):
     return c.value, r.value
 
 
+def emitter_angles(cfg: N.ScanConfig):
+    """geometry.cpp:107-117 (host, libm): k angles, most negative first."""
+    out = np.empty(cfg.k)
+    _check(_lib().ss_emitter_angles(C.byref(cfg), _dp(out)))
+    return out
+
+
+def emitter_positions(cfg: N.ScanConfig, center_x: float = 0.0):
+    """geometry.cpp:119-130: k sources as rows (x, y), mirrored bitwise about center_x."""
+    out = np.empty((cfg.k, 2))
+    _check(_lib().ss_emitter_positions(C.byref(cfg), C.c_double(center_x), _dp(out)))
+    return out
+
+
+def ray_weights(ray4, grid: N.GridSpec, ctx: Optional[Context] = None):
+    """geometry.cpp:175-225 for one ray (source x, y, detector x, y) on the
+    device tracer: (1-based snake columns, lengths) in path order."""
+    ctx = ctx or default_context()
+    r = _f64(ray4).reshape(4)
+    n = N.i64()
+    _check(_lib().ss_ray_weights(ctx.h, _dp(r), C.byref(grid), 0, None, None, C.byref(n)))
+    cols = np.empty(n.value, np.int32)
+    lens = np.empty(n.value)
+    _check(_lib().ss_ray_weights(ctx.h, _dp(r), C.byref(grid), n.value, _ip(cols), _dp(lens),
+                                 C.byref(n)))
+    return cols, lens
+
+
 def enumerate_rays(cfg: N.ScanConfig):
     """geometry.cpp:132-173 -> (rays[M,4] as (sx,sy,dx,dy), samples, pitch)"""
     cnt, samples, pitch = N.i64(), C.c_int(), C.c_double()

@@ -1,6 +1,7 @@
 // C++ facade (include/symsplit_b200.hpp) exercised like the reference's own
 // doctest unit tests (proj/tests/unit/test_centro.cpp, test_solvers.cpp),
 // checked against the oracle (test infrastructure). Prints "ALL PASSED".
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -103,6 +104,29 @@ int main() {
     }
     CHECK(std::sqrt(num / den) <= 1e-10);
     CHECK(got.iterations == 50 && got.mode == Mode::split);
+  }
+  {  // geometry entry points (geometry.cpp:107-225) against the oracle, bit for bit
+    ScanConfig c = parse_scan_config("k 10\ngamma_deg 18\nh_e 2.0\nh_m 1e-4\n");
+    oracle::ScanGeometry og;
+    og.k = 10;
+    og.gamma = oracle::degrees_to_radians(18.0);
+    og.h_e = 2.0;
+    og.h_m = 1e-4;
+    const std::vector<double> a = emitter_angles(c);
+    const std::vector<double> oa = oracle::emitter_angles(og);
+    CHECK(a.size() == oa.size() && std::equal(a.begin(), a.end(), oa.begin()));
+    const std::vector<Point> pos = emitter_positions(c, 0.0);
+    const auto opos = oracle::emitter_positions(og, 0.0);
+    bool same = pos.size() == opos.size();
+    for (std::size_t i = 0; same && i < pos.size(); ++i) {
+      same = pos[i].x == opos[i].x && pos[i].y == opos[i].y;
+    }
+    CHECK(same);
+    GridSpec g{4, 5, 0.1, 0.0, 1.0};
+    const double xc = (2 - 0.5 - 0.5 * 4) * 0.1;
+    const auto w = ray_weights(Ray{{xc, 3.0}, {xc, 0.0}}, g);
+    CHECK(w.size() == 5);
+    for (const auto& e : w) CHECK(std::abs(e.second - 0.1) <= 1e-12);
   }
   if (failures == 0) std::printf("ALL PASSED\n");
   return failures == 0 ? 0 : 1;
