@@ -624,6 +624,7 @@ __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off
 
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
+  cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, true);
   if (loop_over(k)) return;
   using T2 = typename Vec2<T>::type;
@@ -705,6 +706,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
 
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
+  cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, false);
   if (loop_over(k)) return;
   using T2 = typename Vec2<T>::type;
@@ -812,6 +814,7 @@ __device__ __forceinline__ T seg_dot1(const int* __restrict__ idx,
 
 template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_kernel(SartK<T> k, int it) {
+  cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, true);
   if (loop_over(k)) return;
   __shared__ double red[kWarps];
@@ -873,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_ker
 
 template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_tiled_kernel(SartK<T> k, int it) {
+  cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, false);
   if (loop_over(k)) return;
   const SysK<T>& S = k.s[0];
@@ -1343,6 +1347,11 @@ int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+bool pdl_enabled() {
+  static const bool on = env_int("SSB_PDL", 1) != 0;
+  return on;
+}
+
 // Lanes per compressed vector. Several vectors per warp keep independent
 // dependency chains in flight; adjacent rows (rays) share x lines in L1.
 int pick_vs(double avg) {
@@ -1476,11 +1485,30 @@ PairFn<T> single_kernel(const Plan& P, bool fwd) {
 
 bool single_tiled(const Plan& P) { return !P.paired && P.tiled && P.nrhs == 1 && P.nsys == 1; }
 
+// Launch with programmatic dependent launch: the kernel's CTAs are scheduled
+// while the previous pass's tail drains and wait in cudaGridDependencySynchronize
+// (the first statement of every kernel launched this way) for its results.
+template <class T>
+void launch_pdl(PairFn<T> fn, int grid, int block, std::size_t smem, cudaStream_t st,
+                const SartK<T>& k, int it) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, fn, k, it));
+}
+
 template <class T>
 void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
   int smem = 0;
   const PairFn<T> fn = pair_kernel<T>(P, fwd, &smem);
-  fn<<<fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream>>>(k, it);
+  launch_pdl<T>(fn, fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream, k, it);
 }
 
 // multi-RHS kernel: V consecutive slices per lane (vector loads; S % V == 0),
@@ -1505,7 +1533,7 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (single_tiled(P)) {
-    single_kernel<T>(P, true)<<<P.fwd_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
+    launch_pdl<T>(single_kernel<T>(P, true), P.fwd_blocks, kThreads, 0, P.ctx->stream, k, it);
     return;
   }
   if (P.nrhs > 1) {
@@ -1528,7 +1556,7 @@ void launch_back(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (single_tiled(P)) {
-    single_kernel<T>(P, false)<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
+    launch_pdl<T>(single_kernel<T>(P, false), P.back_blocks, kThreads, 0, P.ctx->stream, k, it);
     return;
   }
   if (P.nrhs > 1) {
