@@ -686,12 +686,21 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
           if (codes[s] != SS_OK) code = codes[s];
         }
       }
-      if (cgls) {  // likewise concurrent (context stream + side stream)
+      if (cgls) {
+        // both systems in one loop over the paired streams (independent scalars
+        // and stop tests), or concurrent single-system solves on two streams
         ssb::Matrix* am[2] = {o.a1.get(), o.a2.get()};
         const double* pm[2] = {o.p1.get(), o.p2.get()};
         double* fm[2] = {f1.get(), f2.get()};
         int codes[2] = {SS_OK, SS_OK};
-        ssb::cgls_device_pair(am, pm, *opts, fm, rb, errs, codes);
+        // small systems are launch-latency bound: two concurrent streams win there
+        const char* e = std::getenv("SSB_CGLS_PAIRED");
+        const bool paired = e && *e ? *e != '0' : o.a1->nnz >= 1000000;
+        if (paired) {
+          ssb::cgls_device_paired(o.a1.get(), o.a2.get(), pm, *opts, fm, rb, errs, codes);
+        } else {
+          ssb::cgls_device_pair(am, pm, *opts, fm, rb, errs, codes);
+        }
         for (int s = 0; s < 2; ++s) {
           if (codes[s] != SS_OK) code = codes[s];
         }

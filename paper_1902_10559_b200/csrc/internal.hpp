@@ -259,6 +259,9 @@ void forward_project_dev(Matrix& a, const double* f, double* p);
 // CGLS (cgls.cu): f_dev receives x in fp64; report gets iterations/history/time
 void cgls_device_pair(Matrix* a[2], const double* p[2], const ss_solve_options& o, double* f[2],
                       ss_solve_report rep[2], std::string errs[2], int codes[2]);
+// both folded systems in one CGLS loop over the paired tiled streams (sart.cu)
+void cgls_device_paired(Matrix* a1, Matrix* a2, const double* p[2], const ss_solve_options& o,
+                        double* f[2], ss_solve_report rep[2], std::string errs[2], int codes[2]);
 void cgls_device(Matrix& a, const double* p_dev, const ss_solve_options& o, double* f_dev,
                  ss_solve_report* rep, double* hist_host);
 

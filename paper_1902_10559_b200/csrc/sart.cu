@@ -2503,4 +2503,423 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   return P.release();
 }
 
+// ====================================================================== paired CGLS
+// CGLS (reference cgls_solve, solvers.cpp:99-146) on both folded systems at
+// once, over the SART plan's paired tiled streams: one index stream and
+// interleaved {a1, a2} values, iterates interleaved {x1, x2}, each system with
+// its own scalars and stop / break state (the two branches stay independent
+// solves, as in the reference). The loop is a CUDA-graph WHILE node; the last
+// block of the transposed product decides whether another pass runs.
+namespace {
+
+template <class T>
+struct CgPairK {
+  SartK<T> sk;     // stream layout (tiled pointers, indices / offsets, values)
+  T *x, *r, *s, *d, *q;  // interleaved [n][2]
+  long long rows, cols;
+  double* part;    // [2][grid]
+  double* sc;      // [2][5] gamma, alpha, beta, stop, rnorm2
+  int* st;         // [2][5] done, iterations, err_step_at, err_res_at, -
+  int* loop;       // pass counter, loop-over flag (the WHILE body unrolls passes)
+  unsigned* ticket;
+  double* hist;    // [2][hstride]
+  int hstride;
+  double tol;
+  int max_iters;
+  cudaGraphConditionalHandle cond;
+};
+
+__device__ __forceinline__ bool cg_on(const int* st, int s) {
+  return *(volatile const int*)(st + 5 * s) == 0;
+}
+
+// fixed-order block sums of two values, then of the per-block partials by the
+// last block (returns true there, with the totals)
+__device__ __forceinline__ bool two_sums(double va, double vb, double* part, unsigned* ticket,
+                                         double& ta, double& tb) {
+  __shared__ double red[2][kWarps];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    va += __shfl_xor_sync(0xffffffffu, va, o);
+    vb += __shfl_xor_sync(0xffffffffu, vb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = va;
+    red[1][threadIdx.x >> 5] = vb;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int w = 0; w < kWarps; ++w) t += red[threadIdx.x][w];
+    part[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+  if (!last_block(ticket)) return false;
+  __shared__ double sh[2][kThreads];
+  for (int q = 0; q < 2; ++q) {
+    double t = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) t += part[q * gridDim.x + b];
+    sh[q][threadIdx.x] = t;
+  }
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + o];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  ta = sh[0][0];
+  tb = sh[1][0];
+  if (threadIdx.x == 0) *ticket = 0;
+  return true;
+}
+
+// grid-stride sweep of the paired stream of one direction: (a, b) = dot
+// products of vector g with the interleaved vector `vec`, handed to epi on lane 0
+template <class T, int VS, int UF, int TL, bool FWD, class Epi>
+__device__ __forceinline__ void pair_sweep(const SartK<T>& k, long long n,
+                                           const typename Vec2<T>::type* __restrict__ vec,
+                                           Epi&& epi) {
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int* __restrict__ ptr = FWD ? k.tpf : k.tpb;
+  const int* __restrict__ tfp = FWD ? k.tff : k.tfb;
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
+  int beg = 0, end = 0, tf = 0;
+  if (g < n) {
+    beg = __ldg(ptr + g);
+    end = __ldg(ptr + g + 1);
+    if (TL == 2) tf = __ldg(tfp + g);
+  }
+  for (; g < n; g += gstep) {
+    const int gn = g + gstep;
+    int nbeg = 0, nend = 0, ntf = 0;
+    if (gn < n) {
+      nbeg = __ldg(ptr + gn);
+      nend = __ldg(ptr + gn + 1);
+      if (TL == 2) ntf = __ldg(tfp + gn);
+    }
+    T a, b;
+    if (TL == 2) {
+      seg_dot2c<T, VS, UF>(FWD ? k.tof : k.tob, FWD ? k.tbf : k.tbb, tf, FWD ? k.rv2 : k.cv2,
+                           vec, beg, end, lane, mask, a, b);
+    } else {
+      seg_dot2t<T, VS, UF>(FWD ? k.tif : k.tib, FWD ? k.rv2 : k.cv2, vec, beg, end, lane, mask,
+                           a, b);
+    }
+    if (lane == 0) epi(g, a, b);
+    beg = nbeg;
+    end = nend;
+    tf = ntf;
+  }
+}
+
+// q = A d (both systems); alpha = gamma / ||q||^2, or break when ||q|| = 0
+template <class T, int VS, int UF, int TL>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) cgp_fwd_kernel(CgPairK<T> k) {
+  using T2 = typename Vec2<T>::type;
+  if (*(volatile const int*)(k.loop + 1)) return;
+  const int it = *(volatile const int*)k.loop;
+  const bool on0 = cg_on(k.st, 0), on1 = cg_on(k.st, 1);
+  double qa = 0.0, qb = 0.0;
+  if (on0 || on1) {
+    pair_sweep<T, VS, UF, TL, true>(k.sk, k.rows, reinterpret_cast<const T2*>(k.d),
+                                    [&](int g, T a, T b) {
+      T2 o;
+      o.x = a;
+      o.y = b;
+      reinterpret_cast<T2*>(k.q)[g] = o;
+      qa += static_cast<double>(a) * static_cast<double>(a);
+      qb += static_cast<double>(b) * static_cast<double>(b);
+    });
+  }
+  double ta, tb;
+  if (!two_sums(qa, qb, k.part, k.ticket, ta, tb) || threadIdx.x != 0) return;
+  for (int s = 0; s < 2; ++s) {
+    if (!cg_on(k.st, s)) continue;
+    const double tot = s ? tb : ta;
+    double* sc = k.sc + 5 * s;
+    int* st = k.st + 5 * s;
+    if (tot == 0.0) {
+      st[0] = 1;  // d in the null space: break (solvers.cpp:124-126)
+    } else {
+      const double alpha = sc[0] / tot;
+      sc[1] = alpha;
+      if (!isfinite(alpha)) {
+        st[2] = it + 1;
+        st[0] = 1;
+      }
+    }
+  }
+}
+
+// x += alpha d, r -= alpha q, ||r||^2 (solvers.cpp:130-131, :142)
+template <class T>
+__global__ void __launch_bounds__(kThreads) cgp_axpy_kernel(CgPairK<T> k) {
+  if (*(volatile const int*)(k.loop + 1)) return;
+  const bool on[2] = {cg_on(k.st, 0), cg_on(k.st, 1)};
+  if (!on[0] && !on[1]) return;
+  const T al[2] = {static_cast<T>(k.sc[1]), static_cast<T>(k.sc[5 + 1])};
+  const long long tid = blockIdx.x * (long long)kThreads + threadIdx.x;
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long j = tid; j < 2 * k.cols; j += stride) {
+    const int s = static_cast<int>(j & 1);
+    if (on[s]) k.x[j] = k.x[j] + al[s] * k.d[j];
+  }
+  double ra = 0.0, rb = 0.0;
+  for (long long i = tid; i < 2 * k.rows; i += stride) {
+    const int s = static_cast<int>(i & 1);
+    if (!on[s]) continue;
+    const T ri = k.r[i] - al[s] * k.q[i];
+    k.r[i] = ri;
+    const double r2 = static_cast<double>(ri) * static_cast<double>(ri);
+    if (s) rb += r2; else ra += r2;
+  }
+  double ta, tb;
+  if (!two_sums(ra, rb, k.part, k.ticket, ta, tb) || threadIdx.x != 0) return;
+  if (on[0]) k.sc[4] = ta;
+  if (on[1]) k.sc[5 + 4] = tb;
+}
+
+// s = A^T r (both systems). init: gamma0 and the stop level (solvers.cpp:
+// 115-120); else beta, gamma, history, stop test (:132-141) and the WHILE
+// condition of the next pass
+template <class T, int VS, int UF, int TL>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks) cgp_back_kernel(CgPairK<T> k, int init) {
+  using T2 = typename Vec2<T>::type;
+  if (!init && *(volatile const int*)(k.loop + 1)) return;
+  const int it = *(volatile const int*)k.loop;
+  const bool on0 = cg_on(k.st, 0), on1 = cg_on(k.st, 1);
+  double sa = 0.0, sb = 0.0;
+  if (init || on0 || on1) {
+    pair_sweep<T, VS, UF, TL, false>(k.sk, k.cols, reinterpret_cast<const T2*>(k.r),
+                                     [&](int g, T a, T b) {
+      T2 o;
+      o.x = a;
+      o.y = b;
+      reinterpret_cast<T2*>(k.s)[g] = o;
+      sa += static_cast<double>(a) * static_cast<double>(a);
+      sb += static_cast<double>(b) * static_cast<double>(b);
+    });
+  }
+  double ta, tb;
+  if (!two_sums(sa, sb, k.part, k.ticket, ta, tb) || threadIdx.x != 0) return;
+  bool any = false;
+  for (int s = 0; s < 2; ++s) {
+    const double tot = s ? tb : ta;
+    double* sc = k.sc + 5 * s;
+    int* st = k.st + 5 * s;
+    if (init) {
+      sc[0] = tot;
+      sc[3] = k.tol * sqrt(tot);
+      st[1] = 0;
+      if (!(sqrt(tot) > sc[3])) st[0] = 1;
+    } else if (cg_on(k.st, s)) {
+      if (!isfinite(tot)) {
+        st[3] = it + 1;
+        st[0] = 1;
+      } else {
+        sc[2] = tot / sc[0];
+        sc[0] = tot;
+        st[1] = it + 1;
+        k.hist[s * k.hstride + it] = sqrt(sc[4]);
+        if (!(sqrt(tot) > sc[3])) st[0] = 1;
+      }
+    }
+    any = any || cg_on(k.st, s);
+  }
+  if (!init) {
+    const int nit = it + 1;
+    const bool more = any && nit < k.max_iters;
+    k.loop[0] = nit;
+    k.loop[1] = more ? 0 : 1;
+    cudaGraphSetConditional(k.cond, more ? 1u : 0u);
+  }
+}
+
+// d = s + beta d (d = s before the loop)
+template <class T>
+__global__ void cgp_dupdate_kernel(CgPairK<T> k, int init) {
+  if (!init && *(volatile const int*)(k.loop + 1)) return;
+  const bool on[2] = {init || cg_on(k.st, 0), init || cg_on(k.st, 1)};
+  const T be[2] = {static_cast<T>(k.sc[2]), static_cast<T>(k.sc[5 + 2])};
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 2 * k.cols;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int s = static_cast<int>(j & 1);
+    if (on[s]) k.d[j] = init ? k.s[j] : k.s[j] + be[s] * k.d[j];
+  }
+}
+
+// rhs of system s into slot s of the interleaved r
+__global__ void cgp_rhs_kernel(const double* p, long long n, int slot, float* r) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    r[2 * i + slot] = static_cast<float>(p[i]);
+  }
+}
+__global__ void cgp_rhs_kernel(const double* p, long long n, int slot, double* r) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    r[2 * i + slot] = p[i];
+  }
+}
+
+template <class T>
+__global__ void cgp_out_kernel(const T* x, long long n, double* f0, double* f1) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    f0[j] = static_cast<double>(x[2 * j]);
+    f1[j] = static_cast<double>(x[2 * j + 1]);
+  }
+}
+
+constexpr int kCgPassesPerBody = 4;  // passes unrolled per WHILE-body execution
+
+template <class T>
+void run_cgls_pair(Plan& P, const double* p[2], const ss_solve_options& o, double* f[2],
+                   ss_solve_report rep[2], std::string errs[2], int codes[2]) {
+  Context* ctx = P.ctx;
+  const long long rows = P.rows[0], cols = P.cols[0];
+  DBuf<T> x(2 * cols), r(2 * rows), sv(2 * cols), d(2 * cols), q(2 * rows);
+  const int gv = grid1(ctx, 2 * std::max(rows, cols));
+  const int grid = std::max({P.fwd_blocks, P.back_blocks, gv});
+  DBuf<double> part(2 * static_cast<std::size_t>(grid)), sc(10), hist(2 * (o.max_iters + 1));
+  DBuf<int> st(10), loop(2);
+  DBuf<unsigned> ticket(1);
+  CgPairK<T> k{};
+  k.sk = make_args<T>(P);
+  k.x = x.get();
+  k.r = r.get();
+  k.s = sv.get();
+  k.d = d.get();
+  k.q = q.get();
+  k.rows = rows;
+  k.cols = cols;
+  k.part = part.get();
+  k.sc = sc.get();
+  k.st = st.get();
+  k.loop = loop.get();
+  k.ticket = ticket.get();
+  k.hist = hist.get();
+  k.hstride = o.max_iters + 1;
+  k.tol = o.tol;
+  k.max_iters = o.max_iters;
+  // kernels of this plan's layout
+  void (*fwd)(CgPairK<T>) = nullptr;
+  void (*back)(CgPairK<T>, int) = nullptr;
+  const int vsf = P.vs_fwd, vsb = P.vs_back;
+#define SSB_CGF(V, M) if (vsf == V && (P.c16f ? 2 : 1) == M) fwd = cgp_fwd_kernel<T, V, 4, M>;
+#define SSB_CGB(V, M) if (vsb == V && (P.c16b ? 2 : 1) == M) back = cgp_back_kernel<T, V, 2, M>;
+  SSB_CGF(4, 1) SSB_CGF(8, 1) SSB_CGF(16, 1) SSB_CGF(32, 1)
+  SSB_CGF(4, 2) SSB_CGF(8, 2) SSB_CGF(16, 2) SSB_CGF(32, 2)
+  SSB_CGB(4, 1) SSB_CGB(8, 1) SSB_CGB(16, 1) SSB_CGB(32, 1)
+  SSB_CGB(4, 2) SSB_CGB(8, 2) SSB_CGB(16, 2) SSB_CGB(32, 2)
+#undef SSB_CGF
+#undef SSB_CGB
+  if (!fwd || !back) fail("cgls: unsupported paired kernel shape");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  SSB_CUDA(cudaGraphCreate(&g, 0));
+  cudaStreamCaptureStatus cs;
+  try {
+    SSB_CUDA(cudaGraphConditionalHandleCreate(&k.cond, g, 1, cudaGraphCondAssignDefault));
+    SSB_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, g, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    SSB_CUDA(cudaMemsetAsync(x.get(), 0, 2 * cols * sizeof(T), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(st.get(), 0, 10 * sizeof(int), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(loop.get(), 0, 2 * sizeof(int), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
+    for (int s = 0; s < 2; ++s) {
+      cgp_rhs_kernel<<<grid1(ctx, rows), 256, 0, ctx->stream>>>(p[s], rows, s, r.get());
+    }
+    back<<<P.back_blocks, kThreads, 0, ctx->stream>>>(k, 1);
+    cgp_dupdate_kernel<T><<<gv, 256, 0, ctx->stream>>>(k, 1);
+    const cudaGraphNode_t* deps = nullptr;
+    std::size_t nd = 0;
+    SSB_CUDA(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, nullptr, &deps, &nd));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = k.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    SSB_CUDA(cudaGraphAddNode(&cnode, g, deps, nd, &cp));
+    SSB_CUDA(cudaStreamUpdateCaptureDependencies(ctx->stream, &cnode, 1,
+                                                 cudaStreamSetCaptureDependencies));
+    SSB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SSB_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    for (int pass = 0; pass < std::min(o.max_iters, kCgPassesPerBody); ++pass) {
+      fwd<<<P.fwd_blocks, kThreads, 0, ctx->stream>>>(k);
+      cgp_axpy_kernel<T><<<gv, kThreads, 0, ctx->stream>>>(k);
+      back<<<P.back_blocks, kThreads, 0, ctx->stream>>>(k, 0);
+      cgp_dupdate_kernel<T><<<gv, 256, 0, ctx->stream>>>(k, 0);
+    }
+    SSB_CUDA(cudaStreamEndCapture(ctx->stream, &body));
+    SSB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  } catch (...) {
+    if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(ctx->stream, &junk);
+      if (junk && junk != g) cudaGraphDestroy(junk);
+    }
+    cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraphDestroy(g);
+  cudaEvent_t e0, e1;
+  SSB_CUDA(cudaEventCreate(&e0));
+  SSB_CUDA(cudaEventCreate(&e1));
+  SSB_CUDA(cudaEventRecord(e0, ctx->stream));
+  SSB_CUDA(cudaGraphLaunch(ge, ctx->stream));
+  SSB_CUDA(cudaEventRecord(e1, ctx->stream));
+  SSB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  SSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaGraphExecDestroy(ge);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  int hs[10];
+  int passes = 0;
+  ctx->copy(hs, st.get(), sizeof hs);
+  ctx->copy(&passes, loop.get(), sizeof(int));
+  ctx->launches += 4 + 4LL * std::max(passes, 1);
+  for (int s = 0; s < 2; ++s) {
+    const int* h = hs + 5 * s;
+    if (h[2]) {
+      errs[s] = "cgls_solve: diverged (non-finite step at iteration " + std::to_string(h[2]) + ")";
+      codes[s] = SS_ERR_DIVERGED;
+    } else if (h[3]) {
+      errs[s] = "cgls_solve: diverged (non-finite residual at iteration " + std::to_string(h[3]) + ")";
+      codes[s] = SS_ERR_DIVERGED;
+    }
+    rep[s].iterations = h[1];
+    rep[s].history_len = h[1];
+    rep[s].wall_time_seconds = ms * 1e-3;
+  }
+  cgp_out_kernel<T><<<grid1(ctx, cols), 256, 0, ctx->stream>>>(x.get(), cols, f[0], f[1]);
+  ctx->check_launch("cgp_out_kernel");
+  ctx->sync();
+}
+
+}  // namespace
+
+// both folded systems' CGLS in one loop over the paired streams
+void cgls_device_paired(Matrix* a1, Matrix* a2, const double* p[2], const ss_solve_options& o,
+                        double* f[2], ss_solve_report rep[2], std::string errs[2], int codes[2]) {
+  if (o.tol <= 0) fail("cgls_solve: tol must be positive");
+  if (o.max_iters < 1) fail("cgls_solve: max_iters must be >= 1");
+  ss_solve_options so = o;
+  so.relaxation = 1.0;  // unused by CGLS; the plan builder validates it
+  so.method = SS_METHOD_SART;
+  so.tol = 0.0;
+  std::unique_ptr<Plan> P(make_plan(a1->ctx, a1, a2, so, 1, false));
+  if (!P->paired || !P->tiled) fail("cgls: paired tiled streams unavailable");
+  if (o.dtype == SS_F32) run_cgls_pair<float>(*P, p, o, f, rep, errs, codes);
+  else run_cgls_pair<double>(*P, p, o, f, rep, errs, codes);
+}
+
 }  // namespace ssb

@@ -65,13 +65,15 @@ def test_cgls_errors():
         P.cgls_solve(a, np.ones(3), P.SolveOptions(method="cgls"))
 
 
-def test_cgls_split_config1_matches_oracle():
+@pytest.mark.parametrize("paired", ["1", "0"])  # one paired loop / two concurrent streams
+def test_cgls_split_config1_matches_oracle(paired, monkeypatch):
     """Unlike SART (a contraction), CG loses orthogonality in finite precision:
     a summation-order difference of 1e-16 grows ~10x per iteration on this
     ill-conditioned underdetermined system (measured: 3e-16 after 3 iterations,
     8e-15 after 5, 1e-10 after 10, 4e-6 after 20). So f is compared where CG is
     stable (5 iterations, 1e-12) and, after 30 iterations, the residual norm —
     the quantity CGLS minimises — to 1e-4 relative (measured 2.9e-5)."""
+    monkeypatch.setenv("SSB_CGLS_PAIRED", paired)
     w, cfg, a, csr, f_true, p = oracle_workload(1)
     s = P.build_system(w.scan_config())
     for iters, f_tol in ((5, 1e-12), (30, None)):
@@ -89,3 +91,24 @@ def test_cgls_split_config1_matches_oracle():
     direct = P.solve_direct(P.CentroSystem(s.a, p, 0.0),
                             P.SolveOptions(method="cgls", max_iters=30, tol=1e-10))
     assert direct.iterations == 30 and len(direct.residual_history) == 30
+
+
+@pytest.mark.parametrize("paired", ["1", "0"])
+def test_cgls_split_stops_independently_per_branch(paired, monkeypatch):
+    """The two folded systems stop at their own iterations (the reference runs
+    them as independent solves): compare each branch with the oracle's CGLS."""
+    monkeypatch.setenv("SSB_CGLS_PAIRED", paired)
+    rng = np.random.default_rng(41)
+    h1 = 3 * np.eye(40, 30) + rng.uniform(0, 0.1, (40, 30))
+    h2 = rng.uniform(0.1, 1.0, (40, 30))
+    a = O.reconstruct_matrix(O.Matrix.dense(h1), O.Matrix.dense(h2)).to_dense()
+    p = a @ rng.uniform(0.5, 1.5, 60)
+    sys_ = P.CentroSystem(P.Matrix.dense(a), p, 0.0)
+    split = P.split_system(sys_)
+    got = P.solve_split(sys_, P.SolveOptions(method="cgls", max_iters=500, tol=1e-9))
+    o1 = O.cgls_solve(O.Matrix.dense(h1), split.p1, max_iters=500, tol=1e-9)
+    o2 = O.cgls_solve(O.Matrix.dense(h2), split.p2, max_iters=500, tol=1e-9)
+    assert o1.iterations != o2.iterations
+    assert got.iterations == max(o1.iterations, o2.iterations)
+    want = O.recombine_solution(o1.f, o2.f)
+    assert rel_err(got.f, want) <= 1e-8
