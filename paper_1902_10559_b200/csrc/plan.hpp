@@ -12,7 +12,6 @@ struct Plan {
   int nrhs = 1;
   int dtype = SS_F64;
   int vs_fwd = 32, vs_back = 8;
-  bool noalloc = false;  // matrix loads with L1::no_allocate
   int uf_fwd = 2, uf_back = 2;  // load steps in flight per lane before the gathers
   int fwd_blocks = 0, back_blocks = 0;
   bool sharded = false;

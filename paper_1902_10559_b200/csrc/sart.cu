@@ -142,36 +142,13 @@ __device__ __forceinline__ float upd(float x, double relax, float u, float ci) {
   return __fadd_rn(x, __fmul_rn(static_cast<float>(relax), __fmul_rn(u, ci)));
 }
 
-// Streaming loads that bypass L1 allocation: the matrix is touched once per
-// kernel, so L1 capacity is left to the gathered dense vector.
-__device__ __forceinline__ int4 ld_stream(const int4* p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void ld_stream4(const float* p, float (&v)[4]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-               : "l"(p));
-}
-__device__ __forceinline__ void ld_stream4(const double* p, double (&v)[4]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-               : "=d"(v[0]), "=d"(v[1])
-               : "l"(p));
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-               : "=d"(v[2]), "=d"(v[3])
-               : "l"(p + 2));
-}
-
 // Dot product of one compressed vector [beg,end) with a gathered dense
 // vector by VS cooperating lanes. The scalar head (up to the 16-byte
 // boundary) and tail are loaded first; the 4-wide body issues UF steps of
 // (int4 indices + 4 values) per lane before any dependent gather, so
 // UF*VS*32 bytes of matrix stream are in flight per group; then a VS-lane
 // butterfly.
-template <class T, int VS, int UF, bool NA = false>
+template <class T, int VS, int UF>
 __device__ __forceinline__ T seg_dot(const int* __restrict__ idx, const T* __restrict__ val,
                                      const T* __restrict__ vec, int beg, int end, int lane,
                                      unsigned mask) {
@@ -198,13 +175,8 @@ __device__ __forceinline__ T seg_dot(const int* __restrict__ idx, const T* __res
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
       const int k0 = a + ((q + u * VS) << 2);
-      if (NA) {
-        c[u] = ld_stream(reinterpret_cast<const int4*>(idx + k0));
-        ld_stream4(val + k0, v[u]);
-      } else {
-        c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
-        load4(val + k0, v[u]);
-      }
+      c[u] = __ldg(reinterpret_cast<const int4*>(idx + k0));
+      load4(val + k0, v[u]);
     }
     T g[UF][4];
 #pragma unroll
@@ -315,7 +287,7 @@ __device__ __forceinline__ void fetch_vec(const SartK<T>& k, int i, int lane, Ve
   }
 }
 
-template <class T, int VS, int UF, bool NA, int SYS>
+template <class T, int VS, int UF, int SYS>
 __device__ __forceinline__ double fwd_rows(const SartK<T>& k, long long group, long long ngroups,
                                            int lane, unsigned mask) {
   const SysK<T>& S = k.s[SYS];
@@ -325,7 +297,7 @@ __device__ __forceinline__ double fwd_rows(const SartK<T>& k, long long group, l
   if (group < n) fetch_vec<T, true, SYS>(k, static_cast<int>(group), lane, cur);
   for (long long g = group; g < n; g += ngroups) {
     if (g + ngroups < n) fetch_vec<T, true, SYS>(k, static_cast<int>(g + ngroups), lane, nxt);
-    const T dot = seg_dot<T, VS, UF, NA>(S.ci, S.rv, S.x, cur.beg, cur.end, lane, mask);
+    const T dot = seg_dot<T, VS, UF>(S.ci, S.rv, S.x, cur.beg, cur.end, lane, mask);
     if (lane == 0) {
       const T r = cur.e1 - dot;
       S.w[cur.i] = cur.e2 * r;
@@ -336,7 +308,7 @@ __device__ __forceinline__ double fwd_rows(const SartK<T>& k, long long group, l
   return acc;
 }
 
-template <class T, int VS, int UF, bool NA, int SYS>
+template <class T, int VS, int UF, int SYS>
 __device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, long long ngroups,
                                           int lane, unsigned mask, int it) {
   const SysK<T>& S = k.s[SYS];
@@ -345,7 +317,7 @@ __device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, lo
   if (group < n) fetch_vec<T, false, SYS>(k, static_cast<int>(group), lane, cur);
   for (long long g = group; g < n; g += ngroups) {
     if (g + ngroups < n) fetch_vec<T, false, SYS>(k, static_cast<int>(g + ngroups), lane, nxt);
-    const T u = seg_dot<T, VS, UF, NA>(S.ri, S.cv, S.w, cur.beg, cur.end, lane, mask);
+    const T u = seg_dot<T, VS, UF>(S.ri, S.cv, S.w, cur.beg, cur.end, lane, mask);
     if (lane == 0) {
       if (k.bp_out) {
         k.bp_out[cur.i] = u;
@@ -359,7 +331,7 @@ __device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, lo
   }
 }
 
-template <class T, int VS, int UF, bool NA>
+template <class T, int VS, int UF>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, true);
   if (loop_over(k)) return;
@@ -374,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(Sa
   const long long ngroups = (long long)nb * kThreads / VS;
   double acc = 0.0;
   if (sys_on(k.state, sys)) {
-    acc = sys ? fwd_rows<T, VS, UF, NA, 1>(k, group, ngroups, lane, mask)
-              : fwd_rows<T, VS, UF, NA, 0>(k, group, ngroups, lane, mask);
+    acc = sys ? fwd_rows<T, VS, UF, 1>(k, group, ngroups, lane, mask)
+              : fwd_rows<T, VS, UF, 0>(k, group, ngroups, lane, mask);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -398,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(Sa
   }
 }
 
-template <class T, int VS, int UF, bool NA>
+template <class T, int VS, int UF>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, false);
   if (loop_over(k)) return;
@@ -411,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(S
   const long long group = (bx * (long long)kThreads + threadIdx.x) / VS;
   const long long ngroups = (long long)nb * kThreads / VS;
   if (!sys_on(k.state, sys)) return;
-  if (sys) back_cols<T, VS, UF, NA, 1>(k, group, ngroups, lane, mask, it);
-  else back_cols<T, VS, UF, NA, 0>(k, group, ngroups, lane, mask, it);
+  if (sys) back_cols<T, VS, UF, 1>(k, group, ngroups, lane, mask, it);
+  else back_cols<T, VS, UF, 0>(k, group, ngroups, lane, mask, it);
 }
 
 // ------------------------------------------------------------ paired kernels
@@ -1429,14 +1401,12 @@ SartK<T> make_args(Plan& P) {
 
 template <class T, int VS>
 void launch_fwd1(Plan& P, const SartK<T>& k, int it) {
-  auto* fn = P.uf_fwd >= 4 ? (P.noalloc ? sart_fwd_kernel<T, VS, 4, true> : sart_fwd_kernel<T, VS, 4, false>)
-                           : (P.noalloc ? sart_fwd_kernel<T, VS, 2, true> : sart_fwd_kernel<T, VS, 2, false>);
+  auto* fn = P.uf_fwd >= 4 ? sart_fwd_kernel<T, VS, 4> : sart_fwd_kernel<T, VS, 2>;
   fn<<<P.fwd_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
 }
 template <class T, int VS>
 void launch_back1(Plan& P, const SartK<T>& k, int it) {
-  auto* fn = P.uf_back >= 4 ? (P.noalloc ? sart_back_kernel<T, VS, 4, true> : sart_back_kernel<T, VS, 4, false>)
-                            : (P.noalloc ? sart_back_kernel<T, VS, 2, true> : sart_back_kernel<T, VS, 2, false>);
+  auto* fn = P.uf_back >= 4 ? sart_back_kernel<T, VS, 4> : sart_back_kernel<T, VS, 2>;
   fn<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
 }
 
@@ -1580,9 +1550,9 @@ int occupancy_blocks(Plan& P, bool fwd) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, multi_kernel<T>(P, fwd), kThreads,
                                                       sh);
   } else {
-    e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_fwd_kernel<T, 32, 4, false>,
+    e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_fwd_kernel<T, 32, 4>,
                                                             kThreads, 0)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_back_kernel<T, 8, 4, false>,
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_back_kernel<T, 8, 4>,
                                                             kThreads, 0);
   }
   SSB_CUDA(e);
@@ -2347,7 +2317,6 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->uf_fwd = env_int("SSB_UF_FWD", 4);
     P->uf_back = env_int("SSB_UF_BACK", 4);
   }
-  P->noalloc = env_int("SSB_NOALLOC", 0) != 0;
   if (o.dtype == SS_F32) {
     P->fwd_blocks = occupancy_blocks<float>(*P, true);
     P->back_blocks = occupancy_blocks<float>(*P, false);
