@@ -43,7 +43,10 @@ struct Plan {
   DBuf<unsigned short> tofs_f, tofs_b;
   DBuf<int> tbase_f, tbase_b, tfirst_f, tfirst_b;  // per tile base, per vector first tile
   std::int64_t ntile_f = 0, ntile_b = 0;
-  int layout_mode(bool fwd) const { return !tiled ? 0 : ((fwd ? c16f : c16b) ? 2 : 1); }
+  bool stream_cs = false;  // evict-first hint on the stream loads (fp32, stream > L2)
+  int layout_mode(bool fwd) const {
+    return !tiled ? 0 : ((fwd ? c16f : c16b) ? (stream_cs ? 3 : 2) : 1);
+  }
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;

@@ -399,16 +399,30 @@ template <> struct Vec2<double> { using type = double2; };
 
 // 4 consecutive entries of the interleaved value stream: v[2q] (system 0),
 // v[2q+1] (system 1).
+// Matrix-stream loads: read-only path, or (CS) the evict-first streaming
+// hint (ld.global.cs) so a stream larger than L2 does not displace the
+// gathered x / w. Plans enable it for fp32 streams of 1-16x the L2 (+2.5% on
+// config 3; it costs 3.5% on fp64, 13% on the L2-resident config 2 and 2.6%
+// on config 5's 11.6 GB stream). The remainder loop keeps the read-only
+// path for its offsets (measured faster).
+template <bool CS, class V>
+__device__ __forceinline__ V lds(const V* p) {
+  if constexpr (CS) return __ldcs(p);
+  else return __ldg(p);
+}
+
+template <bool CS = false>
 __device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  const float4 a = lds<CS>(reinterpret_cast<const float4*>(p));
+  const float4 b = lds<CS>(reinterpret_cast<const float4*>(p) + 1);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
+template <bool CS = false>
 __device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p) + h);
+    const double2 a = lds<CS>(reinterpret_cast<const double2*>(p) + h);
     v[2 * h] = a.x;
     v[2 * h + 1] = a.y;
   }
@@ -543,7 +557,7 @@ __device__ __forceinline__ int4 decode16(uint2 o, int b) {
                    b + static_cast<int>(o.y & 0xffffu), b + static_cast<int>(o.y >> 16));
 }
 
-template <class T, int VS, int UF>
+template <class T, int VS, int UF, bool CS = false>
 __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off,
                                           const int* __restrict__ tbase, int tf,
                                           const T* __restrict__ v2,
@@ -561,9 +575,9 @@ __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
       const int k0 = beg + ((q + u * VS) << 2);
-      o[u] = __ldg(reinterpret_cast<const uint2*>(off + k0));
+      o[u] = lds<CS>(reinterpret_cast<const uint2*>(off + k0));
       b[u] = __ldg(tbase + t0 + u);
-      load8(v2 + 2 * k0, v[u]);
+      load8<CS>(v2 + 2 * k0, v[u]);
     }
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
@@ -579,7 +593,7 @@ __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off
     const int4 c = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)),
                             __ldg(tbase + tf + (q - lane) / VS));
     T v[8];
-    load8(v2 + 2 * k0, v);
+    load8<CS>(v2 + 2 * k0, v);
     const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
              g3 = __ldg(xv + c.w);
     sa += v[0] * g0.x + v[2] * g1.x + v[4] * g2.x + v[6] * g3.x;
@@ -616,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
     if (g < gend) {
       beg = __ldg(ptr + g);
       end = __ldg(ptr + g + 1);
-      if (TL == 2) tf = __ldg(k.tff + g);
+      if (TL >= 2) tf = __ldg(k.tff + g);
     }
     for (; g < gend; g += gstep) {
       const int gn = g + gstep;
@@ -624,14 +638,14 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
       if (gn < gend) {  // next row's bounds, ahead of this row's dot product
         nbeg = __ldg(ptr + gn);
         nend = __ldg(ptr + gn + 1);
-        if (TL == 2) ntf = __ldg(k.tff + gn);
+        if (TL >= 2) ntf = __ldg(k.tff + gn);
       }
       T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      if (TL == 2) {
-        seg_dot2c<T, VS, UF>(k.tof, k.tbf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end,
-                             lane, mask, da, db);
+      if (TL >= 2) {
+        seg_dot2c<T, VS, UF, TL == 3>(k.tof, k.tbf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx),
+                                      beg, end, lane, mask, da, db);
       } else if (TL == 1) {
         seg_dot2t<T, VS, UF>(k.tif, k.rv2, reinterpret_cast<const T2*>(k.xx), beg, end, lane,
                              mask, da, db);
@@ -696,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   if (g < gend) {
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
-    if (TL == 2) tf = __ldg(k.tfb + g);
+    if (TL >= 2) tf = __ldg(k.tfb + g);
   }
   for (; g < gend; g += gstep) {
     const int gn = g + gstep;
@@ -704,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     if (gn < gend) {
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
-      if (TL == 2) ntf = __ldg(k.tfb + gn);
+      if (TL >= 2) ntf = __ldg(k.tfb + gn);
     }
     T2 xo, ci;
     xo.x = xo.y = ci.x = ci.y = T(0);
@@ -713,9 +727,9 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
     }
     T ua, ub;
-    if (TL == 2) {
-      seg_dot2c<T, VS, UF>(k.tob, k.tbb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end,
-                           lane, mask, ua, ub);
+    if (TL >= 2) {
+      seg_dot2c<T, VS, UF, TL == 3>(k.tob, k.tbb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww),
+                                    beg, end, lane, mask, ua, ub);
     } else if (TL == 1) {
       seg_dot2t<T, VS, UF>(k.tib, k.cv2, reinterpret_cast<const T2*>(k.ww), beg, end, lane, mask,
                            ua, ub);
@@ -1423,6 +1437,8 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
 #define SSB_PAIR(V, U)                                                                        \
   if (vs == V && uf == U) {                                                                   \
     if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
+    if ((fwd ? P.c16f : P.c16b) && P.stream_cs)                                              \
+      return fwd ? sart_fwd_pair_kernel<T, V, U, 3> : sart_back_pair_kernel<T, V, U, 3>;      \
     if (fwd ? P.c16f : P.c16b)                                                                \
       return fwd ? sart_fwd_pair_kernel<T, V, U, 2> : sart_back_pair_kernel<T, V, U, 2>;      \
     return fwd ? sart_fwd_pair_kernel<T, V, U, 1> : sart_back_pair_kernel<T, V, U, 1>;        \
@@ -2362,6 +2378,13 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   if (P->paired) {
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);
+    // fp32 streams of 1-16x the L2 carry the evict-first hint (see lds):
+    // measured +2.5% at 5.3x (config 3), -2.6% at 92x (config 5)
+    std::int64_t fb = 0, bb = 0;
+    P->kernel_bytes(&fb, &bb);
+    const std::size_t sb = static_cast<std::size_t>(fb + bb);
+    P->stream_cs = o.dtype == SS_F32 && env_int("SSB_STREAM_CS", 1) != 0 &&
+                   sb > ctx->l2_bytes && sb <= 16 * ctx->l2_bytes;
     tr.mark("paired streams");
   } else if (P->nsys == 1 && nrhs == 1) {
     P->tiled = env_int("SSB_TILED", 1) != 0;
