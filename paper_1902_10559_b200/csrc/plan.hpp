@@ -44,6 +44,7 @@ struct Plan {
   DBuf<int> tbase_f, tbase_b, tfirst_f, tfirst_b;  // per tile base, per vector first tile
   std::int64_t ntile_f = 0, ntile_b = 0;
   bool stream_cs = false;  // evict-first hint on the stream loads (fp32, stream > L2)
+  bool l2_window = false;  // persisting L2 access-policy window on the gathered vector
   int layout_mode(bool fwd) const {
     return !tiled ? 0 : ((fwd ? c16f : c16b) ? (stream_cs ? 3 : 2) : 1);
   }

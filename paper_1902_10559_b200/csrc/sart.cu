@@ -1476,17 +1476,30 @@ bool single_tiled(const Plan& P) { return !P.paired && P.tiled && P.nrhs == 1 &&
 // (the first statement of every kernel launched this way) for its results.
 template <class T>
 void launch_pdl(PairFn<T> fn, int grid, int block, std::size_t smem, cudaStream_t st,
-                const SartK<T>& k, int it) {
+                const SartK<T>& k, int it, const void* hot = nullptr, std::size_t hot_bytes = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (hot && hot_bytes) {  // keep the gathered vector L2-resident (persisting window)
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(hot);
+    attr[na].val.accessPolicyWindow.num_bytes = hot_bytes;
+    attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   SSB_CUDA(cudaLaunchKernelEx(&cfg, fn, k, it));
 }
 
@@ -1494,7 +1507,14 @@ template <class T>
 void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
   int smem = 0;
   const PairFn<T> fn = pair_kernel<T>(P, fwd, &smem);
-  launch_pdl<T>(fn, fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream, k, it);
+  const void* hot = nullptr;
+  std::size_t hb = 0;
+  if (P.l2_window) {
+    hot = fwd ? P.xx.get() : P.ww.get();
+    hb = 2 * (fwd ? P.cols[0] : P.rows[0]) * sizeof(T);
+  }
+  launch_pdl<T>(fn, fwd ? P.fwd_blocks : P.back_blocks, kThreads, smem, P.ctx->stream, k, it,
+                hot, hb);
 }
 
 // multi-RHS kernel: V consecutive slices per lane (vector loads; S % V == 0),
@@ -2385,6 +2405,11 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     const std::size_t sb = static_cast<std::size_t>(fb + bb);
     P->stream_cs = o.dtype == SS_F32 && env_int("SSB_STREAM_CS", 1) != 0 &&
                    sb > ctx->l2_bytes && sb <= 16 * ctx->l2_bytes;
+    P->l2_window = env_int("SSB_L2WIN", 0) != 0;
+    if (P->l2_window) {
+      SSB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                  static_cast<std::size_t>(env_int("SSB_L2WIN_MB", 16)) << 20));
+    }
     tr.mark("paired streams");
   } else if (P->nsys == 1 && nrhs == 1) {
     P->tiled = env_int("SSB_TILED", 1) != 0;
