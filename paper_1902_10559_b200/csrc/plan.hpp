@@ -43,10 +43,21 @@ struct Plan {
   DBuf<unsigned short> tofs_f, tofs_b;
   DBuf<int> tbase_f, tbase_b, tfirst_f, tfirst_b;  // per tile base, per vector first tile
   std::int64_t ntile_f = 0, ntile_b = 0;
+  // tiled + 16-bit + mirror-coded pair values (see seg_dot2m): per tile header
+  // {base, sign words} (hs words), one value per entry, exception lists
+  bool mir_f = false, mir_b = false;
+  int hs_f = 0, hs_b = 0;
+  DBuf<unsigned> thdr_f, thdr_b;
+  DBuf<int> eptr_f, eptr_b, eidx_f, eidx_b;
+  DBuf<char> ev2_f, ev2_b;
+  std::int64_t nexc_f = 0, nexc_b = 0;
   bool stream_cs = false;  // evict-first hint on the stream loads (fp32, stream > L2)
   bool l2_window = false;  // persisting L2 access-policy window on the gathered vector
   int layout_mode(bool fwd) const {
-    return !tiled ? 0 : ((fwd ? c16f : c16b) ? (stream_cs ? 3 : 2) : 1);
+    if (!tiled) return 0;
+    if (!(fwd ? c16f : c16b)) return 1;
+    if (fwd ? mir_f : mir_b) return stream_cs ? 5 : 4;
+    return stream_cs ? 3 : 2;
   }
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;

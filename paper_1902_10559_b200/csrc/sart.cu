@@ -81,6 +81,17 @@ struct SartK {
   const unsigned short* tob;    //               u16 tiled (K2)
   const int* tbb;
   const int* tfb;
+  // mirror-coded pair streams (TL 4/5, see seg_dot2m): per tile {int32 base,
+  // sign words}; rv2 / cv2 then hold one value per entry. Buckets whose two
+  // values are not +-equal live in a per-vector exception list.
+  const unsigned* thf;
+  const unsigned* thb;
+  const int* epf;  // exceptions, K1: per row pointer, column, {a1, a2}
+  const int* eif;
+  const T* evf;
+  const int* epb;  // exceptions, K2: per column pointer, row, {a1, a2}
+  const int* eib;
+  const T* evb;
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
   // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
   T* bp_out;
@@ -608,6 +619,118 @@ __device__ __forceinline__ void seg_dot2c(const unsigned short* __restrict__ off
   acc_b = sb;
 }
 
+// Mirror-coded pair stream. Every bucket of the fold holds a1 = +-a2 unless
+// its row meets both a voxel and that voxel's point mirror (the 4-term
+// buckets of split_matrix, centro.cpp:103-130): TL only gives a1 = a2 = TL,
+// TR only gives a1 = -TR, a2 = TR. So the stream stores a2 once per entry plus
+// one sign bit for a1 -- exact in any precision, since negation is -- and the
+// few remaining buckets move to a per-vector exception list {index, a1, a2}
+// (their slot in the stream holds 0). fp32: 6 instead of 10 bytes per entry.
+// The sign bits of a tile sit in its header next to the base: lane l's four
+// entries are bits 4l..4l+3 (header = uint2 {base, bits} for VS <= 8, uint4
+// {base, bits 0-31, bits 32-63, -} for VS = 16, 8 words for VS = 32).
+template <int VS>
+__device__ __forceinline__ void load_hdr(const unsigned* __restrict__ h, int t, int lane,
+                                         int& base, unsigned& nib) {
+  if constexpr (VS <= 8) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(h) + t);
+    base = static_cast<int>(w.x);
+    nib = w.y >> (4 * lane);
+  } else if constexpr (VS == 16) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(h) + t);
+    base = static_cast<int>(w.x);
+    nib = (lane < 8 ? w.y : w.z) >> (4 * (lane & 7));
+  } else {
+    base = static_cast<int>(__ldg(h + 8 * t));
+    nib = __ldg(h + 8 * t + 1 + (lane >> 3)) >> (4 * (lane & 7));
+  }
+}
+
+__device__ __forceinline__ float flip(float v, unsigned nib, int j) {
+  return __int_as_float(__float_as_int(v) ^ static_cast<int>((nib << (31 - j)) & 0x80000000u));
+}
+__device__ __forceinline__ double flip(double v, unsigned nib, int j) {
+  return __hiloint2double(__double2hiint(v) ^ static_cast<int>((nib << (31 - j)) & 0x80000000u),
+                          __double2loint(v));
+}
+
+template <bool CS>
+__device__ __forceinline__ void load4s(const float* p, float (&v)[4]) {
+  const float4 t = lds<CS>(reinterpret_cast<const float4*>(p));
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+template <bool CS>
+__device__ __forceinline__ void load4s(const double* p, double (&v)[4]) {
+  const double2 a = lds<CS>(reinterpret_cast<const double2*>(p));
+  const double2 b = lds<CS>(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+template <class T, int VS, int UF, bool CS = false>
+__device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off,
+                                          const unsigned* __restrict__ hdr, int tf,
+                                          const T* __restrict__ v1,
+                                          const typename Vec2<T>::type* __restrict__ xv, int beg,
+                                          int end, int eb, int ee, const int* __restrict__ eidx,
+                                          const T* __restrict__ ev2, int lane, unsigned mask,
+                                          T& acc_a, T& acc_b) {
+  using T2 = typename Vec2<T>::type;
+  T sa = T(0), sb = T(0);
+  const int nvec = (end - beg) >> 2;
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    uint2 o[UF];
+    int b[UF];
+    unsigned s[UF];
+    T v[UF][4];
+    const int t0 = tf + (q - lane) / VS;
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = beg + ((q + u * VS) << 2);
+      o[u] = lds<CS>(reinterpret_cast<const uint2*>(off + k0));
+      load_hdr<VS>(hdr, t0 + u, lane, b[u], s[u]);
+      load4s<CS>(v1 + k0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int4 c = decode16(o[u], b[u]);
+      const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
+               g3 = __ldg(xv + c.w);
+      sa += flip(v[u][0], s[u], 0) * g0.x + flip(v[u][1], s[u], 1) * g1.x +
+            flip(v[u][2], s[u], 2) * g2.x + flip(v[u][3], s[u], 3) * g3.x;
+      sb += v[u][0] * g0.y + v[u][1] * g1.y + v[u][2] * g2.y + v[u][3] * g3.y;
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = beg + (q << 2);
+    int b;
+    unsigned s;
+    load_hdr<VS>(hdr, tf + (q - lane) / VS, lane, b, s);
+    const int4 c = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)), b);
+    T v[4];
+    load4s<CS>(v1 + k0, v);
+    const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
+             g3 = __ldg(xv + c.w);
+    sa += flip(v[0], s, 0) * g0.x + flip(v[1], s, 1) * g1.x + flip(v[2], s, 2) * g2.x +
+          flip(v[3], s, 3) * g3.x;
+    sb += v[0] * g0.y + v[1] * g1.y + v[2] * g2.y + v[3] * g3.y;
+  }
+  for (int e = eb + lane; e < ee; e += VS) {  // exception buckets (rare)
+    const int c = __ldg(eidx + e);
+    const T2 a = __ldg(reinterpret_cast<const T2*>(ev2) + e);
+    const T2 g = __ldg(xv + c);
+    sa += a.x * g.x;
+    sb += a.y * g.y;
+  }
+#pragma unroll
+  for (int off2 = VS / 2; off2 > 0; off2 >>= 1) {
+    sa += __shfl_xor_sync(mask, sa, off2, VS);
+    sb += __shfl_xor_sync(mask, sb, off2, VS);
+  }
+  acc_a = sa;
+  acc_b = sb;
+}
+
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
   cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
@@ -626,24 +749,35 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const int gend = n, gstep = static_cast<int>(ngroups);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    int beg = 0, end = 0, tf = 0;
+    int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
     if (g < gend) {
       beg = __ldg(ptr + g);
       end = __ldg(ptr + g + 1);
       if (TL >= 2) tf = __ldg(k.tff + g);
+      if (TL >= 4 && k.epf) {
+        eb = __ldg(k.epf + g);
+        ee = __ldg(k.epf + g + 1);
+      }
     }
     for (; g < gend; g += gstep) {
       const int gn = g + gstep;
-      int nbeg = 0, nend = 0, ntf = 0;
+      int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
       if (gn < gend) {  // next row's bounds, ahead of this row's dot product
         nbeg = __ldg(ptr + gn);
         nend = __ldg(ptr + gn + 1);
         if (TL >= 2) ntf = __ldg(k.tff + gn);
+        if (TL >= 4 && k.epf) {
+          neb = __ldg(k.epf + gn);
+          nee = __ldg(k.epf + gn + 1);
+        }
       }
       T e[4] = {T(0), T(0), T(0), T(0)};  // {p1, p2, rinv1, rinv2}, issued before the dot
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
-      if (TL >= 2) {
+      if (TL >= 4) {
+        seg_dot2m<T, VS, UF, TL == 5>(k.tof, k.thf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx),
+                                      beg, end, eb, ee, k.eif, k.evf, lane, mask, da, db);
+      } else if (TL >= 2) {
         seg_dot2c<T, VS, UF, TL == 3>(k.tof, k.tbf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx),
                                       beg, end, lane, mask, da, db);
       } else if (TL == 1) {
@@ -665,6 +799,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
       beg = nbeg;
       end = nend;
       tf = ntf;
+      eb = neb;
+      ee = nee;
     }
   }
 #pragma unroll
@@ -706,19 +842,27 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const int* __restrict__ ptr = TL != 0 ? k.tpb : k.s[0].cp;
   int g = static_cast<int>(group);
   const int gend = n, gstep = static_cast<int>(ngroups);
-  int beg = 0, end = 0, tf = 0;
+  int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
   if (g < gend) {
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
     if (TL >= 2) tf = __ldg(k.tfb + g);
+    if (TL >= 4 && k.epb) {
+      eb = __ldg(k.epb + g);
+      ee = __ldg(k.epb + g + 1);
+    }
   }
   for (; g < gend; g += gstep) {
     const int gn = g + gstep;
-    int nbeg = 0, nend = 0, ntf = 0;
+    int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
     if (gn < gend) {
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
       if (TL >= 2) ntf = __ldg(k.tfb + gn);
+      if (TL >= 4 && k.epb) {
+        neb = __ldg(k.epb + gn);
+        nee = __ldg(k.epb + gn + 1);
+      }
     }
     T2 xo, ci;
     xo.x = xo.y = ci.x = ci.y = T(0);
@@ -727,7 +871,10 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
     }
     T ua, ub;
-    if (TL >= 2) {
+    if (TL >= 4) {
+      seg_dot2m<T, VS, UF, TL == 5>(k.tob, k.thb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww),
+                                    beg, end, eb, ee, k.eib, k.evb, lane, mask, ua, ub);
+    } else if (TL >= 2) {
       seg_dot2c<T, VS, UF, TL == 3>(k.tob, k.tbb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww),
                                     beg, end, lane, mask, ua, ub);
     } else if (TL == 1) {
@@ -747,6 +894,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     beg = nbeg;
     end = nend;
     tf = ntf;
+    eb = neb;
+    ee = nee;
   }
 }
 
@@ -1018,6 +1167,122 @@ __global__ void tile_stream16_kernel(const int* __restrict__ ptr, const int* __r
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(overflow, 1);
+  }
+}
+
+// Bucket class of the mirror-coded stream in the plan type:
+// 0 a1 == a2, 1 a1 == -a2 (both exact), 2 exception.
+template <class T>
+__device__ __forceinline__ int mirror_class(double a1, double a2) {
+  const T a = static_cast<T>(a1), b = static_cast<T>(a2);
+  if (a == b) return 0;
+  if (a == -b) return 1;
+  return 2;
+}
+
+// Mirror-coded 16-bit tiled stream (see seg_dot2m): the permutation and
+// offsets of tile_stream16_kernel, one value (a2) per entry, and the tile's
+// sign bits (bit w of the tile = padded position w) in its header words
+// 1..; word 0 is the base. thdr must be zeroed (partial tiles, padding).
+template <class T>
+__global__ void tile_mirror_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                   const double* __restrict__ v0, const double* __restrict__ v1,
+                                   long long nvec, const int* __restrict__ tptr,
+                                   const int* __restrict__ tfirst, unsigned short* __restrict__ tofs,
+                                   unsigned* __restrict__ thdr, int hs, T* __restrict__ tv,
+                                   int tile, int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long s = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+       s < nvec; s += nw) {
+    const int beg = ptr[s], len = ptr[s + 1] - beg;
+    const int ob = tptr[s], lp = tptr[s + 1] - ob;
+    const int tf = tfirst[s];
+    for (int t = lane; t * tile < lp; t += 32) {
+      thdr[static_cast<long long>(tf + t) * hs] = static_cast<unsigned>(idx[beg + t * tile]);
+    }
+    bool bad = false;
+    for (int p0 = 0; p0 < lp; p0 += 32) {
+      const int p = p0 + lane;
+      bool neg = false;
+      if (p < lp) {
+        const int t0 = (p / tile) * tile;
+        const int r = min(tile, lp - t0) >> 2;
+        const int w = p - t0;
+        const int o = t0 + (w & 3) * r + (w >> 2);
+        const int base = idx[beg + t0];
+        int c = base;
+        T v = T(0);
+        if (o < len) {
+          c = idx[beg + o];
+          const int cls = mirror_class<T>(v0[beg + o], v1[beg + o]);
+          if (cls < 2) {
+            v = static_cast<T>(v1[beg + o]);
+            neg = cls == 1;
+          }
+        }
+        const unsigned d = static_cast<unsigned>(c - base);
+        bad |= d > 0xffffu;
+        tofs[ob + p] = static_cast<unsigned short>(d);
+        tv[ob + p] = v;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, neg);
+      if (lane == 0) {
+        if (tile >= 32) {
+          thdr[static_cast<long long>(tf + p0 / tile) * hs + 1 + (p0 % tile) / 32] = bal;
+        } else {  // 16-entry tiles: two per ballot
+          for (int h = 0; h < 2; ++h) {
+            const int pp = p0 + 16 * h;
+            if (pp < lp) thdr[static_cast<long long>(tf + pp / 16) * hs + 1] = (bal >> (16 * h)) & 0xffffu;
+          }
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(overflow, 1);
+  }
+}
+
+// exception buckets per vector (counts for the pointer scan; cnt[n] stays 0)
+template <class T>
+__global__ void mirror_exc_count_kernel(const int* __restrict__ ptr, const double* __restrict__ v0,
+                                        const double* __restrict__ v1, long long nvec,
+                                        int* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long s = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+       s < nvec; s += nw) {
+    int n = 0;
+    for (int q = ptr[s] + lane; q < ptr[s + 1]; q += 32) n += mirror_class<T>(v0[q], v1[q]) == 2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) cnt[s] = n;
+  }
+}
+
+// exception lists in stored (sorted) order: index and {a1, a2} in the plan type
+template <class T>
+__global__ void mirror_exc_fill_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                       const double* __restrict__ v0, const double* __restrict__ v1,
+                                       long long nvec, const int* __restrict__ eptr,
+                                       int* __restrict__ eidx, T* __restrict__ ev2) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long s = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+       s < nvec; s += nw) {
+    int at = eptr[s];
+    if (at == eptr[s + 1]) continue;
+    for (int q0 = ptr[s]; q0 < ptr[s + 1]; q0 += 32) {
+      const int q = q0 + lane;
+      const bool ex = q < ptr[s + 1] && mirror_class<T>(v0[q], v1[q]) == 2;
+      const unsigned bal = __ballot_sync(0xffffffffu, ex);
+      if (ex) {
+        const int e = at + __popc(bal & ((1u << lane) - 1u));
+        eidx[e] = idx[q];
+        ev2[2 * static_cast<long long>(e)] = static_cast<T>(v0[q]);
+        ev2[2 * static_cast<long long>(e) + 1] = static_cast<T>(v1[q]);
+      }
+      at += __popc(bal);
+    }
   }
 }
 
@@ -1402,6 +1667,14 @@ SartK<T> make_args(Plan& P) {
   k.tob = P.tofs_b.get();
   k.tbb = P.tbase_b.get();
   k.tfb = P.tfirst_b.get();
+  k.thf = P.thdr_f.get();
+  k.thb = P.thdr_b.get();
+  k.epf = P.eptr_f.get();
+  k.eif = P.eidx_f.get();
+  k.evf = reinterpret_cast<const T*>(P.ev2_f.get());
+  k.epb = P.eptr_b.get();
+  k.eib = P.eidx_b.get();
+  k.evb = reinterpret_cast<const T*>(P.ev2_b.get());
   if (P.sharded) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
@@ -1437,6 +1710,10 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
 #define SSB_PAIR(V, U)                                                                        \
   if (vs == V && uf == U) {                                                                   \
     if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
+    if ((fwd ? P.mir_f : P.mir_b) && P.stream_cs)                                            \
+      return fwd ? sart_fwd_pair_kernel<T, V, U, 5> : sart_back_pair_kernel<T, V, U, 5>;      \
+    if (fwd ? P.mir_f : P.mir_b)                                                              \
+      return fwd ? sart_fwd_pair_kernel<T, V, U, 4> : sart_back_pair_kernel<T, V, U, 4>;      \
     if ((fwd ? P.c16f : P.c16b) && P.stream_cs)                                              \
       return fwd ? sart_fwd_pair_kernel<T, V, U, 3> : sart_back_pair_kernel<T, V, U, 3>;      \
     if (fwd ? P.c16f : P.c16b)                                                                \
@@ -2030,6 +2307,15 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
              : nf * (4 + 2 * b) + 4 * (rows[0] + 1);
     k = c16b ? nb * (2 + 2 * b) + 4 * ntile_b + 8 * (cols[0] + 1)
              : nb * (4 + 2 * b) + 4 * (cols[0] + 1);
+    // mirror-coded: offsets + one value per entry + tile headers + exceptions
+    if (mir_f) {
+      f = nf * (2 + b) + 4 * hs_f * ntile_f + 8 * (rows[0] + 1) +
+          (nexc_f ? nexc_f * (4 + 2 * b) + 4 * (rows[0] + 1) : 0);
+    }
+    if (mir_b) {
+      k = nb * (2 + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
+          (nexc_b ? nexc_b * (4 + 2 * b) + 4 * (cols[0] + 1) : 0);
+    }
   } else if (tiled && nsys == 1 && nrhs == 1) {
     f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
              : tnnz_f * (4 + b) + 4 * (rows[0] + 1);
@@ -2070,12 +2356,15 @@ std::string Plan::describe() const {
                 "\"vs_fwd\": %d, \"uf_fwd\": %d, \"vs_back\": %d, \"uf_back\": %d, "
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
-                "\"back_bytes\": %lld, \"graph\": %s}",
+                "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s}",
                 sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
-                        : (paired ? (tiled ? (c16f || c16b ? "paired-tiled-u16" : "paired-tiled") : "paired")
+                        : (paired ? (tiled ? (mir_f || mir_b ? "paired-tiled-u16-mirror"
+                                                                    : (c16f || c16b ? "paired-tiled-u16" : "paired-tiled"))
+                                         : "paired")
                                   : (tiled ? "single-tiled" : "separate")),
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
+                static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
                 graph ? "true" : "false");
   return buf;
 }
@@ -2177,10 +2466,6 @@ bool build_tiled_streams(Plan& P, int w) {
   P.tnnz_f = tiled_ptr(P, P.a[0]->rowptr.get(), rows, P.tptr_f);
   P.tnnz_b = tiled_ptr(P, P.a[0]->colptr.get(), cols, P.tptr_b);
   const std::size_t tb = sizeof(T);
-  P.rv2.alloc(w * P.tnnz_f * tb);
-  P.cv2.alloc(w * P.tnnz_b * tb);
-  T* rv2 = reinterpret_cast<T*>(P.rv2.get());
-  T* cv2 = reinterpret_cast<T*>(P.cv2.get());
   // straight from the fp64 CSR/CSC values (no fp32 matrix copies)
   const auto vals = [&](int s, bool csr) -> const double* {
     if (s >= w) return nullptr;
@@ -2196,8 +2481,10 @@ bool build_tiled_streams(Plan& P, int w) {
     const int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
     const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
     const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
-    T* v2 = fwd ? rv2 : cv2;
+    DBuf<char>& vbuf = fwd ? P.rv2 : P.cv2;
     bool& u16 = fwd ? P.c16f : P.c16b;
+    bool& mir = fwd ? P.mir_f : P.mir_b;
+    mir = mir && u16 && w == 2;
     if (u16) {
       DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
       DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
@@ -2213,16 +2500,64 @@ bool build_tiled_streams(Plan& P, int w) {
       P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
       ntile = total;
       tofs.alloc(tn);
-      tbase.alloc(ntile);
       SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
-      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-          ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
-          tbase.get(), v2, tile, overflow.get());
-      P.ctx->check_launch("tile_stream16_kernel");
-      int bad = 0;
-      P.ctx->copy(&bad, overflow.get(), sizeof(int));
-      if (!bad) return;
-      u16 = false;
+      if (mir) {
+        DBuf<unsigned>& thdr = fwd ? P.thdr_f : P.thdr_b;
+        int& hs = fwd ? P.hs_f : P.hs_b;
+        hs = tile <= 32 ? 2 : (tile == 64 ? 4 : 8);
+        thdr.alloc(static_cast<std::size_t>(ntile) * hs);
+        SSB_CUDA(cudaMemsetAsync(thdr.get(), 0, static_cast<std::size_t>(ntile) * hs * 4,
+                                 P.ctx->stream));
+        vbuf.alloc(tn * tb);
+        tile_mirror_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(
+            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
+            thdr.get(), hs, reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
+        P.ctx->check_launch("tile_mirror_kernel");
+        int bad = 0;
+        P.ctx->copy(&bad, overflow.get(), sizeof(int));
+        if (!bad) {
+          // exception buckets (a1 != +-a2 in the plan type) per vector
+          DBuf<int>& eptr = fwd ? P.eptr_f : P.eptr_b;
+          std::int64_t& nexc = fwd ? P.nexc_f : P.nexc_b;
+          SSB_CUDA(cudaMemsetAsync(cnt.get(), 0, (n + 1) * sizeof(int), P.ctx->stream));
+          mirror_exc_count_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(ptr, vals(0, fwd),
+                                                                    vals(1, fwd), n, cnt.get());
+          P.ctx->check_launch("mirror_exc_count_kernel");
+          eptr.alloc(n + 1);
+          scan_counts(P.ctx, cnt.get(), eptr.get(), n);
+          int ne = 0;
+          P.ctx->copy(&ne, eptr.get() + n, sizeof(int));
+          nexc = ne;
+          if (ne == 0) {
+            eptr.release();
+            return;
+          }
+          DBuf<int>& eidx = fwd ? P.eidx_f : P.eidx_b;
+          DBuf<char>& ev2 = fwd ? P.ev2_f : P.ev2_b;
+          eidx.alloc(ne);
+          ev2.alloc(2 * static_cast<std::size_t>(ne) * tb);
+          mirror_exc_fill_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(
+              ptr, idx, vals(0, fwd), vals(1, fwd), n, eptr.get(), eidx.get(),
+              reinterpret_cast<T*>(ev2.get()));
+          P.ctx->check_launch("mirror_exc_fill_kernel");
+          return;
+        }
+        // a tile spans >= 65536 indices: the same offsets fail 16 bits below
+        (fwd ? P.thdr_f : P.thdr_b).release();
+        mir = false;
+        u16 = false;
+      } else {
+        tbase.alloc(ntile);
+        vbuf.alloc(w * tn * tb);
+        tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
+            tbase.get(), reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
+        P.ctx->check_launch("tile_stream16_kernel");
+        int bad = 0;
+        P.ctx->copy(&bad, overflow.get(), sizeof(int));
+        if (!bad) return;
+        u16 = false;
+      }
       tofs.release();
       tbase.release();
       tfirst.release();
@@ -2230,8 +2565,10 @@ bool build_tiled_streams(Plan& P, int w) {
     }
     DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
     tidx.alloc(tn);
+    vbuf.alloc(w * tn * tb);
     tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-        ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tidx.get(), v2, tile);
+        ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tidx.get(),
+        reinterpret_cast<T*>(vbuf.get()), tile);
     P.ctx->check_launch("tile_stream_kernel");
   };
   build_dir(true);
@@ -2322,6 +2659,7 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->paired = true;
     P->tiled = env_int("SSB_TILED", 1) != 0;
     P->c16f = P->c16b = env_int("SSB_U16", 1) != 0;
+    P->mir_f = P->mir_b = env_int("SSB_MIRROR", 1) != 0;
     tr.mark("pair pattern");
   }
   for (int s = 0; s < P->nsys; ++s) {
@@ -2603,22 +2941,35 @@ __device__ __forceinline__ void pair_sweep(const SartK<T>& k, long long n,
   const int* __restrict__ tfp = FWD ? k.tff : k.tfb;
   const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
   int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
-  int beg = 0, end = 0, tf = 0;
+  const int* __restrict__ ep = FWD ? k.epf : k.epb;
+  int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
   if (g < n) {
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
-    if (TL == 2) tf = __ldg(tfp + g);
+    if (TL >= 2) tf = __ldg(tfp + g);
+    if (TL == 4 && ep) {
+      eb = __ldg(ep + g);
+      ee = __ldg(ep + g + 1);
+    }
   }
   for (; g < n; g += gstep) {
     const int gn = g + gstep;
-    int nbeg = 0, nend = 0, ntf = 0;
+    int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
     if (gn < n) {
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
-      if (TL == 2) ntf = __ldg(tfp + gn);
+      if (TL >= 2) ntf = __ldg(tfp + gn);
+      if (TL == 4 && ep) {
+        neb = __ldg(ep + gn);
+        nee = __ldg(ep + gn + 1);
+      }
     }
     T a, b;
-    if (TL == 2) {
+    if (TL == 4) {
+      seg_dot2m<T, VS, UF>(FWD ? k.tof : k.tob, FWD ? k.thf : k.thb, tf, FWD ? k.rv2 : k.cv2,
+                           vec, beg, end, eb, ee, FWD ? k.eif : k.eib, FWD ? k.evf : k.evb, lane,
+                           mask, a, b);
+    } else if (TL == 2) {
       seg_dot2c<T, VS, UF>(FWD ? k.tof : k.tob, FWD ? k.tbf : k.tbb, tf, FWD ? k.rv2 : k.cv2,
                            vec, beg, end, lane, mask, a, b);
     } else {
@@ -2629,6 +2980,8 @@ __device__ __forceinline__ void pair_sweep(const SartK<T>& k, long long n,
     beg = nbeg;
     end = nend;
     tf = ntf;
+    eb = neb;
+    ee = nee;
   }
 }
 
@@ -2826,12 +3179,15 @@ void run_cgls_pair(Plan& P, const double* p[2], const ss_solve_options& o, doubl
   void (*fwd)(CgPairK<T>) = nullptr;
   void (*back)(CgPairK<T>, int) = nullptr;
   const int vsf = P.vs_fwd, vsb = P.vs_back;
-#define SSB_CGF(V, M) if (vsf == V && (P.c16f ? 2 : 1) == M) fwd = cgp_fwd_kernel<T, V, 4, M>;
-#define SSB_CGB(V, M) if (vsb == V && (P.c16b ? 2 : 1) == M) back = cgp_back_kernel<T, V, 2, M>;
+  const int mf = P.mir_f ? 4 : (P.c16f ? 2 : 1), mb = P.mir_b ? 4 : (P.c16b ? 2 : 1);
+#define SSB_CGF(V, M) if (vsf == V && mf == M) fwd = cgp_fwd_kernel<T, V, 4, M>;
+#define SSB_CGB(V, M) if (vsb == V && mb == M) back = cgp_back_kernel<T, V, 2, M>;
   SSB_CGF(4, 1) SSB_CGF(8, 1) SSB_CGF(16, 1) SSB_CGF(32, 1)
   SSB_CGF(4, 2) SSB_CGF(8, 2) SSB_CGF(16, 2) SSB_CGF(32, 2)
+  SSB_CGF(4, 4) SSB_CGF(8, 4) SSB_CGF(16, 4) SSB_CGF(32, 4)
   SSB_CGB(4, 1) SSB_CGB(8, 1) SSB_CGB(16, 1) SSB_CGB(32, 1)
   SSB_CGB(4, 2) SSB_CGB(8, 2) SSB_CGB(16, 2) SSB_CGB(32, 2)
+  SSB_CGB(4, 4) SSB_CGB(8, 4) SSB_CGB(16, 4) SSB_CGB(32, 4)
 #undef SSB_CGF
 #undef SSB_CGB
   if (!fwd || !back) fail("cgls: unsupported paired kernel shape");

@@ -367,15 +367,69 @@ def test_paired_tiled_layouts_match_oracle(span, per_row):
     split = P.split_system(sys_)
     plan = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0))
     d = plan.describe()
-    assert d["layout"].startswith("paired-tiled")
-    # K2 (columns list rows < 96) always fits 16 bits; K1 falls back for wide rows
-    assert d["back_kernel"].endswith(", 2>")
-    assert d["fwd_kernel"].endswith(", 2>" if span < 65536 else ", 1>")
+    assert d["layout"] == "paired-tiled-u16-mirror"
+    # K2 (columns list rows < 96) always fits 16 bits (mirror-coded); K1 falls
+    # back to int32 indices with interleaved values for wide rows
+    assert d["back_kernel"].endswith(", 4>")
+    assert d["fwd_kernel"].endswith(", 4>" if span < 65536 else ", 1>")
     got = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
     ref = O.solve_split(O.Matrix.triplets(m, n, r, c, v), p, 0.0, 12, 0.0, 1.0)
     assert rel_err(got.f, ref.f) <= TOL_F64
     got32 = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0, dtype="f32"))
     assert rel_err(got32.f, ref.f) <= TOL_F32
+
+
+def _mirror_rich_centro(seed, mh, nh, per_row, frac):
+    """Centrosymmetric system whose rows also meet the point mirror of a
+    fraction `frac` of their columns with a different value: those buckets fold
+    to a1 != +-a2 (the mirror-coded stream's exception lists)."""
+    rng = np.random.default_rng(seed)
+    m, n = 2 * mh, 2 * nh
+    r, c, v = [], [], []
+    for i in range(mh):
+        lo = int(rng.integers(0, n - 4000))
+        cols = np.unique(rng.integers(lo, lo + 4000, per_row))
+        k = max(1, int(frac * len(cols)))
+        extra = n - 1 - cols[:k]  # mirror columns in the same row
+        cols = np.unique(np.concatenate([cols, extra]))
+        vals = rng.uniform(0.1, 1.0, len(cols))
+        r += [i] * len(cols) + [m - 1 - i] * len(cols)
+        c += list(cols) + list(n - 1 - cols)
+        v += list(vals) + list(vals)
+    p = rng.uniform(0.5, 1.5, m)
+    return m, n, np.array(r), np.array(c), np.array(v), p
+
+
+@pytest.mark.parametrize("frac", [0.05, 0.5])
+def test_mirror_coded_exceptions_match_oracle(frac, monkeypatch):
+    """Mirror-coded pair streams: a1 = +-a2 buckets as one value + sign bit,
+    4-term buckets through the per-vector exception lists (both kernels)."""
+    m, n, r, c, v, p = _mirror_rich_centro(31, 80, 20000, 200, frac)
+    a = P.Matrix.from_triplets(m, n, r, c, v)
+    sys_ = P.CentroSystem(a, p, 0.0)
+    split = P.split_system(sys_)
+    opts = P.SolveOptions(max_iters=15, tol=0.0)
+    d = P.SartPlan(split.a1, split.a2, opts).describe()
+    assert d["layout"] == "paired-tiled-u16-mirror"
+    assert d["exceptions"][0] > 0 and d["exceptions"][1] == d["exceptions"][0]
+    ref = O.solve_split(O.Matrix.triplets(m, n, r, c, v), p, 0.0, 15, 0.0, 1.0)
+    got = P.solve_split(sys_, opts)
+    assert rel_err(got.f, ref.f) <= TOL_F64
+    got32 = P.solve_split(sys_, P.SolveOptions(max_iters=15, tol=0.0, dtype="f32"))
+    assert rel_err(got32.f, ref.f) <= TOL_F32
+    # the interleaved 16-bit stream gives the same iterates up to summation order
+    monkeypatch.setenv("SSB_MIRROR", "0")
+    assert P.SartPlan(split.a1, split.a2, opts).describe()["layout"] == "paired-tiled-u16"
+    plain = P.solve_split(sys_, opts)
+    assert rel_err(got.f, plain.f) <= 1e-12
+    # CGLS over the same mirror-coded streams
+    monkeypatch.setenv("SSB_MIRROR", "1")
+    monkeypatch.setenv("SSB_CGLS_PAIRED", "1")
+    cg = P.solve_split(sys_, P.SolveOptions(method="cgls", max_iters=5, tol=1e-10))
+    want_f, it, res = O.solve_split_method(O.Matrix.triplets(m, n, r, c, v), p, "cgls", 0.0, 5,
+                                           1e-10)
+    assert cg.iterations == it and rel_err(cg.f, want_f) <= 1e-10
+    assert abs(cg.residual_norm - res) <= 1e-10 * res
 
 
 @pytest.mark.parametrize("span,per_row", [(3000, 150), (200000, 8)])
