@@ -1170,6 +1170,23 @@ __global__ void tile_stream16_kernel(const int* __restrict__ ptr, const int* __r
   }
 }
 
+// Does any tile of 4*VS entries span >= 65536 indices? (tiles cover stored
+// entries [t0, t0 + tile) of a vector in sorted order; the 16-bit streams
+// then cannot be built for this direction)
+__global__ void tile_overflow_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                     long long nvec, int tile, int* __restrict__ overflow) {
+  for (long long s = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; s < nvec;
+       s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int beg = ptr[s], len = ptr[s + 1] - beg;
+    bool bad = false;
+    for (int t0 = 0; t0 < len && !bad; t0 += tile) {
+      const int last = min(t0 + tile, len) - 1;
+      bad = static_cast<unsigned>(idx[beg + last] - idx[beg + t0]) > 0xffffu;
+    }
+    if (bad) atomicOr(overflow, 1);
+  }
+}
+
 // Bucket class of the mirror-coded stream in the plan type:
 // 0 a1 == a2, 1 a1 == -a2 (both exact), 2 exception.
 template <class T>
@@ -1608,6 +1625,12 @@ bool pdl_enabled() {
 int pick_vs(double avg) {
   if (avg >= 384) return 16;
   if (avg >= 160) return 8;
+  return 4;
+}
+
+int pick_vs_mirror(double avg) {
+  if (avg >= 1024) return 16;
+  if (avg >= 96) return 8;
   return 4;
 }
 
@@ -2485,6 +2508,15 @@ bool build_tiled_streams(Plan& P, int w) {
     bool& u16 = fwd ? P.c16f : P.c16b;
     bool& mir = fwd ? P.mir_f : P.mir_b;
     mir = mir && u16 && w == 2;
+    if (u16) {  // 16 bits fit every tile? (decided before any stream buffer exists)
+      DBuf<int> of(1);
+      SSB_CUDA(cudaMemsetAsync(of.get(), 0, sizeof(int), P.ctx->stream));
+      tile_overflow_kernel<<<grid1(P.ctx, n), 256, 0, P.ctx->stream>>>(ptr, idx, n, tile, of.get());
+      P.ctx->check_launch("tile_overflow_kernel");
+      int bad = 0;
+      P.ctx->copy(&bad, of.get(), sizeof(int));
+      if (bad) u16 = mir = false;
+    }
     if (u16) {
       DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
       DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
@@ -2682,9 +2714,14 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(rows_total > 0 ? nnz_total / rows_total : 0));
   P->vs_back = env_int("SSB_VS_BACK", pick_vs(cols_total > 0 ? nnz_total / cols_total : 0));
   if (P->paired) {
-    P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(nnz_total / std::max(rows_total, 1.0)));
-    P->vs_back = env_int("SSB_VS_BACK", pick_vs(nnz_total / std::max(cols_total, 1.0)));
-    P->uf_fwd = env_int("SSB_UF_FWD", 4);  // measured best for the paired streams
+    // measured best for the paired streams (config 3 sweeps, profiles/r01_notes.md):
+    // fp32 mirror-coded streams carry 6 bytes per entry and prefer 8-lane groups
+    // down to ~100 entries per vector; fp64 mirror-coded K1 spills at UF = 4
+    const bool mir32 = P->mir_f && o.dtype == SS_F32;
+    const auto vs_of = [&](double avg) { return mir32 ? pick_vs_mirror(avg) : pick_vs(avg); };
+    P->vs_fwd = env_int("SSB_VS_FWD", vs_of(nnz_total / std::max(rows_total, 1.0)));
+    P->vs_back = env_int("SSB_VS_BACK", vs_of(nnz_total / std::max(cols_total, 1.0)));
+    P->uf_fwd = env_int("SSB_UF_FWD", P->mir_f && o.dtype == SS_F64 ? 2 : 4);
     P->uf_back = env_int("SSB_UF_BACK", 2);
   }
   if (!P->paired) {
