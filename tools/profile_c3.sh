@@ -6,6 +6,8 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --page raw \
     $CMD > gpurun_out/launches_raw.csv 2> gpurun_out/ncu_launch.err
-ncu --set full --clock-control none --import-source on -k regex:'sart_(fwd|back)_pair' -s 40 -c 4 \
-    -o gpurun_out/prof_pair $CMD > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+for dir in fwd back; do
+  ncu --set full --clock-control none --import-source on -k regex:"sart_${dir}_pair" -s 20 -c 2 \
+      -o gpurun_out/prof_pair_$dir $CMD > gpurun_out/ncu_full_$dir.log 2>&1
+  tail -2 gpurun_out/ncu_full_$dir.log
+done
