@@ -55,7 +55,7 @@ struct Plan {
   bool l2_window = false;  // persisting L2 access-policy window on the gathered vector
   int layout_mode(bool fwd) const {
     if (!tiled) return 0;
-    if (!(fwd ? c16f : c16b)) return 1;
+    if (!(fwd ? c16f : c16b)) return (fwd ? mir_f : mir_b) ? 6 : 1;
     if (fwd ? mir_f : mir_b) return stream_cs ? 5 : 4;
     return stream_cs ? 3 : 2;
   }

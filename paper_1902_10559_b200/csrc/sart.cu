@@ -666,8 +666,11 @@ __device__ __forceinline__ void load4s(const double* p, double (&v)[4]) {
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
-template <class T, int VS, int UF, bool CS = false>
+// With U16 = false (tiles spanning >= 65536 indices, e.g. config 5's K2) the
+// entries keep int32 indices (tidx) and the header's base word is unused.
+template <class T, int VS, int UF, bool CS = false, bool U16 = true>
 __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off,
+                                          const int* __restrict__ tidx,
                                           const unsigned* __restrict__ hdr, int tf,
                                           const T* __restrict__ v1,
                                           const typename Vec2<T>::type* __restrict__ xv, int beg,
@@ -680,6 +683,7 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
   int q = lane;
   for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
     uint2 o[UF];
+    int4 ci[UF];
     int b[UF];
     unsigned s[UF];
     T v[UF][4];
@@ -687,13 +691,16 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
       const int k0 = beg + ((q + u * VS) << 2);
-      o[u] = lds<CS>(reinterpret_cast<const uint2*>(off + k0));
+      if constexpr (U16) o[u] = lds<CS>(reinterpret_cast<const uint2*>(off + k0));
+      else ci[u] = lds<CS>(reinterpret_cast<const int4*>(tidx + k0));
       load_hdr<VS>(hdr, t0 + u, lane, b[u], s[u]);
       load4s<CS>(v1 + k0, v[u]);
     }
 #pragma unroll
     for (int u = 0; u < UF; ++u) {
-      const int4 c = decode16(o[u], b[u]);
+      int4 c;
+      if constexpr (U16) c = decode16(o[u], b[u]);
+      else c = ci[u];
       const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
                g3 = __ldg(xv + c.w);
       sa += flip(v[u][0], s[u], 0) * g0.x + flip(v[u][1], s[u], 1) * g1.x +
@@ -706,7 +713,9 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
     int b;
     unsigned s;
     load_hdr<VS>(hdr, tf + (q - lane) / VS, lane, b, s);
-    const int4 c = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)), b);
+    int4 c;
+    if constexpr (U16) c = decode16(__ldg(reinterpret_cast<const uint2*>(off + k0)), b);
+    else c = __ldg(reinterpret_cast<const int4*>(tidx + k0));
     T v[4];
     load4s<CS>(v1 + k0, v);
     const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
@@ -775,8 +784,9 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
       if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
       T da, db;
       if (TL >= 4) {
-        seg_dot2m<T, VS, UF, TL == 5>(k.tof, k.thf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx),
-                                      beg, end, eb, ee, k.eif, k.evf, lane, mask, da, db);
+        seg_dot2m<T, VS, UF, TL == 5, TL != 6>(k.tof, k.tif, k.thf, tf, k.rv2,
+                                                reinterpret_cast<const T2*>(k.xx), beg, end, eb,
+                                                ee, k.eif, k.evf, lane, mask, da, db);
       } else if (TL >= 2) {
         seg_dot2c<T, VS, UF, TL == 3>(k.tof, k.tbf, tf, k.rv2, reinterpret_cast<const T2*>(k.xx),
                                       beg, end, lane, mask, da, db);
@@ -872,8 +882,9 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     }
     T ua, ub;
     if (TL >= 4) {
-      seg_dot2m<T, VS, UF, TL == 5>(k.tob, k.thb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww),
-                                    beg, end, eb, ee, k.eib, k.evb, lane, mask, ua, ub);
+      seg_dot2m<T, VS, UF, TL == 5, TL != 6>(k.tob, k.tib, k.thb, tf, k.cv2,
+                                              reinterpret_cast<const T2*>(k.ww), beg, end, eb, ee,
+                                              k.eib, k.evb, lane, mask, ua, ub);
     } else if (TL >= 2) {
       seg_dot2c<T, VS, UF, TL == 3>(k.tob, k.tbb, tf, k.cv2, reinterpret_cast<const T2*>(k.ww),
                                     beg, end, lane, mask, ua, ub);
@@ -1206,6 +1217,7 @@ __global__ void tile_mirror_kernel(const int* __restrict__ ptr, const int* __res
                                    const double* __restrict__ v0, const double* __restrict__ v1,
                                    long long nvec, const int* __restrict__ tptr,
                                    const int* __restrict__ tfirst, unsigned short* __restrict__ tofs,
+                                   int* __restrict__ tidx,
                                    unsigned* __restrict__ thdr, int hs, T* __restrict__ tv,
                                    int tile, int* __restrict__ overflow) {
   const int lane = threadIdx.x & 31;
@@ -1240,7 +1252,8 @@ __global__ void tile_mirror_kernel(const int* __restrict__ ptr, const int* __res
         }
         const unsigned d = static_cast<unsigned>(c - base);
         bad |= d > 0xffffu;
-        tofs[ob + p] = static_cast<unsigned short>(d);
+        if (tofs) tofs[ob + p] = static_cast<unsigned short>(d);
+        else tidx[ob + p] = c;  // int32 indices (tiles too wide for 16 bits)
         tv[ob + p] = v;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, neg);
@@ -1733,6 +1746,8 @@ PairFn<T> pair_kernel(const Plan& P, bool fwd, int* smem) {
 #define SSB_PAIR(V, U)                                                                        \
   if (vs == V && uf == U) {                                                                   \
     if (!P.tiled) return fwd ? sart_fwd_pair_kernel<T, V, U, 0> : sart_back_pair_kernel<T, V, U, 0>; \
+    if ((fwd ? P.mir_f : P.mir_b) && !(fwd ? P.c16f : P.c16b))                                \
+      return fwd ? sart_fwd_pair_kernel<T, V, U, 6> : sart_back_pair_kernel<T, V, U, 6>;      \
     if ((fwd ? P.mir_f : P.mir_b) && P.stream_cs)                                            \
       return fwd ? sart_fwd_pair_kernel<T, V, U, 5> : sart_back_pair_kernel<T, V, U, 5>;      \
     if (fwd ? P.mir_f : P.mir_b)                                                              \
@@ -2332,11 +2347,11 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
              : nb * (4 + 2 * b) + 4 * (cols[0] + 1);
     // mirror-coded: offsets + one value per entry + tile headers + exceptions
     if (mir_f) {
-      f = nf * (2 + b) + 4 * hs_f * ntile_f + 8 * (rows[0] + 1) +
+      f = nf * ((c16f ? 2 : 4) + b) + 4 * hs_f * ntile_f + 8 * (rows[0] + 1) +
           (nexc_f ? nexc_f * (4 + 2 * b) + 4 * (rows[0] + 1) : 0);
     }
     if (mir_b) {
-      k = nb * (2 + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
+      k = nb * ((c16b ? 2 : 4) + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
           (nexc_b ? nexc_b * (4 + 2 * b) + 4 * (cols[0] + 1) : 0);
     }
   } else if (tiled && nsys == 1 && nrhs == 1) {
@@ -2482,6 +2497,34 @@ std::int64_t tiled_ptr(Plan& P, const int* ptr, long long n, DBuf<int>& tptr) {
 // padded pointers, then per direction 16-bit offsets + tile bases when every
 // tile spans < 65536 indices, else int32 indices. Returns false if the padded
 // offsets would overflow int32 (the plan then keeps the plain layout).
+// Exception buckets (a1 != +-a2 in the plan type) of one direction, per vector.
+template <class T>
+void build_exceptions(Plan& P, bool fwd, const int* ptr, const int* idx, const double* v0,
+                      const double* v1, long long n, int gw) {
+  DBuf<int>& eptr = fwd ? P.eptr_f : P.eptr_b;
+  std::int64_t& nexc = fwd ? P.nexc_f : P.nexc_b;
+  DBuf<int> cnt(n + 1);
+  SSB_CUDA(cudaMemsetAsync(cnt.get(), 0, (n + 1) * sizeof(int), P.ctx->stream));
+  mirror_exc_count_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(ptr, v0, v1, n, cnt.get());
+  P.ctx->check_launch("mirror_exc_count_kernel");
+  eptr.alloc(n + 1);
+  scan_counts(P.ctx, cnt.get(), eptr.get(), n);
+  int ne = 0;
+  P.ctx->copy(&ne, eptr.get() + n, sizeof(int));
+  nexc = ne;
+  if (ne == 0) {
+    eptr.release();
+    return;
+  }
+  DBuf<int>& eidx = fwd ? P.eidx_f : P.eidx_b;
+  DBuf<char>& ev2 = fwd ? P.ev2_f : P.ev2_b;
+  eidx.alloc(ne);
+  ev2.alloc(2 * static_cast<std::size_t>(ne) * sizeof(T));
+  mirror_exc_fill_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(ptr, idx, v0, v1, n, eptr.get(),
+                                                           eidx.get(), reinterpret_cast<T*>(ev2.get()));
+  P.ctx->check_launch("mirror_exc_fill_kernel");
+}
+
 template <class T>
 bool build_tiled_streams(Plan& P, int w) {
   const long long nnz = P.a[0]->nnz, rows = P.rows[0], cols = P.cols[0];
@@ -2505,9 +2548,10 @@ bool build_tiled_streams(Plan& P, int w) {
     const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
     const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
     DBuf<char>& vbuf = fwd ? P.rv2 : P.cv2;
+    DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
     bool& u16 = fwd ? P.c16f : P.c16b;
     bool& mir = fwd ? P.mir_f : P.mir_b;
-    mir = mir && u16 && w == 2;
+    mir = mir && w == 2;
     if (u16) {  // 16 bits fit every tile? (decided before any stream buffer exists)
       DBuf<int> of(1);
       SSB_CUDA(cudaMemsetAsync(of.get(), 0, sizeof(int), P.ctx->stream));
@@ -2515,12 +2559,10 @@ bool build_tiled_streams(Plan& P, int w) {
       P.ctx->check_launch("tile_overflow_kernel");
       int bad = 0;
       P.ctx->copy(&bad, of.get(), sizeof(int));
-      if (bad) u16 = mir = false;
+      if (bad) u16 = false;
     }
-    if (u16) {
+    if (u16 || mir) {  // per-tile data: first tile of every vector
       DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
-      DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
-      DBuf<int>& tbase = fwd ? P.tbase_f : P.tbase_b;
       std::int64_t& ntile = fwd ? P.ntile_f : P.ntile_b;
       DBuf<int> cnt(n + 1), overflow(1);
       tfirst.alloc(n + 1);
@@ -2531,9 +2573,9 @@ bool build_tiled_streams(Plan& P, int w) {
       int total = 0;
       P.ctx->copy(&total, tfirst.get() + n, sizeof(int));
       ntile = total;
-      tofs.alloc(tn);
       SSB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), P.ctx->stream));
-      if (mir) {
+      DBuf<unsigned short>& tofs = fwd ? P.tofs_f : P.tofs_b;
+      if (mir) {  // one value + sign bits; 16-bit offsets or int32 indices
         DBuf<unsigned>& thdr = fwd ? P.thdr_f : P.thdr_b;
         int& hs = fwd ? P.hs_f : P.hs_b;
         hs = tile <= 32 ? 2 : (tile == 64 ? 4 : 8);
@@ -2541,61 +2583,26 @@ bool build_tiled_streams(Plan& P, int w) {
         SSB_CUDA(cudaMemsetAsync(thdr.get(), 0, static_cast<std::size_t>(ntile) * hs * 4,
                                  P.ctx->stream));
         vbuf.alloc(tn * tb);
+        if (u16) tofs.alloc(tn);
+        else tidx.alloc(tn);
         tile_mirror_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(
-            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
-            thdr.get(), hs, reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
+            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(),
+            u16 ? tofs.get() : nullptr, u16 ? nullptr : tidx.get(), thdr.get(), hs,
+            reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
         P.ctx->check_launch("tile_mirror_kernel");
-        int bad = 0;
-        P.ctx->copy(&bad, overflow.get(), sizeof(int));
-        if (!bad) {
-          // exception buckets (a1 != +-a2 in the plan type) per vector
-          DBuf<int>& eptr = fwd ? P.eptr_f : P.eptr_b;
-          std::int64_t& nexc = fwd ? P.nexc_f : P.nexc_b;
-          SSB_CUDA(cudaMemsetAsync(cnt.get(), 0, (n + 1) * sizeof(int), P.ctx->stream));
-          mirror_exc_count_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(ptr, vals(0, fwd),
-                                                                    vals(1, fwd), n, cnt.get());
-          P.ctx->check_launch("mirror_exc_count_kernel");
-          eptr.alloc(n + 1);
-          scan_counts(P.ctx, cnt.get(), eptr.get(), n);
-          int ne = 0;
-          P.ctx->copy(&ne, eptr.get() + n, sizeof(int));
-          nexc = ne;
-          if (ne == 0) {
-            eptr.release();
-            return;
-          }
-          DBuf<int>& eidx = fwd ? P.eidx_f : P.eidx_b;
-          DBuf<char>& ev2 = fwd ? P.ev2_f : P.ev2_b;
-          eidx.alloc(ne);
-          ev2.alloc(2 * static_cast<std::size_t>(ne) * tb);
-          mirror_exc_fill_kernel<T><<<gw, 256, 0, P.ctx->stream>>>(
-              ptr, idx, vals(0, fwd), vals(1, fwd), n, eptr.get(), eidx.get(),
-              reinterpret_cast<T*>(ev2.get()));
-          P.ctx->check_launch("mirror_exc_fill_kernel");
-          return;
-        }
-        // a tile spans >= 65536 indices: the same offsets fail 16 bits below
-        (fwd ? P.thdr_f : P.thdr_b).release();
-        mir = false;
-        u16 = false;
-      } else {
-        tbase.alloc(ntile);
-        vbuf.alloc(w * tn * tb);
-        tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
-            ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
-            tbase.get(), reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
-        P.ctx->check_launch("tile_stream16_kernel");
-        int bad = 0;
-        P.ctx->copy(&bad, overflow.get(), sizeof(int));
-        if (!bad) return;
-        u16 = false;
+        build_exceptions<T>(P, fwd, ptr, idx, vals(0, fwd), vals(1, fwd), n, gw);
+        return;
       }
-      tofs.release();
-      tbase.release();
-      tfirst.release();
-      ntile = 0;
+      DBuf<int>& tbase = fwd ? P.tbase_f : P.tbase_b;  // interleaved values, 16-bit offsets
+      tofs.alloc(tn);
+      tbase.alloc(ntile);
+      vbuf.alloc(w * tn * tb);
+      tile_stream16_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
+          ptr, idx, vals(0, fwd), vals(1, fwd), n, tptr.get(), tfirst.get(), tofs.get(),
+          tbase.get(), reinterpret_cast<T*>(vbuf.get()), tile, overflow.get());
+      P.ctx->check_launch("tile_stream16_kernel");
+      return;
     }
-    DBuf<int>& tidx = fwd ? P.tidx_f : P.tidx_b;
     tidx.alloc(tn);
     vbuf.alloc(w * tn * tb);
     tile_stream_kernel<T, double><<<gw, 256, 0, P.ctx->stream>>>(
@@ -2984,7 +2991,7 @@ __device__ __forceinline__ void pair_sweep(const SartK<T>& k, long long n,
     beg = __ldg(ptr + g);
     end = __ldg(ptr + g + 1);
     if (TL >= 2) tf = __ldg(tfp + g);
-    if (TL == 4 && ep) {
+    if ((TL == 4 || TL == 6) && ep) {
       eb = __ldg(ep + g);
       ee = __ldg(ep + g + 1);
     }
@@ -2996,14 +3003,15 @@ __device__ __forceinline__ void pair_sweep(const SartK<T>& k, long long n,
       nbeg = __ldg(ptr + gn);
       nend = __ldg(ptr + gn + 1);
       if (TL >= 2) ntf = __ldg(tfp + gn);
-      if (TL == 4 && ep) {
+      if ((TL == 4 || TL == 6) && ep) {
         neb = __ldg(ep + gn);
         nee = __ldg(ep + gn + 1);
       }
     }
     T a, b;
-    if (TL == 4) {
-      seg_dot2m<T, VS, UF>(FWD ? k.tof : k.tob, FWD ? k.thf : k.thb, tf, FWD ? k.rv2 : k.cv2,
+    if (TL == 4 || TL == 6) {
+      seg_dot2m<T, VS, UF, false, TL == 4>(FWD ? k.tof : k.tob, FWD ? k.tif : k.tib,
+                                           FWD ? k.thf : k.thb, tf, FWD ? k.rv2 : k.cv2,
                            vec, beg, end, eb, ee, FWD ? k.eif : k.eib, FWD ? k.evf : k.evb, lane,
                            mask, a, b);
     } else if (TL == 2) {
@@ -3216,15 +3224,18 @@ void run_cgls_pair(Plan& P, const double* p[2], const ss_solve_options& o, doubl
   void (*fwd)(CgPairK<T>) = nullptr;
   void (*back)(CgPairK<T>, int) = nullptr;
   const int vsf = P.vs_fwd, vsb = P.vs_back;
-  const int mf = P.mir_f ? 4 : (P.c16f ? 2 : 1), mb = P.mir_b ? 4 : (P.c16b ? 2 : 1);
+  const int mf = P.mir_f ? (P.c16f ? 4 : 6) : (P.c16f ? 2 : 1);
+  const int mb = P.mir_b ? (P.c16b ? 4 : 6) : (P.c16b ? 2 : 1);
 #define SSB_CGF(V, M) if (vsf == V && mf == M) fwd = cgp_fwd_kernel<T, V, 4, M>;
 #define SSB_CGB(V, M) if (vsb == V && mb == M) back = cgp_back_kernel<T, V, 2, M>;
   SSB_CGF(4, 1) SSB_CGF(8, 1) SSB_CGF(16, 1) SSB_CGF(32, 1)
   SSB_CGF(4, 2) SSB_CGF(8, 2) SSB_CGF(16, 2) SSB_CGF(32, 2)
   SSB_CGF(4, 4) SSB_CGF(8, 4) SSB_CGF(16, 4) SSB_CGF(32, 4)
+  SSB_CGF(4, 6) SSB_CGF(8, 6) SSB_CGF(16, 6) SSB_CGF(32, 6)
   SSB_CGB(4, 1) SSB_CGB(8, 1) SSB_CGB(16, 1) SSB_CGB(32, 1)
   SSB_CGB(4, 2) SSB_CGB(8, 2) SSB_CGB(16, 2) SSB_CGB(32, 2)
   SSB_CGB(4, 4) SSB_CGB(8, 4) SSB_CGB(16, 4) SSB_CGB(32, 4)
+  SSB_CGB(4, 6) SSB_CGB(8, 6) SSB_CGB(16, 6) SSB_CGB(32, 6)
 #undef SSB_CGF
 #undef SSB_CGB
   if (!fwd || !back) fail("cgls: unsupported paired kernel shape");

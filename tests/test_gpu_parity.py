@@ -360,7 +360,7 @@ def _wide_centro(seed, mh, nh, per_row, span):
 
 
 @pytest.mark.parametrize("span,per_row", [(3000, 150), (200000, 8)])
-def test_paired_tiled_layouts_match_oracle(span, per_row):
+def test_paired_tiled_layouts_match_oracle(span, per_row, monkeypatch):
     m, n, r, c, v, p = _wide_centro(7 + span, 96, 120000, per_row, span)
     a = P.Matrix.from_triplets(m, n, r, c, v)
     sys_ = P.CentroSystem(a, p, 0.0)
@@ -368,13 +368,20 @@ def test_paired_tiled_layouts_match_oracle(span, per_row):
     plan = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0))
     d = plan.describe()
     assert d["layout"] == "paired-tiled-u16-mirror"
-    # K2 (columns list rows < 96) always fits 16 bits (mirror-coded); K1 falls
-    # back to int32 indices with interleaved values for wide rows
+    # K2 (columns list rows < 96) always fits 16 bits (mirror-coded); K1 keeps
+    # int32 indices for wide rows (mirror-coded values, layout mode 6)
     assert d["back_kernel"].endswith(", 4>")
-    assert d["fwd_kernel"].endswith(", 4>" if span < 65536 else ", 1>")
+    assert d["fwd_kernel"].endswith(", 4>" if span < 65536 else ", 6>")
+    # the same system through the interleaved (non-mirror) streams
+    monkeypatch.setenv("SSB_MIRROR", "0")
+    d0 = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0)).describe()
+    assert d0["fwd_kernel"].endswith(", 2>" if span < 65536 else ", 1>")
+    plain = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
+    monkeypatch.setenv("SSB_MIRROR", "1")
     got = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
     ref = O.solve_split(O.Matrix.triplets(m, n, r, c, v), p, 0.0, 12, 0.0, 1.0)
     assert rel_err(got.f, ref.f) <= TOL_F64
+    assert rel_err(got.f, plain.f) <= 1e-13
     got32 = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0, dtype="f32"))
     assert rel_err(got32.f, ref.f) <= TOL_F32
 
