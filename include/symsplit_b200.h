@@ -270,6 +270,34 @@ int ss_partition_rows(const int32_t* rowptr, int64_t rows, int parts, int64_t* b
 int ss_plan_create_sharded(ss_ctx_t ctx, ss_matrix_t a, int64_t row_begin, int64_t row_end,
                            const ss_solve_options* opts, ss_plan_t* out);
 
+/* How the ranks of a row-sharded system combine their back-projections.
+ * SS_XCHG_NCCL: K2 writes the partial A_g^T w_g, then ncclAllReduce + update.
+ * SS_XCHG_PEER: fused exchange over NVLink peer memory. K2 stores each chunk
+ *   of columns straight into the owning rank's receive buffer; the last rank
+ *   to arrive on a chunk sums the G partials in rank order, applies the
+ *   update and stores the new x chunk into every rank's replica; the next K1
+ *   waits (device-side) for all chunks. No NCCL call on the data path; the
+ *   regions are mapped with CUDA IPC (handles exchanged once over the
+ *   context's NCCL communicator). Replaces the same reference loop as
+ *   ss_plan_create_sharded (solvers.cpp:173-192). */
+#define SS_XCHG_NCCL 0
+#define SS_XCHG_PEER 1
+/* columns [col_begin, col_end) whose partials rank `rank` of `parts` reduces
+ * and whose x it pushes to every replica (host, no GPU needed) */
+int ss_exchange_owned_columns(int64_t cols, int parts, int rank, int64_t* col_begin,
+                              int64_t* col_end);
+int ss_plan_create_sharded_x(ss_ctx_t ctx, ss_matrix_t a, int64_t row_begin, int64_t row_end,
+                             const ss_solve_options* opts, int exchange, ss_plan_t* out);
+/* One-device emulation of `parts` peer-exchange ranks (tests and single-GPU
+ * measurement of the fused exchange): plans[g] keeps rows
+ * [bounds[g], bounds[g+1]) and the plans' regions are linked directly. Set
+ * each plan's rhs slice with ss_plan_set_rhs, then ss_plan_group_run launches
+ * every rank's kernels in rank order on the shared stream; ss_plan_finish /
+ * get_solution / get_history work per plan. */
+int ss_plan_create_sharded_group(ss_ctx_t ctx, ss_matrix_t a, int parts, const int64_t* bounds,
+                                 const ss_solve_options* opts, ss_plan_t* plans);
+int ss_plan_group_run(ss_plan_t* plans, int parts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,6 +126,12 @@ SIGNATURES = {
     "ss_partition_rows": (C.c_int, [i32p, i64, C.c_int, i64p]),
     "ss_plan_create_sharded": (C.c_int, [vp, vp, i64, i64, C.POINTER(SolveOptionsC),
                                          C.POINTER(vp)]),
+    "ss_exchange_owned_columns": (C.c_int, [i64, C.c_int, C.c_int, i64p, i64p]),
+    "ss_plan_create_sharded_x": (C.c_int, [vp, vp, i64, i64, C.POINTER(SolveOptionsC), C.c_int,
+                                           C.POINTER(vp)]),
+    "ss_plan_create_sharded_group": (C.c_int, [vp, vp, C.c_int, i64p, C.POINTER(SolveOptionsC),
+                                               C.POINTER(vp)]),
+    "ss_plan_group_run": (C.c_int, [C.POINTER(vp), C.c_int]),
     "ss_read_matrix_market": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
     "ss_write_matrix_market": (C.c_int, [vp, C.c_char_p]),
     "ss_read_vector_csv": (C.c_int, [C.c_char_p, dp, i64, i64p]),

@@ -1021,4 +1021,56 @@ int ss_plan_create_sharded(ss_ctx_t h, ss_matrix_t a, int64_t row_begin, int64_t
   });
 }
 
+int ss_exchange_owned_columns(int64_t cols, int parts, int rank, int64_t* col_begin,
+                              int64_t* col_end) {
+  return guarded([&] {
+    need(col_begin, "col_begin");
+    need(col_end, "col_end");
+    ssb::exchange_owned_columns(cols, parts, rank, col_begin, col_end);
+  });
+}
+
+int ss_plan_create_sharded_x(ss_ctx_t h, ss_matrix_t a, int64_t row_begin, int64_t row_end,
+                             const ss_solve_options* opts, int exchange, ss_plan_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::make_sharded_plan(ctx, M(a), row_begin, row_end, *opts, exchange));
+  });
+}
+
+int ss_plan_create_sharded_group(ss_ctx_t h, ss_matrix_t a, int parts, const int64_t* bounds,
+                                 const ss_solve_options* opts, ss_plan_t* plans) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(bounds, "bounds");
+    need(plans, "plans");
+    if (parts < 1) ssb::fail("plan: parts must be >= 1");
+    use_device(ctx);
+    std::vector<std::unique_ptr<ssb::Plan>> made;
+    for (int g = 0; g < parts; ++g) {
+      made.emplace_back(ssb::make_sharded_plan(ctx, M(a), bounds[g], bounds[g + 1], *opts,
+                                               SS_XCHG_PEER, parts, g));
+    }
+    std::vector<ssb::Plan*> raw;
+    for (auto& p : made) raw.push_back(p.get());
+    ssb::link_group(raw.data(), parts);
+    for (int g = 0; g < parts; ++g) plans[g] = wrap(made[g].release());
+  });
+}
+
+int ss_plan_group_run(ss_plan_t* plans, int parts) {
+  return guarded([&] {
+    need(plans, "plans");
+    if (parts < 1) ssb::fail("plan: parts must be >= 1");
+    std::vector<ssb::Plan*> raw;
+    for (int g = 0; g < parts; ++g) raw.push_back(PL(plans[g]));
+    use_device(raw[0]->ctx);
+    ssb::run_group(raw.data(), parts);
+  });
+}
+
 }  // extern "C"

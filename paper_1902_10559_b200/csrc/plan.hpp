@@ -6,6 +6,30 @@
 
 namespace ssb {
 
+// Fused row-sharded exchange over peer memory (replaces the NCCL all-reduce of
+// the back-projection; sart.cu "peer exchange"). Every rank owns one region
+// (plain cudaMalloc, IPC-exportable) with the same layout:
+//   recv [G][cols]  row g: rank g's partial back-projection of the columns
+//                   this rank owns ([me*own, (me+1)*own))
+//   x    [cols]     this rank's replica of the iterate
+//   r2   [2][G]     ||r_g||^2 of every rank, by iteration parity
+//   done            ranks whose K2x finished (monotone over solves)
+//   xready          owners whose reduce pushed their x range here
+//   dflag           first diverged iteration (+1) seen by any owner
+struct PeerExchange {
+  int G = 1, me = 0;
+  bool emulated = false;  // all ranks' plans on one device, launched in rank order
+  std::int64_t cols = 0, own = 0;  // columns, columns owned per rank
+  int rgrid = 0;                    // CTAs of the reduce kernel
+  std::size_t off_recv = 0, off_x = 0, off_r2 = 0, off_done = 0, off_xready = 0,
+              off_dflag = 0, bytes = 0;
+  void* region = nullptr;
+  std::vector<void*> opened;  // peers' regions mapped through CUDA IPC
+  DBuf<char*> peers;          // [G] region base of every rank as seen from this device
+  DBuf<long long> local;      // {epoch base, iterations proceeded this solve, timeout}
+  ~PeerExchange();
+};
+
 struct Plan {
   Context* ctx = nullptr;
   int nsys = 1;
@@ -32,6 +56,7 @@ struct Plan {
   DBuf<int> state;        // [nsys*nrhs][4] stopped, stop_it, diverged_at, -
   DBuf<unsigned> ticket;  // last-block ticket of the forward kernel
   DBuf<char> bp;          // sharded: back-projection + ||r||^2 slot (all-reduced)
+  PeerExchange* px = nullptr;  // sharded over peer memory instead of NCCL
   DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
   DBuf<char> rv2, cv2;    // paired: CSR / CSC values interleaved [nnz][2]
   DBuf<char> pe, cc;      // paired: {p1,p2,rinv1,rinv2} per row, {cinv1,cinv2} per column
@@ -67,6 +92,8 @@ struct Plan {
   bool while_capture = false;             // make_args: kernels read / advance iter_dev
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;
+  float group_ms = -1.0f;
+  double pn_local = -1.0;  // emulated exchange rank: local ||p_g|| (run_group combines)  // emulated exchange group: time of the whole group's solve
   bool launched = false;
   bool empty_rows[2] = {false, false};  // all row sums zero (reference throws)
 
@@ -95,8 +122,18 @@ struct Plan {
 
 Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs,
                 bool reusable = true);
+// exchange: SS_XCHG_NCCL or SS_XCHG_PEER. emul_parts > 0 builds rank
+// emul_rank of a one-device emulation (no communicator; see run_group).
 Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t row_begin, std::int64_t row_end,
-                        const ss_solve_options& o);
+                        const ss_solve_options& o, int exchange = SS_XCHG_NCCL,
+                        int emul_parts = 0, int emul_rank = 0);
+// link the plans of a one-device emulation to each other's exchange regions
+void link_group(Plan* const* plans, int parts);
+// one solve of an emulated group: all ranks' launches in rank order on the
+// shared stream (no launch ever waits on one that has not completed)
+void run_group(Plan* const* plans, int parts);
 void partition_rows(const int* rowptr, std::int64_t rows, int parts, std::int64_t* bounds);
+void exchange_owned_columns(std::int64_t cols, int parts, int rank, std::int64_t* begin,
+                            std::int64_t* end);
 
 }  // namespace ssb

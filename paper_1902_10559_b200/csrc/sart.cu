@@ -1559,6 +1559,352 @@ __global__ void sharded_r2_kernel(const double* partial, int nblk, T* slot) {
   if (threadIdx.x == 0) *slot = static_cast<T>(sh[0]);
 }
 
+// ------------------------------------------------------------ peer exchange
+// Row-sharded SART with the all-reduce replaced by peer-memory traffic
+// (SURVEY §8e level 3; region layout in plan.hpp PeerExchange). Rank h owns
+// the contiguous column range [h*own, (h+1)*own). Per iteration on rank me:
+//   K1x  announces that this rank's previous reduce finished (one atomic per
+//        rank into `xready`), waits until all G owners have pushed the
+//        previous iteration's x range into this rank's replica, settles that
+//        iteration's ||r|| (history, stop test) from the ranks' ||r_g||^2,
+//        then runs the usual K1 over the local rows; its last block stores
+//        ||r_me||^2 into every rank's slot.
+//   K2x  the usual K2 over the local row block's CSC, except that each
+//        column's partial (A_me^T w_me)_j goes straight into row `me` of the
+//        owner's receive buffer — NVLink stores issued from the SpMV as the
+//        columns complete, so the reduce-scatter's transfer overlaps the math.
+//   Rx   (owner side) announces that this rank's K2x finished (`done`), waits
+//        for all G ranks' K2x, sums the G partials of its columns in rank
+//        order (the same bits on every run, independent of timing), applies
+//        the update unless the iteration stopped and stores the new x range
+//        into every replica.
+// Every signal is issued by the kernel *after* the one whose stores it
+// announces: stream order has completed those stores (kernel boundary), so no
+// system-scope fence is needed on the data path (measured: fences at the end
+// of every K2x / reduce CTA cost 13-16 us per iteration). Counters are
+// monotone over solves (epoch base in `local`); no kernel resets a peer's
+// state, and every wait is bounded (timeout flag, reported by Plan::finish) so
+// a lost rank fails the solve instead of hanging the GPU.
+template <class T>
+struct XK {
+  char* const* peers;
+  int G, me;
+  long long cols, own;  // columns, columns owned per rank
+  int rgrid;            // CTAs of the reduce kernel
+  unsigned long long off_recv, off_x, off_r2, off_done, off_xready, off_dflag;
+  long long* local;     // {epoch base, iterations proceeded, timeout}
+  int inline_signal;    // 1: kernels announce; 0 (emulated group): announce kernels do
+};
+
+template <class T>
+__device__ __forceinline__ char* xbase(const XK<T>& x, int r) {
+  return reinterpret_cast<char*>(
+      __ldg(reinterpret_cast<const unsigned long long*>(x.peers) + r));
+}
+template <class T>
+__device__ __forceinline__ T* xrecv(const XK<T>& x, int r) {
+  return reinterpret_cast<T*>(xbase(x, r) + x.off_recv);
+}
+template <class T>
+__device__ __forceinline__ T* xrep(const XK<T>& x, int r) {
+  return reinterpret_cast<T*>(xbase(x, r) + x.off_x);
+}
+template <class T>
+__device__ __forceinline__ double* xr2(const XK<T>& x, int r) {
+  return reinterpret_cast<double*>(xbase(x, r) + x.off_r2);
+}
+template <class T>
+__device__ __forceinline__ unsigned long long* xdone(const XK<T>& x, int r) {
+  return reinterpret_cast<unsigned long long*>(xbase(x, r) + x.off_done);
+}
+template <class T>
+__device__ __forceinline__ unsigned long long* xready(const XK<T>& x, int r) {
+  return reinterpret_cast<unsigned long long*>(xbase(x, r) + x.off_xready);
+}
+template <class T>
+__device__ __forceinline__ int* xdflag(const XK<T>& x, int r) {
+  return reinterpret_cast<int*>(xbase(x, r) + x.off_dflag);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_sys(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// one count into counter `off` of every rank (the stores being announced
+// belong to an earlier, completed kernel of this stream)
+template <class T>
+__device__ void signal_all(const XK<T>& x, unsigned long long off) {
+  for (int r = 0; r < x.G; ++r) {
+    atomicAdd_system(reinterpret_cast<unsigned long long*>(xbase(x, r) + off), 1ull);
+  }
+}
+
+// ~4 s at 1.9 GHz: far beyond any healthy exchange wait (microseconds)
+constexpr long long kSpinCycles = 8000000000LL;
+
+__device__ bool wait_geq(const unsigned long long* p, unsigned long long target,
+                         long long* timeout) {
+  if (ld_acquire_sys(p) >= target) return true;
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < target) {
+    if (*reinterpret_cast<volatile long long*>(timeout) != 0) return false;
+    if (clock64() - t0 > kSpinCycles) {
+      if (atomicExch(reinterpret_cast<unsigned long long*>(timeout), 1ull) == 0ull) {
+        printf("symsplit_b200: exchange wait timed out (counter %llu, want %llu, block %d, "
+               "grid %d)\n", ld_acquire_sys(p), target, static_cast<int>(blockIdx.x),
+               static_cast<int>(gridDim.x));
+      }
+      return false;
+    }
+    __nanosleep(100);
+  }
+  return true;
+}
+
+// ||r||^2 of absolute iteration e: the ranks' contributions in rank order
+template <class T>
+__device__ double xr2_sum(const XK<T>& x, long long e) {
+  const double* s = xr2(x, x.me) + (e & 1) * x.G;
+  double t = 0.0;
+  for (int g = 0; g < x.G; ++g) t += ld_sys(s + g);
+  return t;
+}
+
+template <class T>
+__device__ __forceinline__ unsigned long long xready_target(const XK<T>& x, long long epochs) {
+  return static_cast<unsigned long long>(x.G) * epochs;
+}
+
+// K1x prologue (thread 0 of every block; every block decides alike): wait for
+// the previous iteration's x, settle its residual / stop / divergence.
+template <class T>
+__device__ int xchg_enter(const SartK<T>& k, const XK<T>& x, int it) {
+  volatile int* st = k.state;
+  // reduce it-1 ran iff K1x(it-1) proceeded; announce its x pushes (block 0)
+  if (x.inline_signal && blockIdx.x == 0 && it > 0 && x.local[1] == it) {
+    signal_all(x, x.off_xready);
+  }
+  if (st[0] != 0 || st[2] != 0) return 0;
+  const long long base = x.local[0];
+  if (!wait_geq(xready(x, x.me), xready_target(x, base + it), x.local + 2)) return 0;
+  if (it > 0) {
+    const int d = ld_sys(xdflag(x, x.me));
+    if (d != 0) {
+      if (blockIdx.x == 0) st[2] = d;
+      return 0;
+    }
+    const double res = sqrt(xr2_sum(x, base + it - 1));
+    if (blockIdx.x == 0) k.history[it - 1] = res;
+    if (res <= k.tol * k.pnorm[0]) {
+      if (blockIdx.x == 0) {
+        st[0] = 1;
+        st[1] = it - 1;
+      }
+      return 0;
+    }
+  }
+  if (blockIdx.x == 0) x.local[1] = it + 1;
+  return 1;
+}
+
+template <class T, int VS, int UF, bool U16>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
+    sart_fwd_xchg_kernel(SartK<T> k, XK<T> x, int it) {
+  cudaGridDependencySynchronize();
+  __shared__ double red[kWarps];
+  __shared__ int go;
+  if (threadIdx.x == 0) go = xchg_enter(k, x, it);
+  __syncthreads();
+  if (!go) return;
+  const SysK<T>& S = k.s[0];
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.rows0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
+  double r2 = 0.0;
+  int beg = 0, end = 0, tf = 0;
+  if (g < n) {
+    beg = __ldg(k.tpf + g);
+    end = __ldg(k.tpf + g + 1);
+    if (U16) tf = __ldg(k.tff + g);
+  }
+  for (; g < n; g += gstep) {
+    const int gn = g + gstep;
+    int nbeg = 0, nend = 0, ntf = 0;
+    if (gn < n) {
+      nbeg = __ldg(k.tpf + gn);
+      nend = __ldg(k.tpf + gn + 1);
+      if (U16) ntf = __ldg(k.tff + gn);
+    }
+    T pv = T(0), ri = T(0);
+    if (lane == 0) {
+      pv = S.p[g];
+      ri = S.rinv[g];
+    }
+    const T dot = seg_dot1<T, VS, UF, U16>(k.tif, k.tof, k.tbf, tf, k.rv2, S.x, beg, end, lane,
+                                           mask);
+    if (lane == 0) {
+      const T r = pv - dot;
+      S.w[g] = ri * r;
+      r2 += static_cast<double>(r) * static_cast<double>(r);
+    }
+    beg = nbeg;
+    end = nend;
+    tf = ntf;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kWarps; ++q) t += red[q];
+    k.partial[blockIdx.x] = t;
+  }
+  if (last_block(k.ticket)) {
+    // fixed-order ||r_me||^2, stored into slot [parity][me] of every rank
+    __shared__ double sh[kThreads];
+    double s = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kThreads) s += k.partial[b];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = kThreads / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    const long long e = x.local[0] + it;
+    if (threadIdx.x < x.G) xr2(x, threadIdx.x)[(e & 1) * x.G + x.me] = sh[0];
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
+template <class T, int VS, int UF, bool U16>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
+    sart_back_xchg_kernel(SartK<T> k, XK<T> x, int it) {
+  cudaGridDependencySynchronize();
+  if (!sys_on(k.state, 0)) return;
+  const SysK<T>& S = k.s[0];
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.cols0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
+  const long long row = static_cast<long long>(x.me) * x.cols;
+  int beg = 0, end = 0, tf = 0;
+  if (g < n) {
+    beg = __ldg(k.tpb + g);
+    end = __ldg(k.tpb + g + 1);
+    if (U16) tf = __ldg(k.tfb + g);
+  }
+  for (; g < n; g += gstep) {
+    const int gn = g + gstep;
+    int nbeg = 0, nend = 0, ntf = 0;
+    if (gn < n) {
+      nbeg = __ldg(k.tpb + gn);
+      nend = __ldg(k.tpb + gn + 1);
+      if (U16) ntf = __ldg(k.tfb + gn);
+    }
+    const T u = seg_dot1<T, VS, UF, U16>(k.tib, k.tob, k.tbb, tf, k.cv2, S.w, beg, end, lane,
+                                         mask);
+    if (lane == 0) {  // NVLink store into the owner's receive row
+      xrecv(x, static_cast<int>(static_cast<unsigned>(g) / static_cast<unsigned>(x.own)))[row + g] = u;
+    }
+    beg = nbeg;
+    end = nend;
+    tf = ntf;
+  }
+}
+
+// Owner side: rank-order sum of the G partials of this rank's columns,
+// update (unless the iteration stopped), push the new range to every replica.
+template <class T>
+__global__ void __launch_bounds__(kThreads) xchg_reduce_kernel(SartK<T> k, XK<T> x, int it) {
+  cudaGridDependencySynchronize();  // K2x of this rank has completed
+  if (!sys_on(k.state, 0)) return;
+  __shared__ int go;
+  const long long e = x.local[0] + it;
+  if (threadIdx.x == 0) {
+    if (x.inline_signal && blockIdx.x == 0) signal_all(x, x.off_done);
+    go = wait_geq(xdone(x, x.me), static_cast<unsigned long long>(x.G) * (e + 1), x.local + 2);
+  }
+  __syncthreads();
+  if (!go) return;
+  const bool stop = sqrt(xr2_sum(x, e)) <= k.tol * k.pnorm[0];
+  if (!stop) {
+    const long long j0 = x.me * x.own, j1 = min(j0 + x.own, x.cols);
+    const T* src = xrecv(x, x.me);
+    const T* xl = xrep(x, x.me);
+    const T* ci = k.s[0].cinv;
+    bool bad = false;
+    for (long long j = j0 + blockIdx.x * (long long)kThreads + threadIdx.x; j < j1;
+         j += (long long)gridDim.x * kThreads) {
+      T s = ld_sys(src + j);
+      for (int g = 1; g < x.G; ++g) s += ld_sys(src + g * x.cols + j);
+      const T xn = upd(ld_sys(xl + j), k.relax, s, ci[j]);
+      for (int r = 0; r < x.G; ++r) xrep(x, r)[j] = xn;  // local + NVLink stores
+      bad |= !isfinite(static_cast<double>(xn));
+    }
+    if (bad) {
+      for (int r = 0; r < x.G; ++r) atomicCAS_system(xdflag(x, r), 0, it + 1);
+    }
+  }
+}
+
+// Emulated group: the announcements the kernels make inline on real ranks,
+// as separate launches issued for every rank before any rank's next waiting
+// kernel (kind 0: before K1x, 1: before the reduce, 2: before the final kernel).
+template <class T>
+__global__ void xchg_announce_kernel(SartK<T> k, XK<T> x, int it, int kind) {
+  if (threadIdx.x != 0) return;
+  if (kind == 0 && it > 0 && x.local[1] == it) signal_all(x, x.off_xready);
+  if (kind == 1 && sys_on(k.state, 0)) signal_all(x, x.off_done);
+  if (kind == 2 && x.local[1] > 0 && x.local[1] == k.max_iters) signal_all(x, x.off_xready);
+}
+
+// After the last pass: wait for the final iteration's x, settle its residual /
+// stop state, advance the epoch base by the iterations run.
+template <class T>
+__global__ void xchg_final_kernel(SartK<T> k, XK<T> x) {
+  if (threadIdx.x != 0) return;
+  volatile int* st = k.state;
+  const long long base = x.local[0], L = x.local[1];
+  // the last reduce is announced here when no K1x followed it
+  if (x.inline_signal && L > 0 && L == k.max_iters) signal_all(x, x.off_xready);
+  if (!wait_geq(xready(x, x.me), xready_target(x, base + L), x.local + 2)) return;
+  if (L > 0 && st[0] == 0 && st[2] == 0) {
+    const int d = ld_sys(xdflag(x, x.me));
+    if (d != 0) {
+      st[2] = d;
+    } else {
+      const double res = sqrt(xr2_sum(x, base + L - 1));
+      k.history[L - 1] = res;
+      if (res <= k.tol * k.pnorm[0]) {
+        st[0] = 1;
+        st[1] = static_cast<int>(L - 1);
+      }
+    }
+  }
+  x.local[0] = base + L;
+  x.local[1] = 0;
+}
+
 template <class T>
 __global__ void inv_kernel(const double* sums, T* inv, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -1711,9 +2057,10 @@ SartK<T> make_args(Plan& P) {
   k.epb = P.eptr_b.get();
   k.eib = P.eidx_b.get();
   k.evb = reinterpret_cast<const T*>(P.ev2_b.get());
-  if (P.sharded) {
+  if (P.sharded && !P.px) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
+  if (P.px) k.s[0].x = reinterpret_cast<T*>(static_cast<char*>(P.px->region) + P.px->off_x);
   if (P.while_capture) {
     k.iter = P.iter_dev.get();
     k.cond = P.cond;
@@ -1951,9 +2298,98 @@ int occupancy_pair_blocks(Plan& P, bool fwd) {
 }
 
 template <class T>
+XK<T> make_xargs(const Plan& P) {
+  const PeerExchange& X = *P.px;
+  XK<T> x{};
+  x.peers = X.peers.get();
+  x.G = X.G;
+  x.me = X.me;
+  x.cols = X.cols;
+  x.own = X.own;
+  x.rgrid = X.rgrid;
+  x.off_recv = X.off_recv;
+  x.off_x = X.off_x;
+  x.off_r2 = X.off_r2;
+  x.off_done = X.off_done;
+  x.off_xready = X.off_xready;
+  x.off_dflag = X.off_dflag;
+  x.local = X.local.get();
+  x.inline_signal = X.emulated ? 0 : 1;
+  return x;
+}
+
+template <class T>
+using XchgFn = void (*)(SartK<T>, XK<T>, int);
+
+template <class T>
+XchgFn<T> xchg_kernel(const Plan& P, bool fwd) {
+  const int vs = fwd ? P.vs_fwd : P.vs_back;
+  const int uf = fwd ? P.uf_fwd : P.uf_back;
+  const bool u16 = fwd ? P.c16f : P.c16b;
+#define SSB_X(V, U)                                                                           \
+  if (vs == V && uf == U) {                                                                   \
+    if (u16) return fwd ? sart_fwd_xchg_kernel<T, V, U, true> : sart_back_xchg_kernel<T, V, U, true>; \
+    return fwd ? sart_fwd_xchg_kernel<T, V, U, false> : sart_back_xchg_kernel<T, V, U, false>; \
+  }
+  SSB_X(4, 2) SSB_X(8, 2) SSB_X(16, 2) SSB_X(32, 2)
+  SSB_X(4, 4) SSB_X(8, 4) SSB_X(16, 4) SSB_X(32, 4)
+#undef SSB_X
+  fail("plan: unsupported peer-exchange kernel shape");
+  return nullptr;
+}
+
+// phase: K1x (fwd), else K2x then (with_reduce) the owner-side reduce; an
+// emulated group issues every rank's K2x before any rank's reduce
+template <class T>
+void launch_xchg(Plan& P, const SartK<T>& k, int it, bool fwd, bool with_reduce = true,
+                 bool with_back = true) {
+  const XK<T> x = make_xargs<T>(P);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(fwd ? P.fwd_blocks : P.back_blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = P.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (!with_back) {
+    cfg.gridDim = dim3(P.px->rgrid);
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_reduce_kernel<T>, k, x, it));
+    P.ctx->check_launch("xchg_reduce_kernel");
+    return;
+  }
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_kernel<T>(P, fwd), k, x, it));
+  P.ctx->check_launch(fwd ? "sart_fwd_xchg_kernel" : "sart_back_xchg_kernel");
+  if (fwd || !with_reduce) return;
+  cfg.gridDim = dim3(P.px->rgrid);  // owner-side reduce + push of x
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_reduce_kernel<T>, k, x, it));
+  P.ctx->check_launch("xchg_reduce_kernel");
+}
+
+template <class T>
+void launch_announce(Plan& P, int it, int kind) {
+  xchg_announce_kernel<T><<<1, 32, 0, P.ctx->stream>>>(make_args<T>(P), make_xargs<T>(P), it,
+                                                       kind);
+  P.ctx->check_launch("xchg_announce_kernel");
+}
+
+template <class T>
+void launch_xchg_final(Plan& P) {
+  const SartK<T> k = make_args<T>(P);
+  xchg_final_kernel<T><<<1, 32, 0, P.ctx->stream>>>(k, make_xargs<T>(P));
+  P.ctx->check_launch("xchg_final_kernel");
+}
+
+template <class T>
 void do_iterations(Plan& P, int first, int count) {
   const SartK<T> k = make_args<T>(P);
   for (int it = first; it < first + count; ++it) {
+    if (P.px) {  // K1x over local rows, K2x with the fused peer exchange
+      launch_xchg<T>(P, k, it, true);
+      launch_xchg<T>(P, k, it, false);
+      continue;
+    }
     if (P.sharded) {
       // K1 over local rows, fixed-order ||r_g||^2, K2 partial back-projection,
       // all-reduce [bp | r2], identical update on every rank.
@@ -1998,6 +2434,7 @@ Plan::~Plan() {
   if (graph) cudaGraphExecDestroy(graph);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  delete px;
   delete own;
   delete pair_own[0];
   delete pair_own[1];
@@ -2008,8 +2445,15 @@ void Plan::enqueue_reset() {
     SSB_CUDA(cudaMemsetAsync(x[s].get(), 0, cols[s] * nrhs * tsize(), ctx->stream));
   }
   if (paired) SSB_CUDA(cudaMemsetAsync(xx.get(), 0, 2 * cols[0] * tsize(), ctx->stream));
+  if (px) {  // own replica and divergence flag only: peers never touch them
+    // before this rank's first arrival of the solve (see sart.cu peer exchange)
+    char* r = static_cast<char*>(px->region);
+    SSB_CUDA(cudaMemsetAsync(r + px->off_x, 0, cols[0] * tsize(), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(r + px->off_dflag, 0, sizeof(int), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(px->local.get() + 1, 0, sizeof(long long), ctx->stream));
+  }
   SSB_CUDA(cudaMemsetAsync(state.get(), 0, state.size() * sizeof(int), ctx->stream));
-  SSB_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
+  SSB_CUDA(cudaMemsetAsync(ticket.get(), 0, 2 * sizeof(unsigned), ctx->stream));
 }
 
 void Plan::enqueue_iterations(int first, int count) {
@@ -2018,6 +2462,13 @@ void Plan::enqueue_iterations(int first, int count) {
 }
 
 void Plan::enqueue_epilogue() {
+  if (px) {  // settle the last iteration, then the replica is the solution
+    if (dtype == SS_F32) launch_xchg_final<float>(*this);
+    else launch_xchg_final<double>(*this);
+    SSB_CUDA(cudaMemcpyAsync(x[0].get(), static_cast<char*>(px->region) + px->off_x,
+                             cols[0] * tsize(), cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
   if (!paired) return;
   const int g = grid1(ctx, cols[0]);
   if (dtype == SS_F32) {
@@ -2036,7 +2487,9 @@ void Plan::enqueue_epilogue() {
 constexpr int kPassesPerBody = 8;
 
 void Plan::build_graph() {
-  if (graph || sharded) return;  // NCCL calls stay out of the captured graph
+  // NCCL calls stay out of the captured graph; a peer-exchange plan is captured
+  // when the pass count is fixed (an emulated group launches rank by rank)
+  if (graph || (sharded && !(px && !px->emulated && !(opts.tol > 0.0)))) return;
   if (!(opts.tol > 0.0)) {
     // fixed iteration count (tol = 0 can never stop early): every pass
     // unrolled into the graph, the cheapest replay (a WHILE node's per-pass
@@ -2112,10 +2565,12 @@ void Plan::build_graph() {
 }
 
 void Plan::launch() {
+  if (px && px->emulated) fail("plan: an emulated exchange rank runs through ss_plan_group_run");
+  group_ms = -1.0f;
   SSB_CUDA(cudaEventRecord(ev0, ctx->stream));
   if (graph) {
     SSB_CUDA(cudaGraphLaunch(graph, ctx->stream));
-    ctx->launches += static_cast<std::int64_t>(2) * opts.max_iters + (paired ? 1 : 0);
+    ctx->launches += static_cast<std::int64_t>(px ? 3 : 2) * opts.max_iters + (paired || px ? 1 : 0);
   } else {
     enqueue_reset();
     enqueue_iterations(0, opts.max_iters);
@@ -2129,8 +2584,17 @@ void Plan::finish(ss_solve_report* rep) {
   if (!launched) fail("plan: finish without launch");
   SSB_CUDA(cudaEventSynchronize(ev1));
   SSB_CUDA(cudaEventElapsedTime(&last_ms, ev0, ev1));
+  if (group_ms >= 0.0f) last_ms = group_ms;  // emulated group: one clock for all ranks
   std::vector<int> st(state.size());
   ctx->copy(st.data(), state.get(), st.size() * sizeof(int));
+  if (px) {
+    long long loc[3];
+    ctx->copy(loc, px->local.get(), sizeof loc);
+    if (loc[2] != 0) {
+      fail("sart_solve: peer exchange timed out (a rank of the sharded system stopped "
+           "responding)", SS_ERR_CUDA);
+    }
+  }
   int iters = 0;
   for (int q = 0; q < nsys * nrhs; ++q) {
     if (st[4 * q + 2] != 0) {
@@ -2173,7 +2637,10 @@ void Plan::finish_rhs(int which) {
         reinterpret_cast<const double*>(p[which].get()), rows[which], nrhs, pn);
   }
   ctx->check_launch("pnorm_kernel");
-  if (sharded) {
+  if (sharded && px && px->emulated) {
+    // emulated ranks: run_group combines the ranks' local ||p_g||
+    ctx->copy(&pn_local, pn, sizeof(double));
+  } else if (sharded) {
     // ||p||^2 = sum over ranks of the local ||p_g||^2
     square_kernel<<<1, 32, 0, ctx->stream>>>(pn, nrhs);
     ctx->check_launch("square_kernel");
@@ -2300,14 +2767,32 @@ void Plan::recombine(double* f) {
 }
 
 void Plan::profile(int iters, float* fwd_ms, float* back_ms) {
+  if (px && px->emulated) fail("plan: an emulated exchange rank runs through ss_plan_group_run");
   cudaEvent_t e[3];
   for (auto& q : e) SSB_CUDA(cudaEventCreate(&q));
   float tf = 0.f, tb = 0.f;
   enqueue_reset();
   for (int it = 0; it < iters; ++it) {
     const int i = it % std::max(1, opts.max_iters);
+    if (px && i == 0 && it > 0) {  // exchange epochs: whole solves only
+      enqueue_epilogue();
+      enqueue_reset();
+    }
     SSB_CUDA(cudaEventRecord(e[0], ctx->stream));
-    if (dtype == SS_F32) {
+    if (px) {  // K1x | K2x + reduce (the exchange's share lands in "back")
+      if (dtype == SS_F32) {
+        const SartK<float> k = make_args<float>(*this);
+        launch_xchg<float>(*this, k, i, true);
+        SSB_CUDA(cudaEventRecord(e[1], ctx->stream));
+        launch_xchg<float>(*this, k, i, false);
+      } else {
+        const SartK<double> k = make_args<double>(*this);
+        launch_xchg<double>(*this, k, i, true);
+        SSB_CUDA(cudaEventRecord(e[1], ctx->stream));
+        launch_xchg<double>(*this, k, i, false);
+      }
+      --ctx->launches;  // launch_xchg counted its own; check_launch below adds one
+    } else if (dtype == SS_F32) {
       const SartK<float> k = make_args<float>(*this);
       launch_fwd<float>(*this, k, i);
       ctx->check_launch("sart_fwd_kernel");
@@ -2328,6 +2813,10 @@ void Plan::profile(int iters, float* fwd_ms, float* back_ms) {
     SSB_CUDA(cudaEventElapsedTime(&b, e[1], e[2]));
     tf += a;
     tb += b;
+  }
+  if (px) {
+    enqueue_epilogue();
+    ctx->sync();
   }
   for (auto& q : e) cudaEventDestroy(q);
   *fwd_ms = tf;
@@ -2440,10 +2929,10 @@ void alloc_common(Plan& P) {
   SSB_CUDA(cudaMemsetAsync(P.pnorm.get(), 0, nsr * sizeof(double), P.ctx->stream));
   P.history.alloc(static_cast<std::size_t>(nsr) * (P.opts.max_iters + 1));
   P.state.alloc(4 * nsr);
-  P.ticket.alloc(1);
+  P.ticket.alloc(2);  // K1 last block, K2x last block
   P.iter_dev.alloc(2);  // WHILE loop: pass counter, loop-over flag
   SSB_CUDA(cudaMemsetAsync(P.state.get(), 0, 4 * nsr * sizeof(int), P.ctx->stream));
-  SSB_CUDA(cudaMemsetAsync(P.ticket.get(), 0, sizeof(unsigned), P.ctx->stream));
+  SSB_CUDA(cudaMemsetAsync(P.ticket.get(), 0, 2 * sizeof(unsigned), P.ctx->stream));
   SSB_CUDA(cudaEventCreate(&P.ev0));
   SSB_CUDA(cudaEventCreate(&P.ev1));
 }
@@ -2808,6 +3297,14 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   return P.release();
 }
 
+void exchange_owned_columns(std::int64_t cols, int parts, int rank, std::int64_t* begin,
+                            std::int64_t* end) {
+  if (parts < 1 || rank < 0 || rank >= parts || cols < 0) fail("exchange: bad rank / parts");
+  const std::int64_t own = (cols + parts - 1) / parts;  // as setup_exchange
+  *begin = std::min(cols, rank * own);
+  *end = std::min(cols, *begin + own);
+}
+
 void partition_rows(const int* rowptr, std::int64_t rows, int parts, std::int64_t* bounds) {
   if (parts < 1) fail("partition_rows: parts must be >= 1");
   const double total = static_cast<double>(rowptr[rows]) + static_cast<double>(rows);
@@ -2825,9 +3322,174 @@ void partition_rows(const int* rowptr, std::int64_t rows, int parts, std::int64_
 // Row-sharded plan: keeps rows [rb, re) of the folded system `a` (all its
 // columns). Column normalisers come from the full matrix (every rank holds
 // the same column sums), row normalisers from the local rows.
+namespace {
+
+std::size_t align256(std::size_t v) { return (v + 255) & ~static_cast<std::size_t>(255); }
+
+// Exchange region of a peer-exchange rank (layout in plan.hpp). Ownership and
+// the reduce grid depend only on the column count, G and the SM count, so
+// every rank derives the same ones.
+void setup_exchange(Plan& P, int G, int me, bool emulated) {
+  Context* ctx = P.ctx;
+  auto X = std::make_unique<PeerExchange>();
+  X->G = G;
+  X->me = me;
+  X->emulated = emulated;
+  X->cols = P.cols[0];
+  X->own = (X->cols + G - 1) / G;  // owner of column j: j / own (exchange_owned_columns)
+  X->rgrid = 2 * ctx->sm_count;
+  const std::size_t tb = P.tsize();
+  X->off_recv = 0;
+  X->off_x = align256(static_cast<std::size_t>(G) * X->cols * tb + kSlackBytes);
+  X->off_r2 = align256(X->off_x + X->cols * tb + kSlackBytes);
+  X->off_done = align256(X->off_r2 + 2 * G * sizeof(double));
+  X->off_xready = X->off_done + 64;
+  X->off_dflag = X->off_xready + 64;
+  X->bytes = align256(X->off_dflag + 64);
+  // plain cudaMalloc: pool (cudaMallocAsync) memory cannot be exported over IPC
+  SSB_CUDA(cudaMalloc(&X->region, X->bytes));
+  SSB_CUDA(cudaMemsetAsync(X->region, 0, X->bytes, ctx->stream));
+  X->local.alloc(3);
+  SSB_CUDA(cudaMemsetAsync(X->local.get(), 0, 3 * sizeof(long long), ctx->stream));
+  X->peers.alloc(G);
+  std::vector<char*> bases(G, nullptr);
+  bases[me] = static_cast<char*>(X->region);
+  if (!emulated && G > 1) {
+    // all-gather the IPC handles: each rank fills its slot of a zeroed table,
+    // one byte-wise sum over the communicator. Every rank zeroed its region
+    // before joining, so a mapped peer region is ready to use.
+    cudaIpcMemHandle_t h;
+    SSB_CUDA(cudaIpcGetMemHandle(&h, X->region));
+    std::vector<unsigned char> tab(static_cast<std::size_t>(G) * sizeof h, 0);
+    std::memcpy(tab.data() + me * sizeof h, &h, sizeof h);
+    DBuf<unsigned char> dt(tab.size());
+    SSB_CUDA(cudaMemcpyAsync(dt.get(), tab.data(), tab.size(), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    nccl_check(nccl().AllReduce(dt.get(), dt.get(), tab.size(), ncclUint8, ncclSum,
+                                static_cast<ncclComm_t>(ctx->comm), ctx->stream),
+               "ncclAllReduce(ipc handles)");
+    ctx->copy(tab.data(), dt.get(), tab.size());
+    for (int r = 0; r < G; ++r) {
+      if (r == me) continue;
+      cudaIpcMemHandle_t hr;
+      std::memcpy(&hr, tab.data() + r * sizeof hr, sizeof hr);
+      void* q = nullptr;
+      SSB_CUDA(cudaIpcOpenMemHandle(&q, hr, cudaIpcMemLazyEnablePeerAccess));
+      X->opened.push_back(q);
+      bases[r] = static_cast<char*>(q);
+    }
+  }
+  if (!emulated) {
+    SSB_CUDA(cudaMemcpyAsync(X->peers.get(), bases.data(), G * sizeof(char*),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  }
+  ctx->sync();
+  P.px = X.release();
+}
+
+}  // namespace
+
+PeerExchange::~PeerExchange() {
+  for (void* q : opened) cudaIpcCloseMemHandle(q);
+  if (region) cudaFree(region);
+}
+
+void link_group(Plan* const* plans, int parts) {
+  std::vector<char*> bases(parts);
+  for (int g = 0; g < parts; ++g) {
+    if (!plans[g]->px || !plans[g]->px->emulated || plans[g]->px->G != parts ||
+        plans[g]->px->me != g) {
+      fail("plan: not rank " + std::to_string(g) + " of an emulated group of " +
+           std::to_string(parts));
+    }
+    bases[g] = static_cast<char*>(plans[g]->px->region);
+  }
+  for (int g = 0; g < parts; ++g) {
+    Context* ctx = plans[g]->ctx;
+    SSB_CUDA(cudaMemcpyAsync(plans[g]->px->peers.get(), bases.data(), parts * sizeof(char*),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+  }
+}
+
+void run_group(Plan* const* plans, int parts) {
+  if (parts < 1) fail("plan: empty group");
+  Plan& P0 = *plans[0];
+  for (int g = 0; g < parts; ++g) {
+    Plan& P = *plans[g];
+    if (!P.px || !P.px->emulated || P.ctx != P0.ctx || P.opts.max_iters != P0.opts.max_iters) {
+      fail("plan: group plans must be one emulated exchange on one context");
+    }
+  }
+  Context* ctx = P0.ctx;
+  // ||p||^2 = sum of the ranks' local ||p_g||^2, in rank order
+  double sq = 0.0;
+  for (int g = 0; g < parts; ++g) {
+    const double v = plans[g]->pn_local;
+    if (v < 0.0) fail("plan: group rank " + std::to_string(g) + " has no rhs");
+    sq += v * v;
+  }
+  const double pn = std::sqrt(sq);
+  for (int g = 0; g < parts; ++g) {
+    SSB_CUDA(cudaMemcpyAsync(plans[g]->pnorm.get(), &pn, sizeof pn, cudaMemcpyHostToDevice,
+                             ctx->stream));
+  }
+  ctx->sync();
+  for (int g = 0; g < parts; ++g) plans[g]->enqueue_reset();
+  SSB_CUDA(cudaEventRecord(P0.ev0, ctx->stream));
+  // rank order inside each phase (K1x, K2x, reduce): every wait a kernel
+  // performs is on launches issued, and completed, before it
+  auto announce = [&](int it, int kind) {
+    for (int g = 0; g < parts; ++g) {
+      if (plans[g]->dtype == SS_F32) launch_announce<float>(*plans[g], it, kind);
+      else launch_announce<double>(*plans[g], it, kind);
+    }
+  };
+  for (int it = 0; it < P0.opts.max_iters; ++it) {
+    announce(it, 0);
+    for (int g = 0; g < parts; ++g) {
+      Plan& P = *plans[g];
+      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, true);
+      else launch_xchg<double>(P, make_args<double>(P), it, true);
+    }
+    for (int g = 0; g < parts; ++g) {
+      Plan& P = *plans[g];
+      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, false, false);
+      else launch_xchg<double>(P, make_args<double>(P), it, false, false);
+    }
+    announce(it, 1);
+    for (int g = 0; g < parts; ++g) {
+      Plan& P = *plans[g];
+      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, false, true, false);
+      else launch_xchg<double>(P, make_args<double>(P), it, false, true, false);
+    }
+  }
+  announce(P0.opts.max_iters, 2);
+  for (int g = 0; g < parts; ++g) plans[g]->enqueue_epilogue();
+  SSB_CUDA(cudaEventRecord(P0.ev1, ctx->stream));
+  SSB_CUDA(cudaEventSynchronize(P0.ev1));
+  float ms = 0.0f;
+  SSB_CUDA(cudaEventElapsedTime(&ms, P0.ev0, P0.ev1));
+  for (int g = 0; g < parts; ++g) {
+    Plan& P = *plans[g];
+    SSB_CUDA(cudaEventRecord(P.ev0, ctx->stream));  // finish() re-reads the pair
+    SSB_CUDA(cudaEventRecord(P.ev1, ctx->stream));
+    P.launched = true;
+  }
+  ctx->sync();
+  for (int g = 0; g < parts; ++g) plans[g]->group_ms = ms;
+
+}
+
 Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t re,
-                        const ss_solve_options& o) {
-  if (!ctx->comm) fail("plan: context has no NCCL communicator");
+                        const ss_solve_options& o, int exchange, int emul_parts, int emul_rank) {
+  if (exchange != SS_XCHG_NCCL && exchange != SS_XCHG_PEER) fail("plan: unknown exchange");
+  if (emul_parts > 0) {
+    if (exchange != SS_XCHG_PEER) fail("plan: only the peer exchange can be emulated");
+    if (emul_rank < 0 || emul_rank >= emul_parts) fail("plan: emulated rank out of range");
+  } else if (!ctx->comm) {
+    fail("plan: context has no NCCL communicator");
+  }
   if (rb < 0 || re > a->rows || rb > re) fail("plan: row range out of bounds");
   if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
   if (o.max_iters < 1) fail("sart_solve: max_iters must be >= 1");
@@ -2870,7 +3532,7 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
     P->back_blocks = occupancy_blocks<double>(*P, false);
   }
   alloc_common(*P);
-  P->bp.alloc((a->cols + 1) * P->tsize());
+  if (exchange == SS_XCHG_NCCL) P->bp.alloc((a->cols + 1) * P->tsize());
   // normalisers: rows from the local block, columns from the full matrix
   DBuf<double> rs_full(a->rows), cs_full(a->cols);
   // `a` may live on another context (stream): order the buffers' allocation
@@ -2896,8 +3558,13 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   if (!(max_dev(ctx, rs_full.get(), a->rows) > 0.0)) fail("sart_solve: matrix has no nonzero rows");
   P->tiled = env_int("SSB_TILED", 1) != 0;  // the row block on the tiled streams
   P->c16f = P->c16b = env_int("SSB_U16", 1) != 0;
+  if (exchange == SS_XCHG_PEER) P->tiled = true;  // the exchange kernels are tiled-only
   build_single(*P);
   if (P->tiled) size_single_grid(*P);
+  if (exchange == SS_XCHG_PEER) {
+    if (emul_parts > 0) setup_exchange(*P, emul_parts, emul_rank, true);
+    else setup_exchange(*P, ctx->nranks, ctx->rank, false);
+  }
   ctx->sync();
   return P.release();
 }

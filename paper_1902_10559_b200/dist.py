@@ -2,9 +2,10 @@
 
 world == 2: rank r solves folded system r; no data-path collective.
 world >= 4 (even): ranks [0, W/2) hold A1, ranks [W/2, W) hold A2; each
-group splits its system into nnz-balanced row blocks and all-reduces the
-N/2-length back-projection (+ the ||r||^2 slot) once per iteration over NCCL
-inside the C++ library. torch.distributed only carries the rendezvous (the
+group splits its system into nnz-balanced row blocks and combines the
+N/2-length back-projection once per iteration through the fused peer-memory
+exchange (CUDA IPC regions, NVLink stores from the back-projection kernel; the
+NCCL all-reduce variant stays selectable as the baseline). torch.distributed only carries the rendezvous (the
 128-byte NCCL unique id, over a gloo group) and the barrier.
 """
 from __future__ import annotations
@@ -19,7 +20,9 @@ def group_layout(rank: int, world: int):
     return sysid, rank % half, half, list(range(sysid * half, (sysid + 1) * half))
 
 
-def make_sharded_plan(P, ctx, split, opts, rank: int, world: int):
+def make_sharded_plan(P, ctx, split, opts, rank: int, world: int, exchange: str = "peer"):
+    """exchange "peer": the fused peer-memory exchange (SS_XCHG_PEER, the
+    product path); "nccl": K2 partials + ncclAllReduce (the baseline)."""
     import torch.distributed as tdist
 
     sysid, grank, half, members = group_layout(rank, world)
@@ -33,6 +36,6 @@ def make_sharded_plan(P, ctx, split, opts, rank: int, world: int):
     ptr = a.to_csr()[0]
     bounds = P.symsplit.partition_rows(ptr, half)
     rb, re = int(bounds[grank]), int(bounds[grank + 1])
-    plan = P.symsplit.ShardedSartPlan(ctx, a, rb, re, opts)
+    plan = P.symsplit.ShardedSartPlan(ctx, a, rb, re, opts, exchange=exchange)
     plan.set_rhs(0, p[rb:re])
     return plan

@@ -740,12 +740,26 @@ def partition_rows(rowptr, parts: int):
     return bounds
 
 
+XCHG_NCCL, XCHG_PEER = 0, 1  # SS_XCHG_* of symsplit_b200.h
+
+
+def exchange_owned_columns(cols: int, parts: int, rank: int):
+    """Columns [begin, end) rank `rank` reduces and pushes in the peer
+    exchange (host logic, no GPU)."""
+    b, e = N.i64(), N.i64()
+    _check(_lib().ss_exchange_owned_columns(cols, parts, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
 class ShardedSartPlan(SartPlan):
-    """Rows [row_begin, row_end) of one folded system on this rank; the
-    back-projection is all-reduced over the context's NCCL communicator."""
+    """Rows [row_begin, row_end) of one folded system on this rank. exchange
+    "nccl": the back-projection is all-reduced over the context's NCCL
+    communicator; "peer": the fused peer-memory exchange (K2 stores each
+    column chunk into its owner's buffer over NVLink, the last rank to arrive
+    reduces, updates and broadcasts x; no NCCL on the data path)."""
 
     def __init__(self, ctx: Context, a: Matrix, row_begin: int, row_end: int,
-                 opts: Optional[SolveOptions] = None):
+                 opts: Optional[SolveOptions] = None, exchange: str = "nccl"):
         self.opts = opts or SolveOptions()
         self.ctx = ctx
         self.nsys = 1
@@ -753,8 +767,63 @@ class ShardedSartPlan(SartPlan):
         self.a = (a, None)
         h = N.vp()
         o = self.opts._c()
-        _check(_lib().ss_plan_create_sharded(ctx.h, a.h, row_begin, row_end, C.byref(o),
-                                             C.byref(h)))
+        x = {"nccl": XCHG_NCCL, "peer": XCHG_PEER}[exchange]
+        _check(_lib().ss_plan_create_sharded_x(ctx.h, a.h, row_begin, row_end, C.byref(o), x,
+                                               C.byref(h)))
         self.h = h
         self.rows = row_end - row_begin
         self.cols = a.shape[1]
+
+
+class _GroupMember(SartPlan):
+    """One emulated rank of a ShardGroup (owns its ss_plan_t)."""
+
+    def __init__(self, ctx, a, h, rows, opts):
+        self.opts = opts
+        self.ctx = ctx
+        self.nsys = 1
+        self.nrhs = 1
+        self.a = (a, None)
+        self.h = h
+        self.rows = rows
+        self.cols = a.shape[1]
+
+
+class ShardGroup:
+    """One-device emulation of `parts` peer-exchange ranks of a row-sharded
+    system (ss_plan_create_sharded_group / ss_plan_group_run): the same
+    kernels, chunk ownership, arrival counters and rank-order reductions as
+    the multi-GPU path, with every rank's launches issued in rank order on one
+    stream. Used by the parity tests and the single-GPU exchange measurement."""
+
+    def __init__(self, a: Matrix, parts: int, opts: Optional[SolveOptions] = None,
+                 bounds=None):
+        self.opts = opts or SolveOptions()
+        self.parts = parts
+        if bounds is None:
+            bounds = partition_rows(a.to_csr()[0], parts)
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        hs = (N.vp * parts)()
+        o = self.opts._c()
+        _check(_lib().ss_plan_create_sharded_group(a.ctx.h, a.h, parts,
+                                                   self.bounds.ctypes.data_as(N.i64p),
+                                                   C.byref(o), hs))
+        self.hs = hs
+        self.ranks = [_GroupMember(a.ctx, a, N.vp(hs[g]),
+                                   int(self.bounds[g + 1] - self.bounds[g]), self.opts)
+                      for g in range(parts)]
+
+    def set_rhs(self, p):
+        p = _f64(p)
+        for g, r in enumerate(self.ranks):
+            r.set_rhs(0, p[self.bounds[g]:self.bounds[g + 1]])
+
+    def run(self):
+        _check(_lib().ss_plan_group_run(self.hs, self.parts))
+        return [r.finish() for r in self.ranks]
+
+    def solution(self, rank=0):
+        return self.ranks[rank].solution(0)
+
+    def history(self, rank=0):
+        return self.ranks[rank].history(0)

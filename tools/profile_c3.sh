@@ -11,3 +11,11 @@ for dir in fwd back; do
       -o gpurun_out/prof_pair_$dir $CMD > gpurun_out/ncu_full_$dir.log 2>&1
   tail -2 gpurun_out/ncu_full_$dir.log
 done
+# summarise on the box (gpurun_out/ must stay under 64 MiB to come back)
+python tools/launch_summary.py gpurun_out/launches_raw.csv gpurun_out/launches.csv \
+    gpurun_out/launch_summary.txt "$CMD" && rm -f gpurun_out/launches_raw.csv
+for dir in fwd back; do
+  ncu -i gpurun_out/prof_pair_$dir.ncu-rep --page raw --csv > gpurun_out/raw_$dir.csv 2>/dev/null
+  python tools/ncu_summary.py gpurun_out/raw_$dir.csv gpurun_out/ncu_$dir.json
+done
+du -sh gpurun_out/* | sort -h | tail -5
