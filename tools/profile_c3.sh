@@ -17,5 +17,6 @@ python tools/launch_summary.py gpurun_out/launches_raw.csv gpurun_out/launches.c
 for dir in fwd back; do
   ncu -i gpurun_out/prof_pair_$dir.ncu-rep --page raw --csv > gpurun_out/raw_$dir.csv 2>/dev/null
   python tools/ncu_summary.py gpurun_out/raw_$dir.csv gpurun_out/ncu_$dir.json
+  rm -f gpurun_out/prof_pair_$dir.ncu-rep  # 35 MB each: summarised above
 done
 du -sh gpurun_out/* | sort -h | tail -5
