@@ -3033,7 +3033,6 @@ bool build_tiled_streams(Plan& P, int w) {
     const int* ptr = fwd ? m.rowptr.get() : m.colptr.get();
     const int* idx = fwd ? m.colidx.get() : m.rowidx.get();
     const long long n = fwd ? rows : cols;
-    const int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
     const DBuf<int>& tptr = fwd ? P.tptr_f : P.tptr_b;
     const std::int64_t tn = fwd ? P.tnnz_f : P.tnnz_b;
     DBuf<char>& vbuf = fwd ? P.rv2 : P.cv2;
@@ -3041,14 +3040,31 @@ bool build_tiled_streams(Plan& P, int w) {
     bool& u16 = fwd ? P.c16f : P.c16b;
     bool& mir = fwd ? P.mir_f : P.mir_b;
     mir = mir && w == 2;
+    int tile = 4 * (fwd ? P.vs_fwd : P.vs_back);
     if (u16) {  // 16 bits fit every tile? (decided before any stream buffer exists)
-      DBuf<int> of(1);
-      SSB_CUDA(cudaMemsetAsync(of.get(), 0, sizeof(int), P.ctx->stream));
-      tile_overflow_kernel<<<grid1(P.ctx, n), 256, 0, P.ctx->stream>>>(ptr, idx, n, tile, of.get());
-      P.ctx->check_launch("tile_overflow_kernel");
-      int bad = 0;
-      P.ctx->copy(&bad, of.get(), sizeof(int));
-      if (bad) u16 = false;
+      // a paired plan first narrows its lane groups (smaller tiles span fewer
+      // indices): config 5's K2 fits at 4 lanes, 0.83 -> 0.71 ms vs int32 at 8
+      const bool narrow = w == 2 && std::getenv(fwd ? "SSB_VS_FWD" : "SSB_VS_BACK") == nullptr;
+      const int vs0 = fwd ? P.vs_fwd : P.vs_back;
+      for (;;) {
+        DBuf<int> of(1);
+        SSB_CUDA(cudaMemsetAsync(of.get(), 0, sizeof(int), P.ctx->stream));
+        tile_overflow_kernel<<<grid1(P.ctx, n), 256, 0, P.ctx->stream>>>(ptr, idx, n, tile,
+                                                                          of.get());
+        P.ctx->check_launch("tile_overflow_kernel");
+        int bad = 0;
+        P.ctx->copy(&bad, of.get(), sizeof(int));
+        if (!bad) break;
+        int& vs = fwd ? P.vs_fwd : P.vs_back;
+        if (!narrow || vs <= 4) {  // no width fits: int32 indices at the picked width
+          u16 = false;
+          vs = vs0;
+          tile = 4 * vs;
+          break;
+        }
+        vs /= 2;
+        tile = 4 * vs;
+      }
     }
     if (u16 || mir) {  // per-tile data: first tile of every vector
       DBuf<int>& tfirst = fwd ? P.tfirst_f : P.tfirst_b;
@@ -3269,6 +3285,16 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   if (P->paired) {
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);
+    // the final layout (16-bit fit, lane groups) picks the kernels: size their grids
+    P->fwd_blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(
+        occupancy_pair_blocks(*P, true),
+        (static_cast<long long>(P->rows[0]) * P->vs_fwd + kThreads - 1) / kThreads)));
+    P->back_blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(
+        occupancy_pair_blocks(*P, false),
+        (static_cast<long long>(P->cols[0]) * P->vs_back + kThreads - 1) / kThreads)));
+    if (static_cast<std::size_t>(P->fwd_blocks) * P->nsys * P->nrhs > P->partial.size()) {
+      P->partial.alloc(static_cast<std::size_t>(P->fwd_blocks) * P->nsys * P->nrhs);
+    }
     // fp32 streams of 1-16x the L2 carry the evict-first hint (see lds):
     // measured +2.5% at 5.3x (config 3), -2.6% at 92x (config 5)
     std::int64_t fb = 0, bb = 0;

@@ -386,6 +386,41 @@ def test_paired_tiled_layouts_match_oracle(span, per_row, monkeypatch):
     assert rel_err(got32.f, ref.f) <= TOL_F32
 
 
+def test_paired_lane_groups_narrow_to_fit_16bit(monkeypatch):
+    """Rows of ~110 entries ~2.6K columns apart: 32-entry tiles (8-lane groups)
+    span > 65535 columns, 16-entry tiles fit. The paired plan narrows its lane
+    groups to keep 16-bit offsets (config 5's K2 case) and still matches the
+    oracle; pinning the lane groups at 8 falls back to int32 indices."""
+    rng = np.random.default_rng(31)
+    mh, nh = 96, 300000
+    m, n = 2 * mh, 2 * nh
+    r, c, v = [], [], []
+    for i in range(mh):
+        cols = int(rng.integers(0, 14000)) + np.arange(110) * 2600 + rng.integers(0, 50, 110)
+        vals = rng.uniform(0.1, 1.0, len(cols))
+        r += [i] * len(cols) + [m - 1 - i] * len(cols)
+        c += list(cols) + list(n - 1 - cols)
+        v += list(vals) + list(vals)
+    r, c, v = np.array(r), np.array(c), np.array(v)
+    p = rng.uniform(0.5, 1.5, m)
+    a = P.Matrix.from_triplets(m, n, r, c, v)
+    sys_ = P.CentroSystem(a, p, 0.0)
+    split = P.split_system(sys_)
+    monkeypatch.delenv("SSB_VS_FWD", raising=False)
+    d = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0)).describe()
+    assert d["vs_fwd"] == 4 and d["fwd_kernel"].endswith(", 4>")
+    got = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
+    got32 = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0, dtype="f32"))
+    monkeypatch.setenv("SSB_VS_FWD", "8")
+    d8 = P.SartPlan(split.a1, split.a2, P.SolveOptions(max_iters=12, tol=0.0)).describe()
+    assert d8["vs_fwd"] == 8 and d8["fwd_kernel"].endswith(", 6>")
+    wide = P.solve_split(sys_, P.SolveOptions(max_iters=12, tol=0.0))
+    ref = O.solve_split(O.Matrix.triplets(m, n, r, c, v), p, 0.0, 12, 0.0, 1.0)
+    assert rel_err(got.f, ref.f) <= TOL_F64
+    assert rel_err(wide.f, ref.f) <= TOL_F64
+    assert rel_err(got32.f, ref.f) <= TOL_F32
+
+
 def _mirror_rich_centro(seed, mh, nh, per_row, frac):
     """Centrosymmetric system whose rows also meet the point mirror of a
     fraction `frac` of their columns with a different value: those buckets fold
