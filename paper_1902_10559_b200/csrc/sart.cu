@@ -3318,7 +3318,9 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   if (P->nsys == 1 && P->empty_rows[0]) fail("sart_solve: matrix has no nonzero rows");
   // a reusable plan replays one captured graph; a one-shot solve enqueues its
   // launches directly (the host stays ahead of the 2*max_iters kernels)
-  if (reusable) P->build_graph();
+  // SSB_GRAPH=0: direct launches (ncu lists graph-replayed K1 nodes of this
+  // loop incompletely, so launch lists are taken with it)
+  if (reusable && env_int("SSB_GRAPH", 1) != 0) P->build_graph();
   tr.mark("graph capture");
   return P.release();
 }

@@ -4,8 +4,11 @@
 mkdir -p gpurun_out
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain.log; exit 1; }
-ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --page raw \
+# direct launches for the list: ncu drops the K1 nodes of graph replays (measured)
+SSB_GRAPH=0 $CMD > gpurun_out/plain_nograph.log 2>&1 &&
+SSB_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --page raw \
     $CMD > gpurun_out/launches_raw.csv 2> gpurun_out/ncu_launch.err
+python tools/launch_runs.py gpurun_out/launches_raw.csv
 for dir in fwd back; do
   ncu --set full --clock-control none --import-source on -k regex:"sart_${dir}_pair" -s 20 -c 2 \
       -o gpurun_out/prof_pair_$dir $CMD > gpurun_out/ncu_full_$dir.log 2>&1
@@ -13,7 +16,7 @@ for dir in fwd back; do
 done
 # summarise on the box (gpurun_out/ must stay under 64 MiB to come back)
 python tools/launch_summary.py gpurun_out/launches_raw.csv gpurun_out/launches.csv \
-    gpurun_out/launch_summary.txt "$CMD" && rm -f gpurun_out/launches_raw.csv
+    gpurun_out/launch_summary.txt "SSB_GRAPH=0 $CMD" && rm -f gpurun_out/launches_raw.csv
 for dir in fwd back; do
   ncu -i gpurun_out/prof_pair_$dir.ncu-rep --page raw --csv > gpurun_out/raw_$dir.csv 2>/dev/null
   python tools/ncu_summary.py gpurun_out/raw_$dir.csv gpurun_out/ncu_$dir.json
