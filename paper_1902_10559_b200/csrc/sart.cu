@@ -233,7 +233,7 @@ __device__ __forceinline__ bool sys_on(const int* state, int idx) {
 // the reference's check-before-update stopping rule (solvers.cpp:180-182).
 __device__ void finish_norms(double* partial, int nblk, int nsr, const double* pnorm, double tol,
                              double* history, int hstride, int* state, int it) {
-  __shared__ double sh[1024];
+  __shared__ double sh[kThreads];  // every caller runs kThreads-thread CTAs
   for (int q = 0; q < nsr; ++q) {
     if (!sys_on(state, q)) continue;
     double s = 0.0;
