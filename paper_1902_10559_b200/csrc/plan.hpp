@@ -60,6 +60,8 @@ struct Plan {
   DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
   DBuf<char> rv2, cv2;    // paired: CSR / CSC values interleaved [nnz][2]
   DBuf<char> pe, cc;      // paired: {p1,p2,rinv1,rinv2} per row, {cinv1,cinv2} per column
+  int nband = 1;          // multi-RHS K1 passes over column bands
+  DBuf<int> band_ptr[2];  // per system [nband + 1][rows] positions inside the CSR rows
   // paired + tiled: rows/columns padded to 4 entries and permuted within tiles
   // of 4*VS entries so each gather instruction covers consecutive entries
   bool tiled = false;

@@ -47,6 +47,10 @@ struct SysK {
   const T* cinv;
   T* x;
   T* w;
+  // multi-RHS column band of this K1 pass: row i's entries [bb[i], be[i])
+  // (nullptr: the whole row, rp[i]..rp[i+1])
+  const int* bb;
+  const int* be;
 };
 
 template <class T>
@@ -1392,7 +1396,9 @@ __device__ __forceinline__ void multi_row_dot(const int* __restrict__ idx, const
 }
 
 template <class T, int V, int Q>
-__global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, int it) {
+__global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, int it, int band) {
+  // band: 0 = the whole row in one pass; with column bands 1 = first pass
+  // (w <- partial), 2 = middle (w += partial), 3 = last (r from w + partial)
   it = pass_index(k, it, true);
   if (loop_over(k)) return;
   extern __shared__ double mred[];  // [kWarps][nsys*S]
@@ -1422,8 +1428,32 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
 #pragma unroll
       for (int t = 0; t < V; ++t) acc[q][t] = T(0);
     }
-    const int beg = Sy.rp[i], end = Sy.rp[i + 1];
+    const int beg = Sy.bb ? Sy.bb[i] : Sy.rp[i], end = Sy.be ? Sy.be[i] : Sy.rp[i + 1];
     multi_row_dot<T, V, Q>(Sy.ci, Sy.rv, Sy.x, beg, end, lane, S, acc);
+    if (band == 1 || band == 2) {  // partial dot products of this column band
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+          const int sl = (q * 32 + lane) * V + t;
+          if (s ? onb[q][t] : ona[q][t]) {
+            const long long o = static_cast<long long>(i) * S + sl;
+            Sy.w[o] = band == 1 ? acc[q][t] : Sy.w[o] + acc[q][t];
+          }
+        }
+      }
+      continue;
+    }
+    if (band == 3) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+          const int sl = (q * 32 + lane) * V + t;
+          if (sl < S) acc[q][t] = Sy.w[static_cast<long long>(i) * S + sl] + acc[q][t];
+        }
+      }
+    }
     const T ri = Sy.rinv[i];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -1440,6 +1470,7 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
       }
     }
   }
+  if (band == 1 || band == 2) return;
   const int nsr = k.nsys * S;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -1905,6 +1936,28 @@ __global__ void xchg_final_kernel(SartK<T> k, XK<T> x) {
   x.local[1] = 0;
 }
 
+// Column-band boundaries inside every CSR row (columns ascending): out[b][i] =
+// first position of row i whose column is >= b*cols/nband (b = nband: row end).
+__global__ void band_ptr_kernel(const int* __restrict__ rp, const int* __restrict__ ci,
+                                long long rows, long long cols, int nband, int* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int beg = rp[i], end = rp[i + 1];
+    out[i] = beg;
+    out[static_cast<long long>(nband) * rows + i] = end;
+    for (int b = 1; b < nband; ++b) {
+      const long long c0 = cols * b / nband;
+      int lo = beg, hi = end;  // first position with ci >= c0
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < c0) lo = mid + 1;
+        else hi = mid;
+      }
+      out[static_cast<long long>(b) * rows + i] = lo;
+    }
+  }
+}
+
 template <class T>
 __global__ void inv_kernel(const double* sums, T* inv, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -2182,16 +2235,59 @@ void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
 // multi-RHS kernel: V consecutive slices per lane (vector loads; S % V == 0),
 // Q passes of 32*V slices
 template <class T>
-PairFn<T> multi_kernel(const Plan& P, bool fwd) {
+using MultiFwdFn = void (*)(SartK<T>, int, int);
+
+template <class T>
+PairFn<T> multi_back_kernel(const Plan& P) {
   const int S = P.nrhs;
   const int v = S % 4 == 0 && S >= 128 ? 4 : (S % 2 == 0 && S >= 64 ? 2 : 1);
   const int q = (S + 32 * v - 1) / (32 * v);
 #define SSB_MULTI(V, Q) \
-  if (v == V && q <= Q) return fwd ? sart_fwd_multi_kernel<T, V, Q> : sart_back_multi_kernel<T, V, Q>;
+  if (v == V && q <= Q) return sart_back_multi_kernel<T, V, Q>;
   SSB_MULTI(1, 1) SSB_MULTI(1, 2) SSB_MULTI(2, 1) SSB_MULTI(2, 2) SSB_MULTI(4, 1) SSB_MULTI(4, 2)
 #undef SSB_MULTI
   fail("plan: unsupported multi-RHS shape");
   return nullptr;
+}
+
+template <class T>
+MultiFwdFn<T> multi_fwd_kernel(const Plan& P) {
+  const int S = P.nrhs;
+  const int v = S % 4 == 0 && S >= 128 ? 4 : (S % 2 == 0 && S >= 64 ? 2 : 1);
+  const int q = (S + 32 * v - 1) / (32 * v);
+#define SSB_MULTI(V, Q) \
+  if (v == V && q <= Q) return sart_fwd_multi_kernel<T, V, Q>;
+  SSB_MULTI(1, 1) SSB_MULTI(1, 2) SSB_MULTI(2, 1) SSB_MULTI(2, 2) SSB_MULTI(4, 1) SSB_MULTI(4, 2)
+#undef SSB_MULTI
+  fail("plan: unsupported multi-RHS shape");
+  return nullptr;
+}
+
+// Multi-RHS K1 over column bands (X of all slices larger than a share of L2):
+// one pass per band so each pass's gathered X records stay L2-resident; the
+// partial dot products accumulate in w (band 1 stores, 2 adds, the last pass
+// adds and forms r). Rows' band boundaries are positions inside the CSR rows
+// (columns ascending), so the matrix is still streamed once per iteration.
+template <class T>
+void launch_multi_fwd(Plan& P, const SartK<T>& k, int it) {
+  const std::size_t sh = sizeof(double) * kWarps * P.nsys * P.nrhs;
+  const MultiFwdFn<T> fn = multi_fwd_kernel<T>(P);
+  if (P.nband <= 1) {
+    fn<<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it, 0);
+    return;
+  }
+  for (int b = 0; b < P.nband; ++b) {
+    SartK<T> kb = k;
+    for (int s = 0; s < P.nsys; ++s) {
+      const int* bp = P.band_ptr[s].get();  // [nband + 1][rows]
+      kb.s[s].bb = bp + static_cast<std::size_t>(b) * P.rows[s];
+      kb.s[s].be = bp + static_cast<std::size_t>(b + 1) * P.rows[s];
+    }
+    if (P.nsys == 1) kb.s[1] = kb.s[0];
+    const int band = b == 0 ? 1 : (b == P.nband - 1 ? 3 : 2);
+    fn<<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(kb, it, band);
+    if (b + 1 < P.nband) P.ctx->check_launch("sart_fwd_multi_kernel(band)");
+  }
 }
 
 template <class T>
@@ -2205,8 +2301,7 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (P.nrhs > 1) {
-    const std::size_t sh = sizeof(double) * kWarps * P.nsys * P.nrhs;
-    multi_kernel<T>(P, true)<<<P.fwd_blocks, kThreads, sh, P.ctx->stream>>>(k, it);
+    launch_multi_fwd<T>(P, k, it);
     return;
   }
   switch (P.vs_fwd) {
@@ -2228,7 +2323,7 @@ void launch_back(Plan& P, const SartK<T>& k, int it) {
     return;
   }
   if (P.nrhs > 1) {
-    multi_kernel<T>(P, false)<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
+    multi_back_kernel<T>(P)<<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(k, it);
     return;
   }
   switch (P.vs_back) {
@@ -2245,8 +2340,10 @@ int occupancy_blocks(Plan& P, bool fwd) {
   cudaError_t e;
   if (P.nrhs > 1) {
     const std::size_t sh = fwd ? sizeof(double) * kWarps * P.nsys * P.nrhs : 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, multi_kernel<T>(P, fwd), kThreads,
-                                                      sh);
+    e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, multi_fwd_kernel<T>(P),
+                                                            kThreads, sh)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, multi_back_kernel<T>(P),
+                                                            kThreads, sh);
   } else {
     e = fwd ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sart_fwd_kernel<T, 32, 4>,
                                                             kThreads, 0)
@@ -2570,7 +2667,8 @@ void Plan::launch() {
   SSB_CUDA(cudaEventRecord(ev0, ctx->stream));
   if (graph) {
     SSB_CUDA(cudaGraphLaunch(graph, ctx->stream));
-    ctx->launches += static_cast<std::int64_t>(px ? 3 : 2) * opts.max_iters + (paired || px ? 1 : 0);
+    ctx->launches += static_cast<std::int64_t>(px ? 3 : 1 + nband) * opts.max_iters +
+                     (paired || px ? 1 : 0);
   } else {
     enqueue_reset();
     enqueue_iterations(0, opts.max_iters);
@@ -3256,6 +3354,22 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
       1, std::min<long long>(P->fwd_blocks, (fwd_groups + kThreads - 1) / kThreads)));
   P->back_blocks = static_cast<int>(std::max<long long>(
       1, std::min<long long>(P->back_blocks, (back_groups + kThreads - 1) / kThreads)));
+  if (nrhs > 1) {
+    // K1 over column bands (SSB_BANDS > 1) keeps each pass's X records
+    // L2-resident; measured slower on config 4 at every band count (2: -3%,
+    // 3: -7%, 4: -12%; profiles/r01_notes.md), so one pass is the default
+    const int nb = std::min(8, std::max(1, env_int("SSB_BANDS", 1)));
+    P->nband = nb;
+    if (nb > 1) {
+      for (int s = 0; s < P->nsys; ++s) {
+        P->band_ptr[s].alloc(static_cast<std::size_t>(nb + 1) * P->rows[s]);
+        band_ptr_kernel<<<grid1(ctx, P->rows[s]), 256, 0, ctx->stream>>>(
+            P->a[s]->rowptr.get(), P->a[s]->colidx.get(), P->rows[s], P->cols[s], nb,
+            P->band_ptr[s].get());
+        ctx->check_launch("band_ptr_kernel");
+      }
+    }
+  }
   if (P->paired) {
     const long long fg = static_cast<long long>(P->rows[0]) * P->vs_fwd;
     const long long bg = static_cast<long long>(P->cols[0]) * P->vs_back;

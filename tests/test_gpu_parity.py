@@ -201,6 +201,35 @@ def test_multi_rhs_plan_matches_single(S):
         assert np.allclose(multi.history(0, k), want.residual_history, rtol=TOL_F64, atol=0)
 
 
+@pytest.mark.parametrize("bands", [2, 3, 5])
+def test_multi_rhs_column_bands(bands, monkeypatch):
+    """K1 over column bands (partial dots accumulated in w, the last pass forms
+    r): the same solution as one pass within 1e-12 (only the in-row summation
+    splits at band edges), and the oracle within the north-star tolerance."""
+    w, cfg, a, csr, f_true, p, s = workload(1)
+    gs = P.split_system(P.CentroSystem(s.a, p, 0.0))
+    S = 64
+    ps1 = np.stack([gs.p1 * (1 + 0.01 * k) for k in range(S)])
+    ps2 = np.stack([gs.p2 * (1 - 0.01 * k) for k in range(S)])
+    opts = P.SolveOptions(max_iters=25, tol=0.0)
+
+    def solve():
+        pl = P.SartPlan(gs.a1, gs.a2, opts, nrhs=S)
+        pl.set_rhs(0, ps1.reshape(-1))
+        pl.set_rhs(1, ps2.reshape(-1))
+        pl.run()
+        return pl.solution(0), pl.solution(1), pl.history(1, S - 1)
+
+    monkeypatch.setenv("SSB_BANDS", "1")
+    one = solve()
+    monkeypatch.setenv("SSB_BANDS", str(bands))
+    banded = solve()
+    assert rel_err(banded[0], one[0]) <= 1e-12 and rel_err(banded[1], one[1]) <= 1e-12
+    assert np.allclose(banded[2], one[2], rtol=1e-12, atol=0)
+    want = O.sart_solve(O.split_system(a, p, 0.0).a2, ps2[S - 1], max_iters=25, tol=0.0)
+    assert rel_err(banded[1][S - 1], want.f) <= TOL_F64
+
+
 # ------------------------------------------------------------------ reference pins on the GPU
 def ex1(pins):
     return np.array(pins["example1"]["matrix"], float), np.array(pins["example1"]["rhs"], float)
