@@ -1497,8 +1497,10 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
   }
 }
 
+// one slice pass (Q = 1): 4 CTAs per SM (63 registers, no spills), K2 0.68 ->
+// 0.63 ms on config 4; Q = 2 and the forward kernel spill under that cap
 template <class T, int V, int Q>
-__global__ void __launch_bounds__(kThreads) sart_back_multi_kernel(SartK<T> k, int it) {
+__global__ void __launch_bounds__(kThreads, Q == 1 ? 4 : 1) sart_back_multi_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, false);
   if (loop_over(k)) return;
   const int lane = threadIdx.x & 31;

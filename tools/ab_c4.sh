@@ -1,5 +1,5 @@
-# A/B of the multi-RHS kernels: previous commit's library (ab/lib_old.so) vs the tree's
-for r in 1 2; do
-for lib in ab/lib_old.so paper_1902_10559_b200/libsymsplit_b200.so; do
-  echo "== $lib $(SSB_LIB=$PWD/$lib SSB_BANDS=1 timeout 900 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']; print(d['value'], k['fwd_avg_ms'], k['back_avg_ms'])")"
+# multi-RHS (config 4) measurements: 128 and 256 slices per plan; multi parity tests
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -k "multi" 2>&1 | tail -1
+for r in 1 2; do for spp in 128 256; do
+  echo "== spp $spp $(timeout 900 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline --slices-per-plan $spp 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']; print(d['value'], k['fwd_avg_ms'], k['back_avg_ms'])")"
 done; done
