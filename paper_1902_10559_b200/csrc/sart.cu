@@ -3333,6 +3333,16 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     const auto vs_of = [&](double avg) { return mir32 ? pick_vs_mirror(avg) : pick_vs(avg); };
     P->vs_fwd = env_int("SSB_VS_FWD", vs_of(nnz_total / std::max(rows_total, 1.0)));
     P->vs_back = env_int("SSB_VS_BACK", vs_of(nnz_total / std::max(cols_total, 1.0)));
+    // too few vectors to give every SM one CTA: wider lane groups (config 1,
+    // 640 x 2048 per system: 75.7K -> 86.6K it/s at 32 / 16 lanes; config 2's
+    // 6,144 rows already fill the SMs and measure slower when widened)
+    const double fill = static_cast<double>(ctx->sm_count) * kThreads;
+    while (!std::getenv("SSB_VS_FWD") && P->vs_fwd < 32 && P->rows[0] * P->vs_fwd < fill) {
+      P->vs_fwd *= 2;
+    }
+    while (!std::getenv("SSB_VS_BACK") && P->vs_back < 16 && P->cols[0] * P->vs_back < fill) {
+      P->vs_back *= 2;
+    }
     P->uf_fwd = env_int("SSB_UF_FWD", P->mir_f && o.dtype == SS_F64 ? 2 : 4);
     P->uf_back = env_int("SSB_UF_BACK", 2);
   }
