@@ -746,32 +746,34 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
 
 template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kernel(SartK<T> k, int it) {
-  cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
-  it = pass_index(k, it, true);
-  if (loop_over(k)) return;
   using T2 = typename Vec2<T>::type;
   __shared__ double red[2][kWarps];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
   const long long group = (blockIdx.x * (long long)kThreads + threadIdx.x) / VS;
   const long long ngroups = (long long)gridDim.x * kThreads / VS;
-  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   const int n = static_cast<int>(k.rows0);
   const int* __restrict__ ptr = TL != 0 ? k.tpf : k.s[0].rp;  // tiled: padded pointer
   int g = static_cast<int>(group);
   const int gend = n, gstep = static_cast<int>(ngroups);
+  // the stream layout is constant: the first row's bounds load while the
+  // previous pass drains (PDL), only its results wait for the dependency
+  int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
+  if (g < gend) {
+    beg = __ldg(ptr + g);
+    end = __ldg(ptr + g + 1);
+    if (TL >= 2) tf = __ldg(k.tff + g);
+    if (TL >= 4 && k.epf) {
+      eb = __ldg(k.epf + g);
+      ee = __ldg(k.epf + g + 1);
+    }
+  }
+  cudaGridDependencySynchronize();
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
+  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
-    if (g < gend) {
-      beg = __ldg(ptr + g);
-      end = __ldg(ptr + g + 1);
-      if (TL >= 2) tf = __ldg(k.tff + g);
-      if (TL >= 4 && k.epf) {
-        eb = __ldg(k.epf + g);
-        ee = __ldg(k.epf + g + 1);
-      }
-    }
     for (; g < gend; g += gstep) {
       const int gn = g + gstep;
       int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
