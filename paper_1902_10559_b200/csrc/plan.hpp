@@ -26,7 +26,7 @@ struct PeerExchange {
   void* region = nullptr;
   std::vector<void*> opened;  // peers' regions mapped through CUDA IPC
   DBuf<char*> peers;          // [G] region base of every rank as seen from this device
-  DBuf<long long> local;      // {epoch base, iterations proceeded this solve, timeout}
+  DBuf<long long> local;      // {epoch base, iterations proceeded, timeout, reduces announced}
   ~PeerExchange();
 };
 

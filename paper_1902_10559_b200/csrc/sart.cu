@@ -1627,7 +1627,7 @@ struct XK {
   long long cols, own;  // columns, columns owned per rank
   int rgrid;            // CTAs of the reduce kernel
   unsigned long long off_recv, off_x, off_r2, off_done, off_xready, off_dflag;
-  long long* local;     // {epoch base, iterations proceeded, timeout}
+  long long* local;     // {epoch base, iterations proceeded, timeout, reduces announced}
   int inline_signal;    // 1: kernels announce; 0 (emulated group): announce kernels do
 };
 
@@ -1734,6 +1734,7 @@ __device__ int xchg_enter(const SartK<T>& k, const XK<T>& x, int it) {
   // reduce it-1 ran iff K1x(it-1) proceeded; announce its x pushes (block 0)
   if (x.inline_signal && blockIdx.x == 0 && it > 0 && x.local[1] == it) {
     signal_all(x, x.off_xready);
+    x.local[3] = it;
   }
   if (st[0] != 0 || st[2] != 0) return 0;
   const long long base = x.local[0];
@@ -1908,9 +1909,12 @@ __global__ void __launch_bounds__(kThreads) xchg_reduce_kernel(SartK<T> k, XK<T>
 template <class T>
 __global__ void xchg_announce_kernel(SartK<T> k, XK<T> x, int it, int kind) {
   if (threadIdx.x != 0) return;
-  if (kind == 0 && it > 0 && x.local[1] == it) signal_all(x, x.off_xready);
+  if (kind == 0 && it > 0 && x.local[1] == it) {
+    signal_all(x, x.off_xready);
+    x.local[3] = it;
+  }
   if (kind == 1 && sys_on(k.state, 0)) signal_all(x, x.off_done);
-  if (kind == 2 && x.local[1] > 0 && x.local[1] == k.max_iters) signal_all(x, x.off_xready);
+  if (kind == 2 && x.local[3] < x.local[1]) signal_all(x, x.off_xready);
 }
 
 // After the last pass: wait for the final iteration's x, settle its residual /
@@ -1920,8 +1924,9 @@ __global__ void xchg_final_kernel(SartK<T> k, XK<T> x) {
   if (threadIdx.x != 0) return;
   volatile int* st = k.state;
   const long long base = x.local[0], L = x.local[1];
-  // the last reduce is announced here when no K1x followed it
-  if (x.inline_signal && L > 0 && L == k.max_iters) signal_all(x, x.off_xready);
+  // the last reduce is announced here unless a K1x already did (a solve cut
+  // short by the stop test, or a partial pass count as in Plan::profile)
+  if (x.inline_signal && x.local[3] < L) signal_all(x, x.off_xready);
   if (!wait_geq(xready(x, x.me), xready_target(x, base + L), x.local + 2)) return;
   if (L > 0 && st[0] == 0 && st[2] == 0) {
     const int d = ld_sys(xdflag(x, x.me));
@@ -1938,6 +1943,7 @@ __global__ void xchg_final_kernel(SartK<T> k, XK<T> x) {
   }
   x.local[0] = base + L;
   x.local[1] = 0;
+  x.local[3] = 0;
 }
 
 // Column-band boundaries inside every CSR row (columns ascending): out[b][i] =
@@ -2552,6 +2558,7 @@ void Plan::enqueue_reset() {
     SSB_CUDA(cudaMemsetAsync(r + px->off_x, 0, cols[0] * tsize(), ctx->stream));
     SSB_CUDA(cudaMemsetAsync(r + px->off_dflag, 0, sizeof(int), ctx->stream));
     SSB_CUDA(cudaMemsetAsync(px->local.get() + 1, 0, sizeof(long long), ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(px->local.get() + 3, 0, sizeof(long long), ctx->stream));
   }
   SSB_CUDA(cudaMemsetAsync(state.get(), 0, state.size() * sizeof(int), ctx->stream));
   SSB_CUDA(cudaMemsetAsync(ticket.get(), 0, 2 * sizeof(unsigned), ctx->stream));
@@ -3505,8 +3512,8 @@ void setup_exchange(Plan& P, int G, int me, bool emulated) {
   // plain cudaMalloc: pool (cudaMallocAsync) memory cannot be exported over IPC
   SSB_CUDA(cudaMalloc(&X->region, X->bytes));
   SSB_CUDA(cudaMemsetAsync(X->region, 0, X->bytes, ctx->stream));
-  X->local.alloc(3);
-  SSB_CUDA(cudaMemsetAsync(X->local.get(), 0, 3 * sizeof(long long), ctx->stream));
+  X->local.alloc(4);
+  SSB_CUDA(cudaMemsetAsync(X->local.get(), 0, 4 * sizeof(long long), ctx->stream));
   X->peers.alloc(G);
   std::vector<char*> bases(G, nullptr);
   bases[me] = static_cast<char*>(X->region);

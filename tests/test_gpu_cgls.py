@@ -72,7 +72,10 @@ def test_cgls_split_config1_matches_oracle(paired, monkeypatch):
     ill-conditioned underdetermined system (measured: 3e-16 after 3 iterations,
     8e-15 after 5, 1e-10 after 10, 4e-6 after 20). So f is compared where CG is
     stable (5 iterations, 1e-12) and, after 30 iterations, the residual norm —
-    the quantity CGLS minimises — to 1e-4 relative (measured 2.9e-5)."""
+    the quantity CGLS minimises — to 1e-3 relative. That residual moves with
+    the summation order too: measured 2.9e-5 with 4-lane groups per vector and
+    6.0e-4 with the 32 / 16-lane groups the paired streams use on this small
+    system since they widen to fill the SMs (equally valid orders)."""
     monkeypatch.setenv("SSB_CGLS_PAIRED", paired)
     w, cfg, a, csr, f_true, p = oracle_workload(1)
     s = P.build_system(w.scan_config())
@@ -83,7 +86,7 @@ def test_cgls_split_config1_matches_oracle(paired, monkeypatch):
         assert got.method == "cgls" and got.iterations == it == iters
         if f_tol is not None:
             assert rel_err(got.f, want_f) <= f_tol
-        assert abs(got.residual_norm - res) <= 1e-4 * res
+        assert abs(got.residual_norm - res) <= 1e-3 * res
     got32 = P.solve_split(P.CentroSystem(s.a, p, 0.0),
                           P.SolveOptions(method="cgls", max_iters=5, tol=1e-10, dtype="f32"))
     want_f, it, res = O.solve_split_method(a, p, "cgls", 0.0, 5, 1e-10)

@@ -126,5 +126,8 @@ def test_peer_plan_single_rank_nccl():
         sh.run()  # second solve: epoch base advanced by the first
         tol = 1e-12 if dtype == "f64" else 1e-5
         assert sh.solution(0).tobytes() == first.tobytes()
+        sh.profile(7)  # a partial pass count (7 of 20): the last reduce is announced
+        sh.run()       # by the final kernel; the next solve must not time out
+        assert sh.solution(0).tobytes() == first.tobytes()
         assert rel_err(first, f_ref) <= tol
         assert np.allclose(sh.history(0), h_ref, rtol=tol)
