@@ -3500,7 +3500,9 @@ void setup_exchange(Plan& P, int G, int me, bool emulated) {
   X->emulated = emulated;
   X->cols = P.cols[0];
   X->own = (X->cols + G - 1) / G;  // owner of column j: j / own (exchange_owned_columns)
-  X->rgrid = 2 * ctx->sm_count;
+  // about one owned column per reduce thread (latency-bound gathers of G rows)
+  X->rgrid = static_cast<int>(std::min<std::int64_t>(
+      8LL * ctx->sm_count, std::max<std::int64_t>(ctx->sm_count, (X->own + 255) / 256)));
   const std::size_t tb = P.tsize();
   X->off_recv = 0;
   X->off_x = align256(static_cast<std::size_t>(G) * X->cols * tb + kSlackBytes);
@@ -3685,8 +3687,12 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   P->a[0] = P->own;
   P->rows[0] = rloc;
   P->cols[0] = a->cols;
-  P->vs_fwd = pick_vs(rloc > 0 ? double(nloc) / rloc : 0);
-  P->vs_back = pick_vs(a->cols > 0 ? double(nloc) / a->cols : 0);
+  P->vs_fwd = env_int("SSB_VS_FWD", pick_vs(rloc > 0 ? double(nloc) / rloc : 0));
+  P->vs_back = env_int("SSB_VS_BACK", pick_vs(a->cols > 0 ? double(nloc) / a->cols : 0));
+  // the single-system tiled kernels' measured best (as make_plan): UF 2 in K1
+  // costs ~10 us per launch on a config-3 system (62 vs 52 us)
+  P->uf_fwd = env_int("SSB_UF_FWD", 4);
+  P->uf_back = env_int("SSB_UF_BACK", 4);
   if (o.dtype == SS_F32) {
     P->fwd_blocks = occupancy_blocks<float>(*P, true);
     P->back_blocks = occupancy_blocks<float>(*P, false);
