@@ -171,8 +171,10 @@ void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double to
   const double parent = static_cast<double>(a.rows) * static_cast<double>(a.cols);
   const double half = static_cast<double>(o.a1->rows) * static_cast<double>(o.a1->cols);
   o.fills[0] = parent > 0 ? static_cast<double>(ssb::nonzeros(a)) / parent : 0.0;
-  o.fills[1] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a1)) / half : 0.0;
-  o.fills[2] = half > 0 ? static_cast<double>(ssb::nonzeros(*o.a2)) / half : 0.0;
+  // the fold stores no zeros (it prunes v != 0 like centro.cpp:127-128), so the
+  // folded systems' nonzero counts are their stored counts
+  o.fills[1] = half > 0 ? static_cast<double>(o.a1->nnz) / half : 0.0;
+  o.fills[2] = half > 0 ? static_cast<double>(o.a2->nnz) / half : 0.0;
   tr.mark("  split_rhs + fills");
 }
 
