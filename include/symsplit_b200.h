@@ -134,6 +134,9 @@ int ss_matrix_download_csr(ss_matrix_t a, int32_t* ptr, int32_t* idx, double* va
 int ss_matrix_download_csc(ss_matrix_t a, int32_t* outer, int32_t* inner, double* values);
 /* replaces Matrix::apply / apply_transpose (matrix.cpp:67-76) */
 int ss_matrix_apply(ss_matrix_t a, const double* x, double* y);
+/* replaces Matrix::coeff (matrix.cpp:44-50): the stored value at 0-based
+ * (i, j) or 0; "matrix index out of range" outside the shape */
+int ss_matrix_coeff(ss_matrix_t a, int64_t i, int64_t j, double* out);
 int ss_matrix_apply_transpose(ss_matrix_t a, const double* y, double* x);
 
 /* ------------------------------------------------------------ geometry */
@@ -160,6 +163,15 @@ int ss_ray_weights(ss_ctx_t ctx, const double ray4[4], const ss_grid_spec* grid,
  * 0..M/2-1, mirror rows by reflection; returns A (M x N) on the device */
 int ss_build_system(ss_ctx_t ctx, const ss_scan_config* cfg, int parallelism,
                     ss_matrix_t* out);
+/* replaces build_system(const ScanGeometry&, const GridSpec&, int parallelism)
+ * (geometry.hpp:118, geometry.cpp:227-275) with a caller-supplied grid: the
+ * geometry fields of `geom` are used, its grid_nx / grid_ny are ignored */
+int ss_build_system_grid(ss_ctx_t ctx, const ss_scan_config* geom, const ss_grid_spec* grid,
+                         int parallelism, ss_matrix_t* out);
+/* replaces enumerate_rays(const ScanGeometry&, const GridSpec&)
+ * (geometry.cpp:132-173) with a caller-supplied grid (as above) */
+int ss_enumerate_rays_grid(const ss_scan_config* geom, const ss_grid_spec* grid, double* rays4,
+                           int64_t* count, int* samples, double* pitch);
 
 /* ------------------------------------------------------------ centro */
 /* replaces verify_symmetry (centro.cpp:46-66) */

@@ -16,6 +16,8 @@
 //  * every call runs on the GPU of the Context it was created on.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -92,6 +94,19 @@ class Context {
 
  private:
   std::shared_ptr<ss_context> h_;
+};
+
+// reference DenseStorage (Eigen::MatrixXd): column-major, 0-based (i, j)
+struct DenseStorage {
+  Index r = 0, c = 0;
+  Vector data;  // column-major
+  DenseStorage() = default;
+  DenseStorage(Index rows, Index cols)
+      : r(rows), c(cols), data(static_cast<std::size_t>(rows * cols), 0.0) {}
+  Index rows() const { return r; }
+  Index cols() const { return c; }
+  double& operator()(Index i, Index j) { return data[static_cast<std::size_t>(j * r + i)]; }
+  double operator()(Index i, Index j) const { return data[static_cast<std::size_t>(j * r + i)]; }
 };
 
 // reference matrix.hpp:34-87 (device sparse storage only)
@@ -174,6 +189,30 @@ class Matrix {
     detail::check(ss_matrix_apply_transpose(h_.get(), y.data(), x.data()));
     return x;
   }
+  bool is_sparse() const { return true; }  // device storage is always compressed
+  // reference matrix.cpp:44-50
+  double coeff(Index i, Index j) const {
+    double v = 0.0;
+    detail::check(ss_matrix_coeff(h_.get(), i, j, &v));
+    return v;
+  }
+  // reference matrix.hpp:76-87: every stored entry as f(row, col, value) in
+  // compressed-column order (the order Eigen's InnerIterator visits)
+  template <class F>
+  void for_each(F&& f) const {
+    std::vector<int32_t> outer, inner;
+    Vector values;
+    to_csc(outer, inner, values);
+    for (Index j = 0; j + 1 < static_cast<Index>(outer.size()); ++j) {
+      for (int32_t k = outer[static_cast<std::size_t>(j)];
+           k < outer[static_cast<std::size_t>(j) + 1]; ++k) {
+        f(static_cast<Index>(inner[static_cast<std::size_t>(k)]), j,
+          values[static_cast<std::size_t>(k)]);
+      }
+    }
+  }
+  // reference matrix.cpp:52-55 (DenseStorage: column-major rows x cols)
+  DenseStorage to_dense() const;
   // CSC download (reference Eigen compressed storage): outer, inner, values
   void to_csc(std::vector<int32_t>& outer, std::vector<int32_t>& inner, Vector& values) const {
     outer.resize(static_cast<std::size_t>(cols() + 1));
@@ -186,6 +225,13 @@ class Matrix {
  private:
   std::shared_ptr<ss_matrix> h_;
 };
+
+inline DenseStorage Matrix::to_dense() const {
+  const auto [m, n] = shape();
+  DenseStorage d(m, n);
+  for_each([&](Index i, Index j, double v) { d(i, j) = v; });
+  return d;
+}
 
 // reference centro.hpp:24-51
 struct CentroSystem {
@@ -392,58 +438,166 @@ inline SolveReport solve_split(const CentroSystem& sys, const SolveOptions& opts
 }
 
 // ------------------------------------------------------------------ geometry
-using ScanConfig = ss_scan_config;
-using GridSpec = ss_grid_spec;
-
 inline constexpr double kPi = 3.14159265358979323846;
 inline constexpr double degrees_to_radians(double deg) { return deg * kPi / 180.0; }
 
+// reference geometry.hpp:22-37 (GridSpec): same fields, defaults and helpers
+struct GridSpec {
+  int n_x = 32;
+  int n_y = 32;
+  double voxel_size = 0.1 / 32;
+  double center_x = 0.0;
+  double y_bottom = 0.25;
+
+  int cell_count() const { return n_x * n_y; }
+  double width() const { return n_x * voxel_size; }
+  double height() const { return n_y * voxel_size; }
+  double x_left() const { return center_x - 0.5 * width(); }
+  double x_right() const { return center_x + 0.5 * width(); }
+  double y_top() const { return y_bottom + height(); }
+  // reference geometry.cpp:59-66
+  std::pair<double, double> cell_center(int c, int r) const {
+    if (c < 1 || c > n_x || r < 1 || r > n_y) throw Error("cell_center: cell index out of range");
+    return {center_x + (c - 0.5 - 0.5 * n_x) * voxel_size,
+            y_bottom + (n_y - r + 0.5) * voxel_size};
+  }
+  // reference geometry.cpp:68-74
+  void validate() const {
+    if (n_x < 2 || n_x % 2 != 0) throw Error("grid: n_x must be even and positive (mirror pairing)");
+    if (n_y < 1) throw Error("grid: n_y must be positive");
+    if (!(voxel_size > 0)) throw Error("grid: voxel_size must be positive");
+  }
+  ss_grid_spec c() const { return ss_grid_spec{n_x, n_y, voxel_size, center_x, y_bottom}; }
+};
+
+// reference geometry.hpp:57-68 (ScanGeometry): same fields and defaults
+struct ScanGeometry {
+  int k = 24;
+  double gamma = degrees_to_radians(30.0);  // radians
+  double h_e = 1.0;
+  double h_m = 0.25;
+  double l_m = 0.43;
+  int n_p = 1024;
+  double a_e = 7e-4;
+  double obj_size = 0.1;
+
+  // the C ABI's geometry record (its grid_nx / grid_ny are not read where a
+  // GridSpec is passed alongside)
+  ss_scan_config c(int grid_nx = 32, int grid_ny = 32) const {
+    return ss_scan_config{k, gamma, h_e, h_m, l_m, n_p, a_e, obj_size, grid_nx, grid_ny};
+  }
+  // reference geometry.cpp:94-105 (the same checks, messages and order)
+  void validate() const {
+    std::vector<double> a(static_cast<std::size_t>(k > 0 ? k : 0) + 1);
+    const ss_scan_config cc = c();
+    detail::check(ss_emitter_angles(&cc, a.data()));
+  }
+};
+
+// reference geometry.hpp:137-141 (ScanConfig)
+struct ScanConfig {
+  ScanGeometry geom;
+  int grid_nx = 32;
+  int grid_ny = 32;
+
+  ss_scan_config c() const { return geom.c(grid_nx, grid_ny); }
+  static ScanConfig from_c(const ss_scan_config& s) {
+    ScanConfig o;
+    o.geom = ScanGeometry{s.k, s.gamma, s.h_e, s.h_m, s.l_m, s.n_p, s.a_e, s.obj_size};
+    o.grid_nx = s.grid_nx;
+    o.grid_ny = s.grid_ny;
+    return o;
+  }
+};
+
+// reference geometry.cpp:352-401
 inline ScanConfig parse_scan_config(const std::string& text) {
-  ScanConfig c{};
+  ss_scan_config c{};
   detail::check(ss_parse_scan_config(text.c_str(), &c));
-  return c;
+  return ScanConfig::from_c(c);
 }
 
+// reference geometry.cpp:403-411
 inline GridSpec make_grid(const ScanConfig& c) {
-  GridSpec g{};
-  detail::check(ss_make_grid(&c, &g));
-  return g;
+  const ss_scan_config cc = c.c();
+  ss_grid_spec g{};
+  detail::check(ss_make_grid(&cc, &g));
+  return GridSpec{g.n_x, g.n_y, g.voxel_size, g.center_x, g.y_bottom};
 }
 
+// reference geometry.cpp:76-92 (1-based)
 inline int snake_index(int c, int r, const GridSpec& g) {
+  const ss_grid_spec gc = g.c();
   int j = 0;
-  detail::check(ss_snake_index(c, r, &g, &j));
+  detail::check(ss_snake_index(c, r, &gc, &j));
   return j;
 }
+inline std::pair<int, int> snake_inverse(int j, const GridSpec& g) {
+  const ss_grid_spec gc = g.c();
+  int c = 0, r = 0;
+  detail::check(ss_snake_inverse(j, &gc, &c, &r));
+  return {c, r};
+}
 
-// reference geometry.hpp:74-88 (Point, Ray)
+// reference geometry.hpp:74-88 (Point, Ray, RaySet)
 struct Point {
   double x = 0.0, y = 0.0;
 };
 struct Ray {
   Point source, detector;
 };
+struct RaySet {
+  std::vector<Ray> rays;
+  int positions = 0;
+  int samples_per_position = 0;
+  double sample_pitch = 0.0;
+  Index count() const { return static_cast<Index>(rays.size()); }
+};
 
 // reference geometry.cpp:107-117
-inline std::vector<double> emitter_angles(const ScanConfig& c) {
-  std::vector<double> a(static_cast<std::size_t>(c.k > 0 ? c.k : 0));
+inline std::vector<double> emitter_angles(const ScanGeometry& geom) {
+  std::vector<double> a(static_cast<std::size_t>(geom.k > 0 ? geom.k : 0));
+  const ss_scan_config c = geom.c();
   detail::check(ss_emitter_angles(&c, a.data()));
   return a;
 }
 
 // reference geometry.cpp:119-130
-inline std::vector<Point> emitter_positions(const ScanConfig& c, double center_x = 0.0) {
-  std::vector<double> xy(2 * static_cast<std::size_t>(c.k > 0 ? c.k : 0));
+inline std::vector<Point> emitter_positions(const ScanGeometry& geom, double center_x = 0.0) {
+  std::vector<double> xy(2 * static_cast<std::size_t>(geom.k > 0 ? geom.k : 0));
+  const ss_scan_config c = geom.c();
   detail::check(ss_emitter_positions(&c, center_x, xy.data()));
   std::vector<Point> out(xy.size() / 2);
   for (std::size_t i = 0; i < out.size(); ++i) out[i] = Point{xy[2 * i], xy[2 * i + 1]};
   return out;
 }
 
+// reference geometry.cpp:132-173: traced half then the reversed mirror half
+inline RaySet enumerate_rays(const ScanGeometry& geom, const GridSpec& grid) {
+  const ss_scan_config c = geom.c();
+  const ss_grid_spec g = grid.c();
+  int64_t n = 0;
+  int samples = 0;
+  double pitch = 0.0;
+  detail::check(ss_enumerate_rays_grid(&c, &g, nullptr, &n, &samples, &pitch));
+  std::vector<double> r4(4 * static_cast<std::size_t>(n));
+  detail::check(ss_enumerate_rays_grid(&c, &g, r4.data(), &n, &samples, &pitch));
+  RaySet out;
+  out.rays.resize(static_cast<std::size_t>(n));
+  for (std::size_t i = 0; i < out.rays.size(); ++i) {
+    out.rays[i] = Ray{{r4[4 * i], r4[4 * i + 1]}, {r4[4 * i + 2], r4[4 * i + 3]}};
+  }
+  out.positions = geom.k;
+  out.samples_per_position = samples;
+  out.sample_pitch = pitch;
+  return out;
+}
+
 // reference geometry.cpp:175-225 (1-based snake columns, path order), device tracer
 inline std::vector<std::pair<int, double>> ray_weights(
-    const Ray& ray, const GridSpec& g, const Context& ctx = Context::default_context()) {
+    const Ray& ray, const GridSpec& grid, const Context& ctx = Context::default_context()) {
   const double r4[4] = {ray.source.x, ray.source.y, ray.detector.x, ray.detector.y};
+  const ss_grid_spec g = grid.c();
   int64_t n = 0;
   detail::check(ss_ray_weights(ctx.get(), r4, &g, 0, nullptr, nullptr, &n));
   std::vector<int> cols(static_cast<std::size_t>(n));
@@ -454,14 +608,25 @@ inline std::vector<std::pair<int, double>> ray_weights(
   return out;
 }
 
-// reference geometry.hpp:118: A on the GPU, p = 0, symmetry_tol = 0
-inline CentroSystem build_system(const ScanConfig& cfg, int parallelism = 0,
+// reference geometry.hpp:118 / geometry.cpp:227-275: A on the GPU (traced
+// half + mirror rows), p = 0, symmetry_tol = 0. `parallelism` is accepted for
+// parity; the device build is identical for any value.
+inline CentroSystem build_system(const ScanGeometry& geom, const GridSpec& grid,
+                                 int parallelism = 0,
                                  const Context& ctx = Context::default_context()) {
+  const ss_scan_config c = geom.c();
+  const ss_grid_spec g = grid.c();
   ss_matrix_t h = nullptr;
-  detail::check(ss_build_system(ctx.get(), &cfg, parallelism, &h));
+  detail::check(ss_build_system_grid(ctx.get(), &c, &g, parallelism, &h));
   CentroSystem sys{Matrix(h), {}, 0.0};
   sys.p.assign(static_cast<std::size_t>(sys.a.rows()), 0.0);
   return sys;
+}
+
+// convenience: the grid of a whole scan configuration (make_grid(cfg))
+inline CentroSystem build_system(const ScanConfig& cfg, int parallelism = 0,
+                                 const Context& ctx = Context::default_context()) {
+  return build_system(cfg.geom, make_grid(cfg), parallelism, ctx);
 }
 
 // ------------------------------------------------------------------ file formats
@@ -489,32 +654,66 @@ inline void write_vector_csv(const Vector& v, const std::string& path) {
   detail::check(ss_write_vector_csv(path.c_str(), v.data(), static_cast<int64_t>(v.size())));
 }
 
-inline std::vector<double> shepp_logan_ellipses() {
-  // reference phantom.cpp:18-32, rows (x0, y0, a, b, angle rad, density)
-  const double t[10][6] = {{0.0, 0.0, 0.69, 0.92, 0.0, 2.0},
-                           {0.0, -0.0184, 0.6624, 0.874, 0.0, -0.98},
-                           {0.22, 0.0, 0.11, 0.31, -18.0, -0.02},
-                           {-0.22, 0.0, 0.16, 0.41, 18.0, -0.02},
-                           {0.0, 0.35, 0.21, 0.25, 0.0, 0.01},
-                           {0.0, 0.1, 0.046, 0.046, 0.0, 0.01},
-                           {0.0, -0.1, 0.046, 0.046, 0.0, 0.01},
-                           {-0.08, -0.605, 0.046, 0.023, 0.0, 0.01},
-                           {0.0, -0.606, 0.023, 0.023, 0.0, 0.01},
-                           {0.06, -0.605, 0.023, 0.046, 0.0, 0.01}};
-  std::vector<double> out;
-  for (const auto& e : t) {
-    out.insert(out.end(), {e[0], e[1], e[2], e[3], degrees_to_radians(e[4]), e[5]});
+// ------------------------------------------------------------------ phantom
+// reference phantom.hpp:16-27 (Ellipse); contains() is host-side libm as in
+// phantom.cpp:8-16 (the device rasterizer uses host-computed sin/cos too)
+struct Ellipse {
+  double x0 = 0.0;
+  double y0 = 0.0;
+  double a = 1.0;
+  double b = 1.0;
+  double angle = 0.0;
+  double density = 0.0;
+  bool contains(double x, double y) const {
+    const double dx = x - x0, dy = y - y0;
+    const double ca = std::cos(angle), sa = std::sin(angle);
+    const double u = (dx * ca + dy * sa) / a;
+    const double v = (-dx * sa + dy * ca) / b;
+    return u * u + v * v <= 1.0;
   }
-  return out;
+};
+
+// reference phantom.cpp:18-32
+inline std::vector<Ellipse> shepp_logan_ellipses() {
+  const auto deg = [](double d) { return degrees_to_radians(d); };
+  return {{0.0, 0.0, 0.69, 0.92, deg(0.0), 2.0},
+          {0.0, -0.0184, 0.6624, 0.874, deg(0.0), -0.98},
+          {0.22, 0.0, 0.11, 0.31, deg(-18.0), -0.02},
+          {-0.22, 0.0, 0.16, 0.41, deg(18.0), -0.02},
+          {0.0, 0.35, 0.21, 0.25, deg(0.0), 0.01},
+          {0.0, 0.1, 0.046, 0.046, deg(0.0), 0.01},
+          {0.0, -0.1, 0.046, 0.046, deg(0.0), 0.01},
+          {-0.08, -0.605, 0.046, 0.023, deg(0.0), 0.01},
+          {0.0, -0.606, 0.023, 0.023, deg(0.0), 0.01},
+          {0.06, -0.605, 0.023, 0.046, deg(0.0), 0.01}};
 }
 
-// ------------------------------------------------------------------ phantom
-inline Vector rasterize(const std::vector<double>& ellipses6, const GridSpec& g,
-                        const Context& ctx = Context::default_context()) {
-  Vector out(static_cast<std::size_t>(g.n_x) * static_cast<std::size_t>(g.n_y));
-  detail::check(ss_rasterize(ctx.get(), ellipses6.data(),
-                             static_cast<int>(ellipses6.size() / 6), &g, out.data()));
-  return out;
+// reference phantom.hpp:31-36
+struct PhantomImage {
+  GridSpec grid;
+  Vector values;  // length grid.cell_count(), snake order
+  double min_value = 0.0;
+  double max_value = 0.0;
+};
+
+// reference phantom.cpp:34-58, rasterized on the device
+inline PhantomImage rasterize(const std::vector<Ellipse>& ellipses, const GridSpec& grid,
+                              const Context& ctx = Context::default_context()) {
+  grid.validate();
+  std::vector<double> e6;
+  e6.reserve(6 * ellipses.size());
+  for (const Ellipse& e : ellipses) e6.insert(e6.end(), {e.x0, e.y0, e.a, e.b, e.angle, e.density});
+  PhantomImage img;
+  img.grid = grid;
+  img.values.assign(static_cast<std::size_t>(grid.cell_count()), 0.0);
+  const ss_grid_spec g = grid.c();
+  detail::check(ss_rasterize(ctx.get(), e6.data(), static_cast<int>(ellipses.size()), &g,
+                             img.values.data()));
+  if (!img.values.empty()) {
+    img.min_value = *std::min_element(img.values.begin(), img.values.end());
+    img.max_value = *std::max_element(img.values.begin(), img.values.end());
+  }
+  return img;
 }
 
 inline Vector forward_project(const Matrix& a, const Vector& f, double noise_sigma = 0.0,

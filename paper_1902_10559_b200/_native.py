@@ -77,6 +77,7 @@ SIGNATURES = {
     "ss_matrix_download_csr": (C.c_int, [vp, i32p, i32p, dp]),
     "ss_matrix_download_csc": (C.c_int, [vp, i32p, i32p, dp]),
     "ss_matrix_apply": (C.c_int, [vp, dp, dp]),
+    "ss_matrix_coeff": (C.c_int, [vp, C.c_int64, C.c_int64, dp]),
     "ss_matrix_apply_transpose": (C.c_int, [vp, dp, dp]),
     "ss_parse_scan_config": (C.c_int, [C.c_char_p, C.POINTER(ScanConfig)]),
     "ss_make_grid": (C.c_int, [C.POINTER(ScanConfig), C.POINTER(GridSpec)]),
@@ -85,6 +86,10 @@ SIGNATURES = {
                                    C.POINTER(C.c_int)]),
     "ss_enumerate_rays": (C.c_int, [C.POINTER(ScanConfig), dp, i64p, C.POINTER(C.c_int), dp]),
     "ss_build_system": (C.c_int, [vp, C.POINTER(ScanConfig), C.c_int, C.POINTER(vp)]),
+    "ss_build_system_grid": (C.c_int, [vp, C.POINTER(ScanConfig), C.POINTER(GridSpec), C.c_int,
+                                       C.POINTER(vp)]),
+    "ss_enumerate_rays_grid": (C.c_int, [C.POINTER(ScanConfig), C.POINTER(GridSpec), dp, i64p,
+                                         C.POINTER(C.c_int), dp]),
     "ss_verify_symmetry": (C.c_int, [vp, C.c_double, C.POINTER(SymmetryReportC)]),
     "ss_split_rhs": (C.c_int, [vp, dp, i64, dp, dp]),
     "ss_split_system": (C.c_int, [vp, dp, i64, C.c_double, C.POINTER(vp), C.POINTER(vp), dp, dp,

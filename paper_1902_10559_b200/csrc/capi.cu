@@ -2,6 +2,7 @@
 // the reference function it replaces, runs on the device, and converts
 // exceptions to status codes + a thread-local message.
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -204,6 +205,7 @@ void ss_default_options(ss_solve_options* o) {
   o->parallelism = 0;
   o->dtype = SS_F64;
   o->method = SS_METHOD_SART;
+  o->dense_cap = 0;  // 0 selects the reference default 5e7 (solvers.hpp:26)
 }
 
 int ss_device_count(int* out) {
@@ -341,6 +343,26 @@ int ss_matrix_download_csc(ss_matrix_t a, int32_t* outer, int32_t* inner, double
   });
 }
 
+int ss_matrix_coeff(ss_matrix_t a, int64_t i, int64_t j, double* out) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    need(out, "out");
+    if (i < 0 || i >= m->rows || j < 0 || j >= m->cols) ssb::fail("matrix index out of range");
+    use_device(m->ctx);
+    // row i of the CSR (columns ascending): its bounds, then a binary search
+    // over its column indices
+    int be[2] = {0, 0};
+    to_host(m->ctx, be, m->rowptr.get() + i, 2);
+    std::vector<int> cols(static_cast<std::size_t>(be[1] - be[0]));
+    if (!cols.empty()) to_host(m->ctx, cols.data(), m->colidx.get() + be[0], cols.size());
+    const auto it = std::lower_bound(cols.begin(), cols.end(), static_cast<int>(j));
+    *out = 0.0;
+    if (it != cols.end() && *it == j) {
+      to_host(m->ctx, out, m->val.get() + be[0] + (it - cols.begin()), 1);
+    }
+  });
+}
+
 int ss_matrix_apply(ss_matrix_t a, const double* x, double* y) {
   return guarded([&] {
     ssb::Matrix* m = M(a);
@@ -415,6 +437,31 @@ int ss_build_system(ss_ctx_t h, const ss_scan_config* cfg, int parallelism, ss_m
     need(out, "out");
     use_device(ctx);
     *out = wrap(ssb::build_system(ctx, *cfg));
+  });
+}
+
+int ss_build_system_grid(ss_ctx_t h, const ss_scan_config* geom, const ss_grid_spec* grid,
+                         int parallelism, ss_matrix_t* out) {
+  (void)parallelism;  // the device build is identical for any worker count
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(geom, "geom");
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::build_system(ctx, *geom, to_grid(grid)));
+  });
+}
+
+int ss_enumerate_rays_grid(const ss_scan_config* geom, const ss_grid_spec* grid, double* rays4,
+                           int64_t* count, int* samples, double* pitch) {
+  return guarded([&] {
+    need(geom, "geom");
+    need(count, "count");
+    const ssb::RayTable t = ssb::enumerate_rays(*geom, to_grid(grid), rays4 != nullptr);
+    *count = t.m;
+    if (samples) *samples = t.samples;
+    if (pitch) *pitch = t.pitch;
+    if (rays4) std::memcpy(rays4, t.all4.data(), t.all4.size() * sizeof(double));
   });
 }
 
@@ -998,6 +1045,9 @@ int ss_ctx_attach_nccl(ss_ctx_t h, const void* uid, int nranks, int rank) {
     std::memcpy(&id, uid, sizeof id);
     ncclComm_t comm;
     ssb::nccl_check(ssb::nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+    // re-attaching (e.g. a fallback that builds a second plan) replaces the
+    // communicator: release the old one instead of leaking it
+    if (ctx->comm) ssb::nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
     ctx->comm = comm;
     ctx->nranks = nranks;
     ctx->rank = rank;

@@ -1,7 +1,7 @@
 // Host side of the build path: scan configuration, ray enumeration and the
 // per-ray constants the GPU tracer consumes. Everything that needs libm
 // (sin/cos/hypot/log) stays here so its bits match the reference's glibc
-// build; the O(nnz) work happens on the device (ops.cu, kernels_exact.cu).
+// build; the O(nnz) work happens on the device (ops.cu).
 // Compiled with -ffp-contract=off (the reference host build has no FMA).
 #include <algorithm>
 #include <cmath>

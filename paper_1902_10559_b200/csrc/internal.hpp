@@ -226,6 +226,7 @@ Matrix* matrix_from_csc_host(Context* ctx, std::int64_t rows, std::int64_t cols,
                              std::int64_t nnz, const int* outer, const int* inner,
                              const double* v);
 Matrix* build_system(Context* ctx, const ss_scan_config& cfg);
+Matrix* build_system(Context* ctx, const ss_scan_config& cfg, const Grid& g);
 void check_finite(Matrix& a);
 std::int64_t nonzeros(Matrix& a);
 ss_symmetry_report verify_symmetry(Matrix& a, double tol);

@@ -20,6 +20,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -38,11 +40,13 @@ inline const NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.GetErrorString =
         reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
   });
   if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy ||
-      !api.GetErrorString) {
+      !api.GroupStart || !api.GroupEnd || !api.GetErrorString) {
     fail("NCCL unavailable: " + (err.empty() ? std::string("missing symbols") : err), SS_ERR_NCCL);
   }
   return api;

@@ -1144,7 +1144,12 @@ void ray_weights_dev(Context* ctx, double sx, double sy, double ex, double ey, c
 }
 
 Matrix* build_system(Context* ctx, const ss_scan_config& cfg) {
-  const Grid g = make_grid(cfg);
+  return build_system(ctx, cfg, make_grid(cfg));
+}
+
+// reference build_system(const ScanGeometry&, const GridSpec&, int)
+// (geometry.cpp:227-275): the grid is the caller's (cfg.grid_nx / grid_ny unused)
+Matrix* build_system(Context* ctx, const ss_scan_config& cfg, const Grid& g) {
   const RayTable rt = enumerate_rays(cfg, g, false);
   const std::int64_t mh = rt.m / 2, m = rt.m, n = g.cell_count();
   std::vector<double> xb(g.n_x + 1), yb(g.n_y + 1);

@@ -96,8 +96,8 @@ struct SartK {
   const int* epb;  // exceptions, K2: per column pointer, row, {a1, a2}
   const int* eib;
   const T* evb;
-  // row-sharded: K2 writes the partial back-projection to bp_out[0..cols)
-  // and K1's ||r_g||^2 lands in bp_out[cols] (one all-reduce per iteration)
+  // row-sharded: K2 writes the partial back-projection to bp_out[0..cols);
+  // K1's ||r_g||^2 goes to an fp64 slot behind it (one grouped all-reduce)
   T* bp_out;
   // graph WHILE-loop mode: the iteration index lives on the device; the last
   // block of K1 advances it and decides whether the loop body runs again
@@ -1554,11 +1554,11 @@ __global__ void __launch_bounds__(kThreads, Q == 1 ? 4 : 1) sart_back_multi_kern
 // After the all-reduce of [A_g^T w_g | ||r_g||^2] every rank applies the same
 // update (SURVEY §8e level 3) with the reference's check-before-update order.
 template <class T>
-__global__ void sart_sharded_update_kernel(T* x, const T* bp, const T* cinv, long long cols,
-                                           const double* pnorm, double tol, double relax,
-                                           double* history, int* state, int it) {
+__global__ void sart_sharded_update_kernel(T* x, const T* bp, const double* r2, const T* cinv,
+                                           long long cols, const double* pnorm, double tol,
+                                           double relax, double* history, int* state, int it) {
   if (!sys_on(state, 0)) return;
-  const double res = sqrt(static_cast<double>(bp[cols]));
+  const double res = sqrt(*r2);
   if (blockIdx.x == 0 && threadIdx.x == 0) history[it] = res;
   if (res <= tol * pnorm[0]) return;  // break before the update
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < cols;
@@ -1569,19 +1569,18 @@ __global__ void sart_sharded_update_kernel(T* x, const T* bp, const T* cinv, lon
   }
 }
 
-template <class T>
-__global__ void sharded_stop_kernel(const T* bp, long long cols, const double* pnorm, double tol,
-                                    int* state, int it) {
-  if (state[0] == 0 && state[2] == 0 && sqrt(static_cast<double>(bp[cols])) <= tol * pnorm[0]) {
+__global__ void sharded_stop_kernel(const double* r2, const double* pnorm, double tol, int* state,
+                                    int it) {
+  if (state[0] == 0 && state[2] == 0 && sqrt(*r2) <= tol * pnorm[0]) {
     state[0] = 1;
     state[1] = it;
   }
 }
 
 // Fixed-order sum of the forward kernel's per-block ||r_g||^2 partials into
-// the all-reduce slot bp[cols].
-template <class T>
-__global__ void sharded_r2_kernel(const double* partial, int nblk, T* slot) {
+// the fp64 all-reduce slot behind the back-projection (fp64 in every plan
+// dtype, like the unsharded plans' residual).
+__global__ void sharded_r2_kernel(const double* partial, int nblk, double* slot) {
   __shared__ double sh[kThreads];
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partial[b];
@@ -1591,7 +1590,16 @@ __global__ void sharded_r2_kernel(const double* partial, int nblk, T* slot) {
     if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *slot = static_cast<T>(sh[0]);
+  if (threadIdx.x == 0) *slot = sh[0];
+}
+
+// byte offset of the fp64 ||r_g||^2 slot behind the [cols] back-projection
+inline std::size_t sharded_r2_offset(long long cols, std::size_t tsize) {
+  return (static_cast<std::size_t>(cols) * tsize + 15) & ~static_cast<std::size_t>(15);
+}
+inline double* sharded_r2_slot(Plan& P) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(P.bp.get()) +
+                                   sharded_r2_offset(P.cols[0], P.tsize()));
 }
 
 // ------------------------------------------------------------ peer exchange
@@ -1681,10 +1689,15 @@ __device__ __forceinline__ int ld_sys(const int* p) {
   asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// one count into counter `off` of every rank (the stores being announced
-// belong to an earlier, completed kernel of this stream)
+// one count into counter `off` of every rank. The stores being announced
+// belong to an earlier, completed kernel of this stream (or to this thread);
+// one system-scope fence in the announcing thread makes them cumulatively
+// visible before any count lands, so a consumer's ld.acquire.sys of the
+// counter pairs with it (PTX memory model) -- no per-CTA fences on the data
+// path, one fence per rank per announcement.
 template <class T>
 __device__ void signal_all(const XK<T>& x, unsigned long long off) {
+  __threadfence_system();
   for (int r = 0; r < x.G; ++r) {
     atomicAdd_system(reinterpret_cast<unsigned long long*>(xbase(x, r) + off), 1ull);
   }
@@ -2502,23 +2515,30 @@ void do_iterations(Plan& P, int first, int count) {
       // all-reduce [bp | r2], identical update on every rank.
       T* bp = reinterpret_cast<T*>(P.bp.get());
       const long long cols = P.cols[0];
+      double* r2 = sharded_r2_slot(P);
       launch_fwd<T>(P, k, it);
       P.ctx->check_launch("sart_fwd(sharded)");
-      sharded_r2_kernel<T><<<1, kThreads, 0, P.ctx->stream>>>(P.partial.get(), P.fwd_blocks,
-                                                             bp + cols);
+      sharded_r2_kernel<<<1, kThreads, 0, P.ctx->stream>>>(P.partial.get(), P.fwd_blocks, r2);
       P.ctx->check_launch("sharded_r2_kernel");
       launch_back<T>(P, k, it);
       P.ctx->check_launch("sart_back(sharded)");
-      nccl_check(nccl().AllReduce(bp, bp, static_cast<std::size_t>(cols + 1),
+      // [bp] in the plan dtype and ||r_g||^2 in fp64, fused into one NCCL launch
+      nccl_check(nccl().GroupStart(), "ncclGroupStart");
+      nccl_check(nccl().AllReduce(bp, bp, static_cast<std::size_t>(cols),
                                   sizeof(T) == 4 ? ncclFloat32 : ncclFloat64, ncclSum,
                                   static_cast<ncclComm_t>(P.ctx->comm), P.ctx->stream),
                  "ncclAllReduce");
+      nccl_check(nccl().AllReduce(r2, r2, 1, ncclFloat64, ncclSum,
+                                  static_cast<ncclComm_t>(P.ctx->comm), P.ctx->stream),
+                 "ncclAllReduce(r2)");
+      nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
       sart_sharded_update_kernel<T><<<P.back_blocks, kThreads, 0, P.ctx->stream>>>(
-          reinterpret_cast<T*>(P.x[0].get()), bp, reinterpret_cast<const T*>(P.cinv[0].get()),
-          cols, P.pnorm.get(), P.opts.tol, P.opts.relaxation, P.history.get(), P.state.get(), it);
+          reinterpret_cast<T*>(P.x[0].get()), bp, r2,
+          reinterpret_cast<const T*>(P.cinv[0].get()), cols, P.pnorm.get(), P.opts.tol,
+          P.opts.relaxation, P.history.get(), P.state.get(), it);
       P.ctx->check_launch("sart_sharded_update_kernel");
-      sharded_stop_kernel<T><<<1, 1, 0, P.ctx->stream>>>(bp, cols, P.pnorm.get(), P.opts.tol,
-                                                        P.state.get(), it);
+      sharded_stop_kernel<<<1, 1, 0, P.ctx->stream>>>(r2, P.pnorm.get(), P.opts.tol,
+                                                      P.state.get(), it);
       P.ctx->check_launch("sharded_stop_kernel");
       continue;
     }
@@ -3489,10 +3509,33 @@ namespace {
 
 std::size_t align256(std::size_t v) { return (v + 255) & ~static_cast<std::size_t>(255); }
 
+// All-gather of the ranks' IPC handles plus one status byte each: every rank
+// fills its slot of a zeroed table (handle, status 1) -- or only zeros when its
+// local setup failed -- and one byte-wise sum over the communicator combines
+// them. Every rank of a peer-exchange plan calls this exactly once, whether or
+// not its own setup succeeded, so no rank can block the others.
+std::vector<unsigned char> exchange_table(Context* ctx, int G, int me,
+                                          const cudaIpcMemHandle_t* h) {
+  const std::size_t hs = sizeof(cudaIpcMemHandle_t);
+  std::vector<unsigned char> tab(static_cast<std::size_t>(G) * (hs + 1), 0);
+  if (h) {
+    std::memcpy(tab.data() + me * hs, h, hs);
+    tab[static_cast<std::size_t>(G) * hs + me] = 1;
+  }
+  DBuf<unsigned char> dt(tab.size());
+  SSB_CUDA(cudaMemcpyAsync(dt.get(), tab.data(), tab.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  nccl_check(nccl().AllReduce(dt.get(), dt.get(), tab.size(), ncclUint8, ncclSum,
+                              static_cast<ncclComm_t>(ctx->comm), ctx->stream),
+             "ncclAllReduce(ipc handles)");
+  ctx->copy(tab.data(), dt.get(), tab.size());
+  return tab;
+}
+
 // Exchange region of a peer-exchange rank (layout in plan.hpp). Ownership and
 // the reduce grid depend only on the column count, G and the SM count, so
 // every rank derives the same ones.
-void setup_exchange(Plan& P, int G, int me, bool emulated) {
+void setup_exchange(Plan& P, int G, int me, bool emulated, bool* joined) {
   Context* ctx = P.ctx;
   auto X = std::make_unique<PeerExchange>();
   X->G = G;
@@ -3511,29 +3554,34 @@ void setup_exchange(Plan& P, int G, int me, bool emulated) {
   X->off_xready = X->off_done + 64;
   X->off_dflag = X->off_xready + 64;
   X->bytes = align256(X->off_dflag + 64);
-  // plain cudaMalloc: pool (cudaMallocAsync) memory cannot be exported over IPC
-  SSB_CUDA(cudaMalloc(&X->region, X->bytes));
-  SSB_CUDA(cudaMemsetAsync(X->region, 0, X->bytes, ctx->stream));
-  X->local.alloc(4);
-  SSB_CUDA(cudaMemsetAsync(X->local.get(), 0, 4 * sizeof(long long), ctx->stream));
-  X->peers.alloc(G);
+  // Local setup first (allocation, IPC export). A failure here must not
+  // leave the other ranks blocked in the handle exchange below: it is
+  // reported through the exchange's status bytes and every rank fails alike.
   std::vector<char*> bases(G, nullptr);
-  bases[me] = static_cast<char*>(X->region);
-  if (!emulated && G > 1) {
-    // all-gather the IPC handles: each rank fills its slot of a zeroed table,
-    // one byte-wise sum over the communicator. Every rank zeroed its region
-    // before joining, so a mapped peer region is ready to use.
-    cudaIpcMemHandle_t h;
-    SSB_CUDA(cudaIpcGetMemHandle(&h, X->region));
-    std::vector<unsigned char> tab(static_cast<std::size_t>(G) * sizeof h, 0);
-    std::memcpy(tab.data() + me * sizeof h, &h, sizeof h);
-    DBuf<unsigned char> dt(tab.size());
-    SSB_CUDA(cudaMemcpyAsync(dt.get(), tab.data(), tab.size(), cudaMemcpyHostToDevice,
-                             ctx->stream));
-    nccl_check(nccl().AllReduce(dt.get(), dt.get(), tab.size(), ncclUint8, ncclSum,
-                                static_cast<ncclComm_t>(ctx->comm), ctx->stream),
-               "ncclAllReduce(ipc handles)");
-    ctx->copy(tab.data(), dt.get(), tab.size());
+  cudaIpcMemHandle_t h{};
+  std::string local_err;
+  try {
+    // plain cudaMalloc: pool (cudaMallocAsync) memory cannot be exported over IPC
+    SSB_CUDA(cudaMalloc(&X->region, X->bytes));
+    SSB_CUDA(cudaMemsetAsync(X->region, 0, X->bytes, ctx->stream));
+    X->local.alloc(4);
+    SSB_CUDA(cudaMemsetAsync(X->local.get(), 0, 4 * sizeof(long long), ctx->stream));
+    X->peers.alloc(G);
+    bases[me] = static_cast<char*>(X->region);
+    if (!emulated && G > 1) SSB_CUDA(cudaIpcGetMemHandle(&h, X->region));
+  } catch (const std::exception& e) {
+    local_err = e.what();
+  }
+  if (emulated || G == 1) {
+    if (!local_err.empty()) fail("peer exchange setup: " + local_err);
+  } else {
+    *joined = true;
+    std::vector<unsigned char> tab = exchange_table(ctx, G, me, local_err.empty() ? &h : nullptr);
+    const unsigned char* status = tab.data() + static_cast<std::size_t>(G) * sizeof h;
+    if (!local_err.empty()) fail("peer exchange setup: " + local_err);
+    for (int r = 0; r < G; ++r) {
+      if (status[r] != 1) fail("peer exchange setup failed on rank " + std::to_string(r));
+    }
     for (int r = 0; r < G; ++r) {
       if (r == me) continue;
       cudaIpcMemHandle_t hr;
@@ -3646,6 +3694,10 @@ void run_group(Plan* const* plans, int parts) {
 
 }
 
+Plan* make_sharded_plan_local(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t re,
+                              const ss_solve_options& o, int exchange, int emul_parts,
+                              int emul_rank, bool* joined);
+
 Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t re,
                         const ss_solve_options& o, int exchange, int emul_parts, int emul_rank) {
   if (exchange != SS_XCHG_NCCL && exchange != SS_XCHG_PEER) fail("plan: unknown exchange");
@@ -3655,6 +3707,26 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   } else if (!ctx->comm) {
     fail("plan: context has no NCCL communicator");
   }
+  // A real peer-exchange rank that fails before its handle exchange still
+  // joins it (with status 0), so the other ranks fail too instead of blocking.
+  const bool joins = exchange == SS_XCHG_PEER && emul_parts == 0 && ctx->nranks > 1;
+  bool joined = false;  // set once this rank took part in the handle exchange
+  try {
+    return make_sharded_plan_local(ctx, a, rb, re, o, exchange, emul_parts, emul_rank, &joined);
+  } catch (...) {
+    if (joins && !joined) {
+      try {
+        exchange_table(ctx, ctx->nranks, ctx->rank, nullptr);
+      } catch (...) {
+      }
+    }
+    throw;
+  }
+}
+
+Plan* make_sharded_plan_local(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t re,
+                              const ss_solve_options& o, int exchange, int emul_parts,
+                              int emul_rank, bool* joined) {
   if (rb < 0 || re > a->rows || rb > re) fail("plan: row range out of bounds");
   if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
   if (o.max_iters < 1) fail("sart_solve: max_iters must be >= 1");
@@ -3701,7 +3773,7 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
     P->back_blocks = occupancy_blocks<double>(*P, false);
   }
   alloc_common(*P);
-  if (exchange == SS_XCHG_NCCL) P->bp.alloc((a->cols + 1) * P->tsize());
+  if (exchange == SS_XCHG_NCCL) P->bp.alloc(sharded_r2_offset(a->cols, P->tsize()) + sizeof(double));
   // normalisers: rows from the local block, columns from the full matrix
   DBuf<double> rs_full(a->rows), cs_full(a->cols);
   // `a` may live on another context (stream): order the buffers' allocation
@@ -3731,8 +3803,8 @@ Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t r
   build_single(*P);
   if (P->tiled) size_single_grid(*P);
   if (exchange == SS_XCHG_PEER) {
-    if (emul_parts > 0) setup_exchange(*P, emul_parts, emul_rank, true);
-    else setup_exchange(*P, ctx->nranks, ctx->rank, false);
+    if (emul_parts > 0) setup_exchange(*P, emul_parts, emul_rank, true, joined);
+    else setup_exchange(*P, ctx->nranks, ctx->rank, false, joined);
   }
   ctx->sync();
   return P.release();

@@ -6,7 +6,8 @@ sm_100a library through its C ABI (include/symsplit_b200.h). Matrices live on
 the GPU; vectors cross the boundary as numpy float64 arrays.
 
 Differences from the reference, all deliberate:
-  * only Method.sart exists here (dense min-norm / CGLS are out of scope);
+  * Method.sart is the default (the reference defaults to dense_minnorm);
+    Method.cgls and Method.dense_minnorm also run on the device;
   * Matrix storage is always sparse on the device — `Matrix.dense(d)` stores
     the nonzero entries, so its fold follows the sparse (4-term) semantics
     (centro.cpp:109-130); for exactly centrosymmetric inputs both agree;
@@ -235,10 +236,18 @@ class Matrix:
         return d
 
     def coeff(self, i, j):
-        ptr, idx, val = self.to_csr()
-        seg = idx[ptr[i]:ptr[i + 1]]
-        k = np.searchsorted(seg, j)
-        return float(val[ptr[i] + k]) if k < len(seg) and seg[k] == j else 0.0
+        """matrix.cpp:44-50: stored value at 0-based (i, j), or 0."""
+        out = C.c_double()
+        _check(_lib().ss_matrix_coeff(self.h, int(i), int(j), C.byref(out)))
+        return out.value
+
+    def for_each(self, f):
+        """matrix.hpp:76-87: f(row, col, value) over the stored entries in
+        compressed-column order."""
+        outer, inner, val = self.to_csc()
+        for j in range(len(outer) - 1):
+            for k in range(outer[j], outer[j + 1]):
+                f(int(inner[k]), j, float(val[k]))
 
     def apply(self, x):
         x = _f64(x)
@@ -536,23 +545,40 @@ def ray_weights(ray4, grid: N.GridSpec, ctx: Optional[Context] = None):
     return cols, lens
 
 
-def enumerate_rays(cfg: N.ScanConfig):
-    """geometry.cpp:132-173 -> (rays[M,4] as (sx,sy,dx,dy), samples, pitch)"""
+def enumerate_rays(cfg: N.ScanConfig, grid: Optional[N.GridSpec] = None):
+    """geometry.cpp:132-173 -> (rays[M,4] as (sx,sy,dx,dy), samples, pitch);
+    with `grid` the reference's enumerate_rays(geometry, grid)."""
     cnt, samples, pitch = N.i64(), C.c_int(), C.c_double()
-    _check(_lib().ss_enumerate_rays(C.byref(cfg), None, C.byref(cnt), C.byref(samples),
-                                    C.byref(pitch)))
+
+    def call(out):
+        if grid is None:
+            return _lib().ss_enumerate_rays(C.byref(cfg), out, C.byref(cnt), C.byref(samples),
+                                            C.byref(pitch))
+        return _lib().ss_enumerate_rays_grid(C.byref(cfg), C.byref(grid), out, C.byref(cnt),
+                                             C.byref(samples), C.byref(pitch))
+    _check(call(None))
     rays = np.empty((cnt.value, 4))
-    _check(_lib().ss_enumerate_rays(C.byref(cfg), _dp(rays), C.byref(cnt), C.byref(samples),
-                                    C.byref(pitch)))
+    _check(call(_dp(rays)))
     return rays, samples.value, pitch.value
 
 
-def build_system(cfg: N.ScanConfig, parallelism: int = 0,
-                 ctx: Optional[Context] = None) -> CentroSystem:
-    """geometry.cpp:227-275 on the GPU: A with p = 0 and symmetry_tol = 0."""
+def build_system(geometry: N.ScanConfig, grid: Optional[N.GridSpec] = None,
+                 parallelism: int = 0, ctx: Optional[Context] = None) -> CentroSystem:
+    """geometry.cpp:227-275 on the GPU: A with p = 0 and symmetry_tol = 0.
+
+    build_system(geometry, grid, parallelism=0) is the reference signature
+    (geometry.hpp:118, bindings.cpp:246): `geometry`'s k / gamma / h_e / h_m /
+    l_m / n_p / obj_size with the caller's grid. build_system(cfg) uses
+    make_grid(cfg)."""
     ctx = ctx or default_context()
+    if isinstance(grid, int) and not isinstance(grid, bool):  # build_system(cfg, parallelism)
+        grid, parallelism = None, grid
     h = N.vp()
-    _check(_lib().ss_build_system(ctx.h, C.byref(cfg), parallelism, C.byref(h)))
+    if grid is None:
+        _check(_lib().ss_build_system(ctx.h, C.byref(geometry), parallelism, C.byref(h)))
+    else:
+        _check(_lib().ss_build_system_grid(ctx.h, C.byref(geometry), C.byref(grid), parallelism,
+                                           C.byref(h)))
     a = Matrix(h, ctx)
     return CentroSystem(a, np.zeros(a.shape[0]), 0.0)
 
@@ -755,8 +781,9 @@ class ShardedSartPlan(SartPlan):
     """Rows [row_begin, row_end) of one folded system on this rank. exchange
     "nccl": the back-projection is all-reduced over the context's NCCL
     communicator; "peer": the fused peer-memory exchange (K2 stores each
-    column chunk into its owner's buffer over NVLink, the last rank to arrive
-    reduces, updates and broadcasts x; no NCCL on the data path)."""
+    column's partial into its owner's receive row over NVLink; each owner sums
+    the ranks' partials of its own columns in rank order, applies the update
+    and pushes its x range into every replica; no NCCL on the data path)."""
 
     def __init__(self, ctx: Context, a: Matrix, row_begin: int, row_end: int,
                  opts: Optional[SolveOptions] = None, exchange: str = "nccl"):

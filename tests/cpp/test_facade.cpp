@@ -69,14 +69,30 @@ int main() {
     CHECK(thrown);
   }
   {  // BASELINE config 1 through the facade vs the oracle
-    ScanConfig cfg{10, degrees_to_radians(18.0), 2.0, 1e-4, 1.0, 128, 7e-4, 1.0, 64, 64};
-    CentroSystem sys = build_system(cfg);
-    CHECK(sys.a.rows() == 1280 && sys.a.stored() == 98032);
-    const GridSpec g = make_grid(cfg);
+    // the reference CLI's call shape (tools/main.cpp:160-162, :278, :406-407)
+    ScanConfig cfg;
+    cfg.geom.k = 10;
+    cfg.geom.gamma = degrees_to_radians(18.0);
+    cfg.geom.h_e = 2.0;
+    cfg.geom.h_m = 1e-4;
+    cfg.geom.l_m = 1.0;
+    cfg.geom.n_p = 128;
+    cfg.geom.obj_size = 1.0;
+    cfg.grid_nx = cfg.grid_ny = 64;
+    const int parallelism = 0;
+    const GridSpec grid = make_grid(cfg);
+    CentroSystem sys = build_system(cfg.geom, grid, parallelism);
+    CHECK(sys.a.rows() == 1280 && sys.a.stored() == 98032 && sys.symmetry_tol == 0.0);
     std::vector<double> ell(48);
     ss_random_ellipses(1000, 8, ell.data());
-    const Vector f_true = rasterize(ell, g);
-    sys.p = forward_project(sys.a, f_true);
+    std::vector<Ellipse> es;
+    for (int q = 0; q < 8; ++q) {
+      es.push_back({ell[6 * q], ell[6 * q + 1], ell[6 * q + 2], ell[6 * q + 3], ell[6 * q + 4],
+                    ell[6 * q + 5]});
+    }
+    const PhantomImage truth = rasterize(es, grid);
+    CHECK(truth.values.size() == 4096 && truth.max_value >= truth.min_value);
+    sys.p = forward_project(sys.a, truth.values);
     SolveOptions o;
     o.max_iters = 50;
     o.tol = 0.0;
@@ -93,6 +109,50 @@ int main() {
     oc.grid_nx = oc.grid_ny = 64;
     oracle::CentroSystem os = oracle::build_system(oc.geom, oracle::make_grid(oc));
     os.p = sys.p;
+    {  // Matrix::coeff / for_each / to_dense (matrix.hpp:53-81) on the built A
+      std::vector<int32_t> outer, inner;
+      Vector vals;
+      sys.a.to_csc(outer, inner, vals);
+      const auto& oa = os.a;
+      std::size_t k = 0;
+      bool order_ok = true;
+      sys.a.for_each([&](Index i, Index j, double v) {
+        order_ok = order_ok && k < vals.size() && inner[k] == i && vals[k] == v &&
+                   outer[static_cast<std::size_t>(j)] <= static_cast<int32_t>(k) &&
+                   static_cast<int32_t>(k) < outer[static_cast<std::size_t>(j) + 1];
+        ++k;
+      });
+      CHECK(order_ok && k == vals.size());
+      // coeff at stored entries and at a zero, bit for bit with the oracle
+      bool coeff_ok = true;
+      for (std::size_t q = 0; q < vals.size(); q += 997) {
+        Index j = 0;
+        while (outer[static_cast<std::size_t>(j) + 1] <= static_cast<int32_t>(q)) ++j;
+        coeff_ok = coeff_ok && sys.a.coeff(inner[q], j) == vals[q] &&
+                   oa.coeff(inner[q], j) == vals[q];
+      }
+      CHECK(coeff_ok);
+      CHECK(sys.a.coeff(0, 4095) == oa.coeff(0, 4095));
+      bool thrown = false;
+      try {
+        sys.a.coeff(1280, 0);
+      } catch (const Error& e) {
+        thrown = std::string(e.what()) == "matrix index out of range";
+      }
+      CHECK(thrown);
+      const DenseStorage d = sys.a.to_dense();
+      double dsum = 0.0, vsum = 0.0;
+      for (double v : d.data) dsum += v;
+      for (double v : vals) vsum += v;
+      CHECK(d.rows() == 1280 && d.cols() == 4096 && std::abs(dsum - vsum) <= 1e-9 * vsum);
+      CHECK(d(inner[0], 0) == vals[0]);
+      // enumerate_rays / GridSpec helpers with the reference's numbers
+      const RaySet rays = enumerate_rays(cfg.geom, grid);
+      CHECK(rays.count() == 1280 && rays.positions == 10 && rays.samples_per_position == 128);
+      const auto cc = grid.cell_center(1, 1);
+      const auto occ = oracle::make_grid(oc).cell_center(1, 1);
+      CHECK(cc.first == occ.first && cc.second == occ.second);
+    }
     oracle::SolveOptions oo;
     oo.max_iters = 50;
     oo.tol = 0.0;
@@ -106,7 +166,7 @@ int main() {
     CHECK(got.iterations == 50 && got.mode == Mode::split);
   }
   {  // geometry entry points (geometry.cpp:107-225) against the oracle, bit for bit
-    ScanConfig c = parse_scan_config("k 10\ngamma_deg 18\nh_e 2.0\nh_m 1e-4\n");
+    const ScanGeometry c = parse_scan_config("k 10\ngamma_deg 18\nh_e 2.0\nh_m 1e-4\n").geom;
     oracle::ScanGeometry og;
     og.k = 10;
     og.gamma = oracle::degrees_to_radians(18.0);
@@ -122,6 +182,15 @@ int main() {
       same = pos[i].x == opos[i].x && pos[i].y == opos[i].y;
     }
     CHECK(same);
+    bool bad = false;  // ScanGeometry::validate (geometry.cpp:94-105)
+    try {
+      ScanGeometry odd;
+      odd.k = 3;
+      odd.validate();
+    } catch (const Error& e) {
+      bad = std::string(e.what()) == "geometry: k must be even and >= 2 (mirror pairing)";
+    }
+    CHECK(bad);
     GridSpec g{4, 5, 0.1, 0.0, 1.0};
     const double xc = (2 - 0.5 - 0.5 * 4) * 0.1;
     const auto w = ray_weights(Ray{{xc, 3.0}, {xc, 0.0}}, g);

@@ -93,10 +93,11 @@ def test_verify_symmetry_built():
 
 
 # ------------------------------------------------------------------ SART parity
-@pytest.mark.parametrize("idx", [1, 2, 3])
+# config 3 at its full 200 iterations (and configs 4, 5): tests/test_golden_large.py
+@pytest.mark.parametrize("idx", [1, 2])
 def test_solve_split_f64(idx):
     w, cfg, a, csr, f_true, p, s = workload(idx)
-    iters = w.iters if idx < 3 else 10  # config 3: bounded oracle time (paired 16-bit fp64 path)
+    iters = w.iters
     if a is None:
         f1, f2 = O.fold_rows_csr(csr)
         p1, p2 = O.split_rhs(p)
@@ -117,10 +118,10 @@ def test_solve_split_f64(idx):
     assert abs(got.solution_norm - want_sn) <= TOL_F64 * want_sn
 
 
-@pytest.mark.parametrize("idx", [2, 3])
+@pytest.mark.parametrize("idx", [2])
 def test_solve_split_f32(idx):
     w, cfg, a, csr, f_true, p, s = workload(idx)
-    iters = w.iters if idx == 2 else 10  # config 3: bounded oracle time
+    iters = w.iters
     if a is None:
         f1, f2 = O.fold_rows_csr(csr)
         p1, p2 = O.split_rhs(p)

@@ -53,8 +53,11 @@ def test_no_gpu_fails_loudly():
 
 def test_default_options_match_reference():
     o = N.SolveOptionsC()
+    # a C caller's stack struct holds garbage: every field must be written
+    C.memset(C.byref(o), 0x5A, C.sizeof(o))
     N.load().ss_default_options(C.byref(o))
     assert (o.max_iters, o.tol, o.relaxation, o.parallelism, o.dtype) == (200, 1e-10, 1.0, 0, 0)
+    assert o.method == 0 and o.dense_cap == 0  # 0 = the reference's 5e7 cap
     d = P.SolveOptions()
     assert (d.max_iters, d.tol, d.relaxation, d.parallelism) == (200, 1e-10, 1.0, 0)
 

@@ -102,13 +102,14 @@ int run_build(const Args& a) {
   }
   const char* env = std::getenv("SYMSPLIT_PARALLEL");
   const int par = static_cast<int>(num(a, "parallel", env ? std::atof(env) : 0.0));
-  symsplit::CentroSystem sys = symsplit::build_system(cfg, par);
+  // the reference's call shape (tools/main.cpp:160-171)
+  const symsplit::GridSpec grid = symsplit::make_grid(cfg);
+  symsplit::CentroSystem sys = symsplit::build_system(cfg.geom, grid, par);
   const std::string phantom = a.get("phantom");
   if (!phantom.empty()) {
     if (phantom != "shepp-logan") throw Usage("--phantom: unknown phantom: " + phantom);
-    const auto grid = symsplit::make_grid(cfg);
-    sys.p = symsplit::forward_project(sys.a,
-                                      symsplit::rasterize(symsplit::shepp_logan_ellipses(), grid));
+    const symsplit::PhantomImage image = symsplit::rasterize(symsplit::shepp_logan_ellipses(), grid);
+    sys.p = symsplit::forward_project(sys.a, image.values);
   }
   if (a.has("out-matrix")) symsplit::write_matrix_market(sys.a, a.get("out-matrix"));
   if (a.has("out-rhs")) {
