@@ -86,25 +86,6 @@ struct Plan {
     if (fwd ? mir_f : mir_b) return stream_cs ? 5 : 4;
     return stream_cs ? 3 : 2;
   }
-  // TMA-fed ring kernels (ring.cuh) over the mirror-coded streams, per
-  // direction: chunk tables (first vector of each chunk, first chunk of each
-  // CTA) and the shared-memory slot geometry
-  bool ring_f = false, ring_b = false;
-  int ring_stages_f = 0, ring_stages_b = 0;
-  unsigned ring_slot_f = 0, ring_slot_b = 0, ring_offv_f = 0, ring_offv_b = 0;
-  unsigned ring_offh_f = 0, ring_offh_b = 0, ring_offm_f = 0, ring_offm_b = 0;
-  unsigned ring_offe_f = 0, ring_offe_b = 0, ring_tail_f = 0, ring_tail_b = 0;
-  int ring_uf_f = 4, ring_uf_b = 4;
-  int ring_threads = 512;      // CTA size of the ring kernels
-  bool ring_prefetch = false;  // L1 prefetch of the next round's gathers
-  bool ring_interleave = true; // CTA b streams chunks b, b+G, ... (one sweeping front)
-  std::int64_t ring_nchunk_f = 0, ring_nchunk_b = 0;
-  DBuf<char> ring_desc_f, ring_desc_b;   // RingDesc per chunk
-  DBuf<int> ring_cta_f, ring_cta_b;       // first chunk of every CTA
-  DBuf<int> ring_meta_f, ring_meta_b;     // int4 per vector {begin, first tile, first exception, 0}
-  // dynamic schedule of the paired kernels: contiguous nnz-balanced vector
-  // range per CTA (grabbed one at a time by its lane groups)
-  DBuf<int> dyn_f, dyn_b;
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;

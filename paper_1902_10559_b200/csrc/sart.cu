@@ -99,11 +99,6 @@ struct SartK {
   // row-sharded: K2 writes the partial back-projection to bp_out[0..cols);
   // K1's ||r_g||^2 goes to an fp64 slot behind it (one grouped all-reduce)
   T* bp_out;
-  // paired kernels, dynamic schedule: CTA b takes vectors [cv[b], cv[b+1])
-  // (contiguous, nnz-balanced), its lane groups grab them one at a time from
-  // a shared counter; nullptr: grid-stride over all vectors
-  const int* cvf;
-  const int* cvb;
   // graph WHILE-loop mode: the iteration index lives on the device; the last
   // block of K1 advances it and decides whether the loop body runs again
   int* iter;
@@ -240,17 +235,16 @@ __device__ __forceinline__ bool sys_on(const int* state, int idx) {
 
 // Fixed-order reduction of per-block partials by the last block of K1, then
 // the reference's check-before-update stopping rule (solvers.cpp:180-182).
-template <int NT = kThreads>  // the caller's CTA size
 __device__ void finish_norms(double* partial, int nblk, int nsr, const double* pnorm, double tol,
                              double* history, int hstride, int* state, int it) {
-  __shared__ double sh[NT];
+  __shared__ double sh[kThreads];  // every caller runs kThreads-thread CTAs
   for (int q = 0; q < nsr; ++q) {
     if (!sys_on(state, q)) continue;
     double s = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += NT) s += partial[q * nblk + b];
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partial[q * nblk + b];
     sh[threadIdx.x] = s;
     __syncthreads();
-    for (int o = NT / 2; o > 0; o >>= 1) {
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
       if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
       __syncthreads();
     }
@@ -761,17 +755,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const int n = static_cast<int>(k.rows0);
   const int* __restrict__ ptr = TL != 0 ? k.tpf : k.s[0].rp;  // tiled: padded pointer
   int g = static_cast<int>(group);
-  int gend = n;
-  const int gstep = static_cast<int>(ngroups);
-  __shared__ int ctr;
-  const bool dyn = k.cvf != nullptr;
-  if (dyn) {
-    const int b0 = __ldg(k.cvf + blockIdx.x);
-    gend = __ldg(k.cvf + blockIdx.x + 1);
-    g = b0 + static_cast<int>(threadIdx.x) / VS;
-    if (threadIdx.x == 0) ctr = b0 + kThreads / VS;
-    __syncthreads();
-  }
+  const int gend = n, gstep = static_cast<int>(ngroups);
   // the stream layout is constant: the first row's bounds load while the
   // previous pass drains (PDL), only its results wait for the dependency
   int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
@@ -790,14 +774,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
-    for (int gn; g < gend; g = gn) {
-      if (dyn) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&ctr, 1);
-        gn = __shfl_sync(mask, t, 0, VS);
-      } else {
-        gn = g + gstep;
-      }
+    for (; g < gend; g += gstep) {
+      const int gn = g + gstep;
       int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
       if (gn < gend) {  // next row's bounds, ahead of this row's dot product
         nbeg = __ldg(ptr + gn);
@@ -879,17 +857,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
   const int n = static_cast<int>(k.cols0);
   const int* __restrict__ ptr = TL != 0 ? k.tpb : k.s[0].cp;
   int g = static_cast<int>(group);
-  int gend = n;
-  const int gstep = static_cast<int>(ngroups);
-  __shared__ int ctr;
-  const bool dyn = k.cvb != nullptr;
-  if (dyn) {
-    const int b0 = __ldg(k.cvb + blockIdx.x);
-    gend = __ldg(k.cvb + blockIdx.x + 1);
-    g = b0 + static_cast<int>(threadIdx.x) / VS;
-    if (threadIdx.x == 0) ctr = b0 + kThreads / VS;
-    __syncthreads();
-  }
+  const int gend = n, gstep = static_cast<int>(ngroups);
   int beg = 0, end = 0, tf = 0, eb = 0, ee = 0;
   if (g < gend) {
     beg = __ldg(ptr + g);
@@ -900,14 +868,8 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
       ee = __ldg(k.epb + g + 1);
     }
   }
-  for (int gn; g < gend; g = gn) {
-    if (dyn) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&ctr, 1);
-      gn = __shfl_sync(mask, t, 0, VS);
-    } else {
-      gn = g + gstep;
-    }
+  for (; g < gend; g += gstep) {
+    const int gn = g + gstep;
     int nbeg = 0, nend = 0, ntf = 0, neb = 0, nee = 0;
     if (gn < gend) {
       nbeg = __ldg(ptr + gn);
@@ -953,8 +915,6 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     ee = nee;
   }
 }
-
-#include "ring.cuh"
 
 // ------------------------------------------------------------ single-system tiled kernels
 // One system (sart_solve, the per-rank system of a 2-GPU run, a row shard) on
@@ -2182,8 +2142,6 @@ SartK<T> make_args(Plan& P) {
     k.cond = P.cond;
   }
   k.max_iters = P.opts.max_iters;
-  k.cvf = P.dyn_f.get();
-  k.cvb = P.dyn_b.get();
   return k;
 }
 
@@ -2284,73 +2242,7 @@ void launch_pdl(PairFn<T> fn, int grid, int block, std::size_t smem, cudaStream_
 }
 
 template <class T>
-using RingFn = void (*)(SartK<T>, int, RingArgs);
-
-// the ring kernel of a plan direction, or nullptr when that shape is not
-// instantiated (the plan then keeps the register-streamed pair kernel)
-template <class T>
-RingFn<T> ring_kernel(const Plan& P, bool fwd) {
-  const int vs = fwd ? P.vs_fwd : P.vs_back;
-  const int uf = fwd ? P.ring_uf_f : P.ring_uf_b;
-  const bool u16 = fwd ? P.c16f : P.c16b;
-  const int nt = P.ring_threads;
-#define SSB_RING(V, U, N)                                                                      \
-  if (vs == V && uf == U && nt == N) {                                                         \
-    if (u16) return fwd ? sart_ring_kernel<T, V, U, true, true, N> : sart_ring_kernel<T, V, U, true, false, N>; \
-    return fwd ? sart_ring_kernel<T, V, U, false, true, N> : sart_ring_kernel<T, V, U, false, false, N>; \
-  }
-  SSB_RING(8, 2, 512) SSB_RING(16, 2, 512) SSB_RING(32, 2, 512)
-  SSB_RING(8, 4, 512) SSB_RING(16, 4, 512) SSB_RING(32, 4, 512)
-  if constexpr (sizeof(T) == 4) {
-    SSB_RING(8, 2, 1024) SSB_RING(16, 2, 1024) SSB_RING(32, 2, 1024)
-  }
-#undef SSB_RING
-  return nullptr;
-}
-
-template <class T>
-RingArgs ring_args(const Plan& P, bool fwd) {
-  RingArgs r{};
-  r.desc = reinterpret_cast<const RingDesc*>(fwd ? P.ring_desc_f.get() : P.ring_desc_b.get());
-  r.cta_chunk = fwd ? P.ring_cta_f.get() : P.ring_cta_b.get();
-  r.vmeta = reinterpret_cast<const int4*>(fwd ? P.ring_meta_f.get() : P.ring_meta_b.get());
-  r.epi = reinterpret_cast<const unsigned char*>(fwd ? P.pe.get() : P.cc.get());
-  r.stages = fwd ? P.ring_stages_f : P.ring_stages_b;
-  r.off_v = fwd ? P.ring_offv_f : P.ring_offv_b;
-  r.off_h = fwd ? P.ring_offh_f : P.ring_offh_b;
-  r.off_m = fwd ? P.ring_offm_f : P.ring_offm_b;
-  r.off_e = fwd ? P.ring_offe_f : P.ring_offe_b;
-  r.stage_bytes = fwd ? P.ring_slot_f : P.ring_slot_b;
-  r.evict_first = P.stream_cs ? 1 : 0;
-  r.prefetch = P.ring_prefetch ? 1 : 0;
-  r.nchunk = static_cast<int>(fwd ? P.ring_nchunk_f : P.ring_nchunk_b);
-  r.interleave = P.ring_interleave ? 1 : 0;
-  return r;
-}
-
-template <class T>
-void launch_ring(Plan& P, const SartK<T>& k, int it, bool fwd) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(fwd ? P.fwd_blocks : P.back_blocks);
-  cfg.blockDim = dim3(P.ring_threads);
-  cfg.dynamicSmemBytes = static_cast<std::size_t>(fwd ? P.ring_stages_f : P.ring_stages_b) *
-                             (fwd ? P.ring_slot_f : P.ring_slot_b) +
-                         (fwd ? P.ring_tail_f : P.ring_tail_b);
-  cfg.stream = P.ctx->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  SSB_CUDA(cudaLaunchKernelEx(&cfg, ring_kernel<T>(P, fwd), k, it, ring_args<T>(P, fwd)));
-}
-
-template <class T>
 void launch_pair(Plan& P, const SartK<T>& k, int it, bool fwd) {
-  if (fwd ? P.ring_f : P.ring_b) {
-    launch_ring<T>(P, k, it, fwd);
-    return;
-  }
   int smem = 0;
   const PairFn<T> fn = pair_kernel<T>(P, fwd, &smem);
   const void* hot = nullptr;
@@ -3111,26 +3003,16 @@ std::string Plan::describe() const {
          std::to_string(uf_fwd) + ", " + std::to_string(layout_mode(true)) + ">";
     bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + std::to_string(layout_mode(false)) + ">";
-    const auto rk = [&](bool f) {
-      return "sart_ring_kernel<" + std::string(t) + ", " + std::to_string(f ? vs_fwd : vs_back) +
-             ", " + std::to_string(f ? ring_uf_f : ring_uf_b) + ", " +
-             ((f ? c16f : c16b) ? "true" : "false") + ", " + (f ? "true" : "false") + ", " +
-             std::to_string(ring_threads) + ">";
-    };
-    if (ring_f) fk = rk(true);
-    if (ring_b) bk = rk(false);
   }
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
-  char buf[1024];
+  char buf[768];
   std::snprintf(buf, sizeof buf,
                 "{\"layout\": \"%s\", \"dtype\": \"%s\", \"nsys\": %d, \"nrhs\": %d, "
                 "\"vs_fwd\": %d, \"uf_fwd\": %d, \"vs_back\": %d, \"uf_back\": %d, "
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
-                "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s, "
-                "\"ring\": [%d, %d], \"ring_stages\": [%d, %d], \"ring_slot_bytes\": [%u, %u], "
-                "\"ring_chunks\": [%lld, %lld]}",
+                "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s}",
                 sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
                         : (paired ? (tiled ? (mir_f || mir_b ? "paired-tiled-u16-mirror"
                                                                     : (c16f || c16b ? "paired-tiled-u16" : "paired-tiled"))
@@ -3139,9 +3021,7 @@ std::string Plan::describe() const {
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
-                graph ? "true" : "false", ring_f ? 1 : 0, ring_b ? 1 : 0, ring_stages_f,
-                ring_stages_b, ring_slot_f, ring_slot_b, static_cast<long long>(ring_nchunk_f),
-                static_cast<long long>(ring_nchunk_b));
+                graph ? "true" : "false");
   return buf;
 }
 
@@ -3412,180 +3292,6 @@ void build_paired_t(Plan& P) {
   P.ctx->sync();
 }
 
-// Chunk descriptors and slot geometry of the TMA ring kernels (ring.cuh) for
-// one direction of a mirror-coded paired plan: consecutive vectors packed into
-// chunks of <= cap entries, <= cap/(2 VS) tiles and <= 512 vectors (a chunk
-// holds at least one whole vector); per chunk the 16-byte-aligned byte range
-// of every array the producer copies; then one contiguous run of chunks per
-// CTA (one CTA per SM), balanced by streamed bytes plus a per-vector cost.
-template <class T>
-void build_ring_dir(Plan& P, bool fwd) {
-  if (!ring_kernel<T>(P, fwd)) return;  // shape not instantiated: pair kernel
-  const std::int64_t n = fwd ? P.rows[0] : P.cols[0];
-  const int vs = fwd ? P.vs_fwd : P.vs_back;
-  const bool u16 = fwd ? P.c16f : P.c16b;
-  const int hs = fwd ? P.hs_f : P.hs_b;
-  const std::int64_t isz = u16 ? 2 : 4, tsz = sizeof(T), hsz = 4 * hs;
-  const std::int64_t esz = (fwd ? 4 : 2) * tsz;  // epilogue operands per vector
-  std::vector<int> ptr(n + 1), tfs(n + 1), ep(n + 1, 0);
-  P.ctx->copy(ptr.data(), (fwd ? P.tptr_f : P.tptr_b).get(), (n + 1) * sizeof(int));
-  P.ctx->copy(tfs.data(), (fwd ? P.tfirst_f : P.tfirst_b).get(), (n + 1) * sizeof(int));
-  const DBuf<int>& eptr = fwd ? P.eptr_f : P.eptr_b;
-  if (eptr.get()) P.ctx->copy(ep.data(), eptr.get(), (n + 1) * sizeof(int));
-  std::int64_t cap = env_int("SSB_RING_CAP", sizeof(T) == 4 ? 4096 : 2048);
-  std::int64_t maxlen = 0, maxt = 0;
-  for (std::int64_t v = 0; v < n; ++v) {
-    maxlen = std::max<std::int64_t>(maxlen, ptr[v + 1] - ptr[v]);
-    maxt = std::max<std::int64_t>(maxt, tfs[v + 1] - tfs[v]);
-  }
-  cap = std::max<std::int64_t>(cap, (maxlen + 63) & ~63LL);
-  // vectors per chunk: twice the average fill, so the metadata / epilogue
-  // regions stay small next to the stream (shared memory left to L1)
-  const double avg = n > 0 ? std::max(1.0, static_cast<double>(ptr[n]) / n) : 1.0;
-  const std::int64_t capv = std::max(1, env_int("SSB_RING_CAPV", static_cast<int>(std::min(
-      512.0, std::max(16.0, 2.0 * cap / avg + 8.0)))));
-  const std::int64_t capt = std::max<std::int64_t>(maxt, std::max<std::int64_t>(1, cap / (2 * vs)));
-  std::vector<RingDesc> desc;
-  const auto lo = [](std::int64_t b) { return b & ~15LL; };
-  const auto hi = [](std::int64_t b) { return (b + 15) & ~15LL; };
-  for (std::int64_t v = 0; v < n;) {
-    std::int64_t e = v + 1;
-    while (e < n && e - v < capv && ptr[e + 1] - ptr[v] <= cap && tfs[e + 1] - tfs[v] <= capt) ++e;
-    RingDesc d{};
-    d.vbeg = static_cast<int>(v);
-    d.vend = static_cast<int>(e);
-    d.i0 = lo(ptr[v] * isz);
-    d.ib = static_cast<unsigned>(hi(ptr[e] * isz) - d.i0);
-    d.v0 = lo(ptr[v] * tsz);
-    d.vb = static_cast<unsigned>(hi(ptr[e] * tsz) - d.v0);
-    d.h0 = lo(tfs[v] * hsz);
-    d.hb = static_cast<unsigned>(hi(tfs[e] * hsz) - d.h0);
-    d.e0 = lo(v * esz);
-    d.eb = static_cast<unsigned>(hi(e * esz) - d.e0);
-    desc.push_back(d);
-    v = e;
-  }
-  const std::int64_t nch = static_cast<std::int64_t>(desc.size());
-  const auto al = [](std::int64_t b) { return (b + 32 + 127) & ~127LL; };  // + alignment slop
-  const std::int64_t ri = al(cap * isz), rv = al(cap * tsz), rh = al(capt * hsz);
-  const std::int64_t rm = al((capv + 1) * 16), re = al(capv * esz);
-  const std::int64_t slot = ri + rv + rh + rm + re;
-  int maxsm = 0;
-  SSB_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.ctx->device));
-  const int static_bytes = 2048;  // barriers, slot bookkeeping, reduction scratch
-  // CTAs: one per SM, never more than chunks; contiguous byte-balanced runs
-  const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(P.ctx->sm_count, nch)));
-  std::vector<double> wsum(nch + 1, 0.0);
-  for (std::int64_t c = 0; c < nch; ++c) {
-    const RingDesc& d = desc[c];
-    wsum[c + 1] = wsum[c] + d.ib + d.vb + d.hb + (d.vend - d.vbeg) * 48.0;
-  }
-  std::vector<int> cta(grid + 1, 0);
-  std::int64_t c = 0;
-  for (int b = 1; b < grid; ++b) {
-    const double target = wsum[nch] * b / grid;
-    while (c < nch && wsum[c] < target) ++c;
-    cta[b] = static_cast<int>(std::max<std::int64_t>(cta[b - 1], c));
-  }
-  cta[grid] = static_cast<int>(nch);
-  // behind the slots: two ints per chunk of the longest CTA run (+ 1)
-  int maxrun = 0;
-  for (int b = 0; b < grid; ++b) maxrun = std::max(maxrun, cta[b + 1] - cta[b]);
-  if (P.ring_interleave) maxrun = static_cast<int>((nch + grid - 1) / grid);
-  const std::int64_t tail = ((2 * (static_cast<std::int64_t>(maxrun) + 1)) * 4 + 127) & ~127LL;
-  int stages = std::min(kRingMaxStages, std::max(2, env_int("SSB_RING_STAGES", 4)));
-  while (stages > 2 && stages * slot + tail > maxsm - static_bytes) --stages;
-  if (stages * slot + tail > maxsm - static_bytes) fail("plan: ring slot exceeds shared memory");
-  std::vector<int> meta(4 * (n + 1), 0);
-  for (std::int64_t v = 0; v <= n; ++v) {
-    meta[4 * v] = ptr[v];
-    meta[4 * v + 1] = tfs[v];
-    meta[4 * v + 2] = ep[v];
-  }
-  DBuf<char>& dd = fwd ? P.ring_desc_f : P.ring_desc_b;
-  DBuf<int>& dct = fwd ? P.ring_cta_f : P.ring_cta_b;
-  DBuf<int>& dm = fwd ? P.ring_meta_f : P.ring_meta_b;
-  dd.alloc(nch * sizeof(RingDesc));
-  dct.alloc(grid + 1);
-  dm.alloc(4 * (n + 1));
-  SSB_CUDA(cudaMemcpyAsync(dd.get(), desc.data(), nch * sizeof(RingDesc), cudaMemcpyHostToDevice,
-                           P.ctx->stream));
-  SSB_CUDA(cudaMemcpyAsync(dct.get(), cta.data(), (grid + 1) * sizeof(int), cudaMemcpyHostToDevice,
-                           P.ctx->stream));
-  SSB_CUDA(cudaMemcpyAsync(dm.get(), meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice,
-                           P.ctx->stream));
-  P.ctx->sync();
-  (fwd ? P.ring_nchunk_f : P.ring_nchunk_b) = nch;
-  (fwd ? P.ring_stages_f : P.ring_stages_b) = stages;
-  (fwd ? P.ring_slot_f : P.ring_slot_b) = static_cast<unsigned>(slot);
-  (fwd ? P.ring_tail_f : P.ring_tail_b) = static_cast<unsigned>(tail);
-  (fwd ? P.ring_offv_f : P.ring_offv_b) = static_cast<unsigned>(ri);
-  (fwd ? P.ring_offh_f : P.ring_offh_b) = static_cast<unsigned>(ri + rv);
-  (fwd ? P.ring_offm_f : P.ring_offm_b) = static_cast<unsigned>(ri + rv + rh);
-  (fwd ? P.ring_offe_f : P.ring_offe_b) = static_cast<unsigned>(ri + rv + rh + rm);
-  (fwd ? P.fwd_blocks : P.back_blocks) = grid;
-  (fwd ? P.ring_f : P.ring_b) = true;
-  // the slots' share of the unified L1 / shared memory: just enough carveout
-  RingFn<T> fn = ring_kernel<T>(P, fwd);
-  const int dyn = static_cast<int>(stages * slot + tail);
-  SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-  int smem_per_sm = 0;
-  SSB_CUDA(cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                                  P.ctx->device));
-  const int pct = std::min(100, static_cast<int>((dyn + static_bytes + 1024) * 100LL / smem_per_sm + 1));
-  SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                env_int("SSB_RING_CARVEOUT", pct)));
-}
-
-// Dynamic schedule of the paired kernels (SSB_DYN=1): every CTA of the grid
-// owns a contiguous run of vectors balanced by padded entries plus a
-// per-vector cost, and its lane groups take them one at a time (adjacent rays
-// / voxels share an SM's L1; no tail of groups with one vector more than the
-// rest, as with the grid-stride schedule).
-void build_dyn_dir(Plan& P, bool fwd) {
-  const std::int64_t n = fwd ? P.rows[0] : P.cols[0];
-  const int grid = fwd ? P.fwd_blocks : P.back_blocks;
-  const DBuf<int>& tp = fwd ? P.tptr_f : P.tptr_b;
-  std::vector<int> ptr(n + 1);
-  P.ctx->copy(ptr.data(), tp.get(), (n + 1) * sizeof(int));
-  const double cost = env_int("SSB_DYN_COST", 16);  // entries-equivalent per vector
-  const double total = ptr[n] + cost * n;
-  std::vector<int> cv(grid + 1, 0);
-  std::int64_t v = 0;
-  for (int b = 1; b < grid; ++b) {
-    const double target = total * b / grid;
-    while (v < n && ptr[v] + cost * v < target) ++v;
-    cv[b] = static_cast<int>(v);
-  }
-  cv[grid] = static_cast<int>(n);
-  DBuf<int>& d = fwd ? P.dyn_f : P.dyn_b;
-  d.alloc(grid + 1);
-  SSB_CUDA(cudaMemcpyAsync(d.get(), cv.data(), (grid + 1) * sizeof(int), cudaMemcpyHostToDevice,
-                           P.ctx->stream));
-  P.ctx->sync();
-}
-
-void build_dyn(Plan& P) {
-  if (!P.paired || !P.tiled || P.nrhs != 1 || P.sharded || env_int("SSB_DYN", 1) == 0) return;
-  if (!P.ring_f) build_dyn_dir(P, true);
-  if (!P.ring_b) build_dyn_dir(P, false);
-}
-
-// TMA ring kernels for the mirror-coded paired streams (SSB_RING=0: the
-// register-streamed pair kernels)
-template <class T>
-void build_ring(Plan& P) {
-  if (!P.paired || !P.tiled || P.nrhs != 1 || P.sharded || env_int("SSB_RING", 0) == 0) return;
-  P.ring_threads = env_int("SSB_RING_THREADS", 512);
-  const int uf = P.ring_threads >= 1024 ? 2 : 4;
-  P.ring_uf_f = env_int("SSB_RING_UF_FWD", uf);
-  P.ring_uf_b = env_int("SSB_RING_UF_BACK", uf);
-  P.ring_prefetch = env_int("SSB_RING_PF", 0) != 0;
-  P.ring_interleave = env_int("SSB_RING_IL", 1) != 0;
-  if (P.mir_f) build_ring_dir<T>(P, true);
-  if (P.mir_b) build_ring_dir<T>(P, false);
-}
-
 // single-system plans: tiled streams when enabled (else the plain CSR/CSC kernels)
 void build_single(Plan& P) {
   if (!P.tiled) return;
@@ -3741,9 +3447,6 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->back_blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(
         occupancy_pair_blocks(*P, false),
         (static_cast<long long>(P->cols[0]) * P->vs_back + kThreads - 1) / kThreads)));
-    if (o.dtype == SS_F32) build_ring<float>(*P);
-    else build_ring<double>(*P);
-    build_dyn(*P);
     if (static_cast<std::size_t>(P->fwd_blocks) * P->nsys * P->nrhs > P->partial.size()) {
       P->partial.alloc(static_cast<std::size_t>(P->fwd_blocks) * P->nsys * P->nrhs);
     }
