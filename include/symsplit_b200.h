@@ -125,6 +125,9 @@ int ss_matrix_from_triplets(ss_ctx_t ctx, int64_t rows, int64_t cols, int64_t co
                             const int32_t* row, const int32_t* col, const double* values,
                             ss_matrix_t* out);
 int ss_matrix_destroy(ss_matrix_t a);
+/* ss_solve_split keeps the fold of its matrix and the SART plan over it on the
+ * (immutable) matrix handle for the next call; this frees them early */
+int ss_matrix_release_cache(ss_matrix_t a);
 int ss_matrix_shape(ss_matrix_t a, int64_t* rows, int64_t* cols, int64_t* stored);
 /* replaces Matrix::nonzeros / fill_ratio (matrix.cpp:28-42) */
 int ss_matrix_nonzeros(ss_matrix_t a, int64_t* out);
@@ -270,6 +273,10 @@ int ss_plan_describe(ss_plan_t plan, char* buf, int64_t cap);
 /* time `iters` bare iterations of the loop with CUDA events on the context
  * stream (per-kernel split: fwd_ms = forward kernels, back_ms = back kernels) */
 int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms);
+/* in-loop time of one SART kernel (fwd != 0: K1, else K2): `reps` launches back
+ * to back with the loop's launch configuration, events around the batch;
+ * ms = time per launch. Resets the plan. */
+int ss_plan_time_kernel(ss_plan_t plan, int fwd, int reps, float* ms);
 
 /* ------------------------------------------------------------ row-sharded multi-GPU */
 /* One process per GPU. Ranks r0..r0+n-1 of an NCCL communicator share one

@@ -78,6 +78,7 @@ SIGNATURES = {
     "ss_matrix_download_csc": (C.c_int, [vp, i32p, i32p, dp]),
     "ss_matrix_apply": (C.c_int, [vp, dp, dp]),
     "ss_matrix_coeff": (C.c_int, [vp, C.c_int64, C.c_int64, dp]),
+    "ss_matrix_release_cache": (C.c_int, [vp]),
     "ss_matrix_apply_transpose": (C.c_int, [vp, dp, dp]),
     "ss_parse_scan_config": (C.c_int, [C.c_char_p, C.POINTER(ScanConfig)]),
     "ss_make_grid": (C.c_int, [C.POINTER(ScanConfig), C.POINTER(GridSpec)]),
@@ -124,6 +125,7 @@ SIGNATURES = {
     "ss_plan_solution_device": (vp, [vp, C.c_int]),
     "ss_plan_stats": (C.c_int, [vp, i64p, i64p, C.POINTER(C.c_int)]),
     "ss_plan_profile": (C.c_int, [vp, C.c_int, fp, fp]),
+    "ss_plan_time_kernel": (C.c_int, [vp, C.c_int, C.c_int, fp]),
     "ss_plan_kernel_bytes": (C.c_int, [vp, i64p, i64p]),
     "ss_plan_describe": (C.c_int, [vp, C.c_char_p, i64]),
     "ss_nccl_unique_id": (C.c_int, [vp]),

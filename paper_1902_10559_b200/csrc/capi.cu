@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <limits>
+#include <mutex>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -179,6 +181,60 @@ void split_device(ssb::Matrix& a, const double* p_dev, std::int64_t m, double to
   tr.mark("  split_rhs + fills");
 }
 
+}  // namespace
+
+namespace ssb {
+// solve_split's per-matrix cache (Matrix::solve_cache). A matrix handle is
+// immutable, so its fold (the reference recomputes it every call,
+// centro.cpp:144-156) and the SART plan over A1/A2 (normalisers, CSC, paired
+// streams, captured loop) are derived once and reused; a call with new options
+// rebuilds the plan only. The symmetry report is kept independent of the
+// tolerance (the fold is computed with an unbounded one) and each call applies
+// its own symmetry_tol. Calls on one matrix serialise on `mu`.
+struct SolveCache {
+  std::mutex mu;
+  bool folded = false;
+  ss_symmetry_report rep{};
+  std::unique_ptr<Matrix> a1, a2;
+  std::unique_ptr<Plan> plan;
+  ss_solve_options plan_opts{};
+};
+}  // namespace ssb
+
+namespace {
+
+bool same_plan_options(const ss_solve_options& a, const ss_solve_options& b) {
+  return a.max_iters == b.max_iters && a.tol == b.tol && a.relaxation == b.relaxation &&
+         a.dtype == b.dtype;
+}
+
+// fold of A for solve_split, from the matrix's cache (computed on first use)
+ssb::SolveCache& folded_cache(ssb::Matrix& a, double tol, std::unique_lock<std::mutex>& lk) {
+  if (!a.solve_cache) a.solve_cache = std::make_shared<ssb::SolveCache>();
+  ssb::SolveCache& C = *a.solve_cache;
+  lk = std::unique_lock<std::mutex>(C.mu);
+  if (tol < 0) ssb::fail("verify_symmetry: tol must be non-negative");
+  if (!C.folded) {
+    ssb::Matrix *x = nullptr, *y = nullptr;
+    const ss_symmetry_report r =
+        ssb::fold_checked(a, std::numeric_limits<double>::max(), x, y);
+    if (!r.holds) {  // odd shape (or a non-finite violation): nothing to cache
+      ss_symmetry_report q = r;
+      throw ssb::Failure(SS_ERR_SYMMETRY, symmetry_message("split_system", q, tol));
+    }
+    C.a1.reset(x);
+    C.a2.reset(y);
+    C.rep = r;
+    C.folded = true;
+  }
+  if (!(C.rep.max_violation <= tol)) {
+    ss_symmetry_report q = C.rep;
+    q.holds = 0;
+    throw ssb::Failure(SS_ERR_SYMMETRY, symmetry_message("split_system", q, tol));
+  }
+  return C;
+}
+
 ssb::Grid to_grid(const ss_grid_spec* g) {
   need(g, "grid");
   ssb::Grid o;
@@ -284,6 +340,14 @@ int ss_matrix_from_triplets(ss_ctx_t h, int64_t rows, int64_t cols, int64_t coun
     need(out, "out");
     use_device(ctx);
     *out = wrap(ssb::matrix_from_triplets_host(ctx, rows, cols, count, row, col, values));
+  });
+}
+
+int ss_matrix_release_cache(ss_matrix_t a) {
+  return guarded([&] {
+    ssb::Matrix* m = M(a);
+    use_device(m->ctx);
+    m->solve_cache.reset();
   });
 }
 
@@ -676,8 +740,18 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
     const double t0 = now();
     auto dp = to_device(c, p, m);
     tr.mark("h2d p");
-    SplitOut o;
-    split_device(*A, dp.get(), m, symmetry_tol, o, nullptr);
+    if (m != A->rows) ssb::fail("split_system: right-hand side length does not match rows");
+    // the fold of A comes from the matrix's cache (first call: computed and kept)
+    std::unique_lock<std::mutex> lk;
+    ssb::SolveCache& C = folded_cache(*A, symmetry_tol, lk);
+    struct {
+      ssb::Matrix* a1;
+      ssb::Matrix* a2;
+      ssb::DBuf<double> p1, p2;
+    } o{C.a1.get(), C.a2.get(), {}, {}};
+    o.p1.alloc(m / 2);
+    o.p2.alloc(m / 2);
+    ssb::split_rhs_dev(c, dp.get(), o.p1.get(), o.p2.get(), m / 2);
     c->sync();
     const double split_seconds = now() - t0;
     tr.mark("split_system");
@@ -724,7 +798,7 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       ss_solve_report rb[2] = {};
       int code = SS_OK;
       if (dense) {  // the two branches concurrently (the reference's two threads)
-        ssb::Matrix* am[2] = {o.a1.get(), o.a2.get()};
+        ssb::Matrix* am[2] = {o.a1, o.a2};
         const double* pm[2] = {o.p1.get(), o.p2.get()};
         double* fm[2] = {f1.get(), f2.get()};
         double secs[2] = {0.0, 0.0};
@@ -738,7 +812,7 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       if (cgls) {
         // both systems in one loop over the paired streams (independent scalars
         // and stop tests), or concurrent single-system solves on two streams
-        ssb::Matrix* am[2] = {o.a1.get(), o.a2.get()};
+        ssb::Matrix* am[2] = {o.a1, o.a2};
         const double* pm[2] = {o.p1.get(), o.p2.get()};
         double* fm[2] = {f1.get(), f2.get()};
         int codes[2] = {SS_OK, SS_OK};
@@ -746,7 +820,7 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
         const char* e = std::getenv("SSB_CGLS_PAIRED");
         const bool paired = e && *e ? *e != '0' : o.a1->nnz >= 1000000;
         if (paired) {
-          ssb::cgls_device_paired(o.a1.get(), o.a2.get(), pm, *opts, fm, rb, errs, codes);
+          ssb::cgls_device_paired(o.a1, o.a2, pm, *opts, fm, rb, errs, codes);
         } else {
           ssb::cgls_device_pair(am, pm, *opts, fm, rb, errs, codes);
         }
@@ -775,7 +849,14 @@ int ss_solve_split(ss_matrix_t a, const double* p, int64_t m, double symmetry_to
       if (report) *report = rep;
       return;
     }
-    std::unique_ptr<ssb::Plan> P(ssb::make_plan(c, o.a1.get(), o.a2.get(), *opts, 1, false));
+    // the SART plan over A1/A2 (normalisers, CSC, paired streams, captured
+    // loop) is cached with the fold; new options rebuild it
+    if (!C.plan || !same_plan_options(C.plan_opts, *opts)) {
+      C.plan.reset();
+      C.plan.reset(ssb::make_plan(c, o.a1, o.a2, *opts, 1, true));
+      C.plan_opts = *opts;
+    }
+    ssb::Plan* P = C.plan.get();
     tr.mark("plan (csc, norms, graph)");
     for (int s = 0; s < 2; ++s) {
       if (P->empty_rows[s]) errs[s] = "sart_solve: matrix has no nonzero rows";
@@ -1022,6 +1103,15 @@ int ss_plan_profile(ss_plan_t plan, int iters, float* fwd_ms, float* back_ms) {
     need(fwd_ms, "fwd_ms");
     need(back_ms, "back_ms");
     P->profile(iters, fwd_ms, back_ms);
+  });
+}
+
+int ss_plan_time_kernel(ss_plan_t plan, int fwd, int reps, float* ms) {
+  return guarded([&] {
+    ssb::Plan* P = PL(plan);
+    use_device(P->ctx);
+    need(ms, "ms");
+    P->time_kernel(fwd != 0, reps, ms);
   });
 }
 

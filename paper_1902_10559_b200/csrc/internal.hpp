@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <memory>
 #include <vector>
 
 #include "../../include/symsplit_b200.h"
@@ -166,6 +167,9 @@ struct Matrix {
   bool has_f32 = false;
   DBuf<float> val32, cval32;
   DBuf<int> csc_perm;  // CSR position of each CSC entry (kept on request)
+  // solve_split's derived data of this (immutable) matrix -- its fold A1/A2
+  // and the paired SART plan over them -- kept for the next call (capi.cu)
+  std::shared_ptr<struct SolveCache> solve_cache;
 
   void ensure_csc(bool keep_perm = false);
   // CSC of a matrix with ref's exact CSR pattern: ref's ordering, own values

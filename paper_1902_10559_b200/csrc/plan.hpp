@@ -117,6 +117,7 @@ struct Plan {
   void get_history(int which, int slice, double* h, int* len);
   void recombine(double* f_slice_major);
   void profile(int iters, float* fwd_ms, float* back_ms);
+  void time_kernel(bool fwd, int reps, float* ms);
   void stats(std::int64_t* mbytes, std::int64_t* vbytes, int* kernels) const;
   void kernel_bytes(std::int64_t* fwd, std::int64_t* back) const;
   std::string describe() const;

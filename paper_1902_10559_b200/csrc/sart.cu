@@ -2952,6 +2952,38 @@ void Plan::profile(int iters, float* fwd_ms, float* back_ms) {
   *back_ms = tb;
 }
 
+// One SART kernel launched `reps` times back to back on the plan stream (the
+// same launch configuration and programmatic dependent launch as inside the
+// loop), CUDA events around the batch: the kernel's in-loop time per launch
+// without per-launch events between launches. The iterate changes (K2) but
+// the work per launch does not; the plan is reset afterwards.
+void Plan::time_kernel(bool fwd, int reps, float* ms) {
+  if (px) fail("plan: time_kernel is not available for peer-exchange plans");
+  if (reps < 1) fail("plan: reps must be >= 1");
+  enqueue_reset();
+  SSB_CUDA(cudaEventRecord(ev0, ctx->stream));
+  for (int r = 0; r < reps; ++r) {
+    if (dtype == SS_F32) {
+      const SartK<float> k = make_args<float>(*this);
+      if (fwd) launch_fwd<float>(*this, k, 0);
+      else launch_back<float>(*this, k, 0);
+    } else {
+      const SartK<double> k = make_args<double>(*this);
+      if (fwd) launch_fwd<double>(*this, k, 0);
+      else launch_back<double>(*this, k, 0);
+    }
+    ctx->check_launch(fwd ? "sart_fwd_kernel" : "sart_back_kernel");
+  }
+  SSB_CUDA(cudaEventRecord(ev1, ctx->stream));
+  SSB_CUDA(cudaEventSynchronize(ev1));
+  float t = 0.f;
+  SSB_CUDA(cudaEventElapsedTime(&t, ev0, ev1));
+  *ms = t / reps;
+  enqueue_reset();
+  ctx->sync();
+  launched = false;
+}
+
 void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
   // bytes of matrix data each kernel must stream per launch, in this plan's format
   const std::int64_t b = static_cast<std::int64_t>(tsize());

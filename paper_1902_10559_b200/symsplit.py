@@ -241,6 +241,10 @@ class Matrix:
         _check(_lib().ss_matrix_coeff(self.h, int(i), int(j), C.byref(out)))
         return out.value
 
+    def release_cache(self):
+        """Free the fold and SART plan solve_split keeps on this matrix."""
+        _check(_lib().ss_matrix_release_cache(self.h))
+
     def for_each(self, f):
         """matrix.hpp:76-87: f(row, col, value) over the stored entries in
         compressed-column order."""
@@ -743,6 +747,13 @@ class SartPlan:
         a, b = C.c_float(), C.c_float()
         _check(_lib().ss_plan_profile(self.h, iters, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def time_kernel(self, fwd: bool, reps: int = 50) -> float:
+        """In-loop milliseconds per launch of K1 (fwd) or K2: `reps` launches
+        back to back, CUDA events around the batch. Resets the plan."""
+        ms = C.c_float()
+        _check(_lib().ss_plan_time_kernel(self.h, 1 if fwd else 0, reps, C.byref(ms)))
+        return ms.value
 
 
 # ----------------------------------------------------------------- multi-GPU helpers
