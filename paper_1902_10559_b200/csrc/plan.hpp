@@ -86,6 +86,11 @@ struct Plan {
     if (fwd ? mir_f : mir_b) return stream_cs ? 5 : 4;
     return stream_cs ? 3 : 2;
   }
+  // persistent loop (sart_persistent_pair_kernel): one cooperative launch per
+  // solve, grid barriers between the K1 and K2 phases
+  bool persistent = false;
+  int pgrid = 0;
+  DBuf<unsigned> gbar;  // {arrivals, generation}
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;
   cudaGraphExec_t graph = nullptr;

@@ -672,7 +672,15 @@ __device__ __forceinline__ void load4s(const double* p, double (&v)[4]) {
 
 // With U16 = false (tiles spanning >= 65536 indices, e.g. config 5's K2) the
 // entries keep int32 indices (tidx) and the header's base word is unused.
-template <class T, int VS, int UF, bool CS = false, bool U16 = true>
+// gathered-vector load: read-only path, or (NC = false) a plain load for a
+// vector that other CTAs rewrite during the same (persistent) kernel
+template <bool NC, class V>
+__device__ __forceinline__ V ldx(const V* p) {
+  if constexpr (NC) return __ldg(p);
+  else return *p;
+}
+
+template <class T, int VS, int UF, bool CS = false, bool U16 = true, bool NC = true>
 __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off,
                                           const int* __restrict__ tidx,
                                           const unsigned* __restrict__ hdr, int tf,
@@ -705,8 +713,8 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
       int4 c;
       if constexpr (U16) c = decode16(o[u], b[u]);
       else c = ci[u];
-      const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
-               g3 = __ldg(xv + c.w);
+      const T2 g0 = ldx<NC>(xv + c.x), g1 = ldx<NC>(xv + c.y), g2 = ldx<NC>(xv + c.z),
+               g3 = ldx<NC>(xv + c.w);
       sa += flip(v[u][0], s[u], 0) * g0.x + flip(v[u][1], s[u], 1) * g1.x +
             flip(v[u][2], s[u], 2) * g2.x + flip(v[u][3], s[u], 3) * g3.x;
       sb += v[u][0] * g0.y + v[u][1] * g1.y + v[u][2] * g2.y + v[u][3] * g3.y;
@@ -722,8 +730,8 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
     else c = __ldg(reinterpret_cast<const int4*>(tidx + k0));
     T v[4];
     load4s<CS>(v1 + k0, v);
-    const T2 g0 = __ldg(xv + c.x), g1 = __ldg(xv + c.y), g2 = __ldg(xv + c.z),
-             g3 = __ldg(xv + c.w);
+    const T2 g0 = ldx<NC>(xv + c.x), g1 = ldx<NC>(xv + c.y), g2 = ldx<NC>(xv + c.z),
+             g3 = ldx<NC>(xv + c.w);
     sa += flip(v[0], s, 0) * g0.x + flip(v[1], s, 1) * g1.x + flip(v[2], s, 2) * g2.x +
           flip(v[3], s, 3) * g3.x;
     sb += v[0] * g0.y + v[1] * g1.y + v[2] * g2.y + v[3] * g3.y;
@@ -731,7 +739,7 @@ __device__ __forceinline__ void seg_dot2m(const unsigned short* __restrict__ off
   for (int e = eb + lane; e < ee; e += VS) {  // exception buckets (rare)
     const int c = __ldg(eidx + e);
     const T2 a = __ldg(reinterpret_cast<const T2*>(ev2) + e);
-    const T2 g = __ldg(xv + c);
+    const T2 g = ldx<NC>(xv + c);
     sa += a.x * g.x;
     sb += a.y * g.y;
   }
@@ -913,6 +921,168 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
     tf = ntf;
     eb = neb;
     ee = nee;
+  }
+}
+
+// ------------------------------------------------------------ persistent paired loop
+// Small folded pairs (configs 1-2: L2-resident, ~10 us per pass of two
+// launches) are launch- and tail-latency bound. The persistent kernel runs the
+// whole loop in one cooperative launch: per pass the K1 phase (rows) and the
+// K2 phase (columns) of the pair kernels, separated by grid barriers. Every
+// CTA sums the per-CTA ||r||^2 partials in the same fixed order as
+// finish_norms, so all CTAs take the same stop decision (the reference's
+// check-before-update rule, solvers.cpp:180-182) without a further barrier;
+// CTA 0 records the history. Gathered vectors are read with plain loads (they
+// change inside the kernel); the gpu-scope fences of the barrier order them.
+constexpr long long kBarrierSpinCycles = 4000000000LL;  // ~2 s: a lost CTA traps
+
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const long long t0 = clock64();
+      while (*gen == g) {
+        __nanosleep(32);
+        if (clock64() - t0 > kBarrierSpinCycles) __trap();
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <class T, int VSF, int VSB, int UF, int TL>
+__global__ void __launch_bounds__(kThreads, 2)
+    sart_persistent_pair_kernel(SartK<T> k, int first, int count, unsigned* bar) {
+  using T2 = typename Vec2<T>::type;
+  constexpr bool U16 = TL != 6;
+  __shared__ double red[2][kWarps];
+  __shared__ double sh[kThreads];
+  __shared__ int go[2];
+  const int nrow = static_cast<int>(k.rows0), ncol = static_cast<int>(k.cols0);
+  for (int it = first; it < first + count; ++it) {
+    const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+    if (!on0 && !on1) break;  // every CTA reads the same settled state
+    // ---- K1 phase: r = p - A x, w = row_inv r, per-CTA ||r||^2 partials
+    {
+      const int lane = threadIdx.x & (VSF - 1);
+      const unsigned mask = group_mask<VSF>();
+      const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VSF);
+      double r2a = 0.0, r2b = 0.0;
+      for (int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VSF);
+           g < nrow; g += gstep) {
+        const int beg = __ldg(k.tpf + g), end = __ldg(k.tpf + g + 1), tf = __ldg(k.tff + g);
+        int eb = 0, ee = 0;
+        if (k.epf) {
+          eb = __ldg(k.epf + g);
+          ee = __ldg(k.epf + g + 1);
+        }
+        T e[4] = {T(0), T(0), T(0), T(0)};
+        if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
+        T da, db;
+        seg_dot2m<T, VSF, UF, false, U16, false>(k.tof, k.tif, k.thf, tf, k.rv2,
+                                                reinterpret_cast<const T2*>(k.xx), beg, end, eb,
+                                                ee, k.eif, k.evf, lane, mask, da, db);
+        if (lane == 0) {
+          const T ra = e[0] - da, rb = e[1] - db;
+          T2 wo;
+          wo.x = on0 ? e[2] * ra : T(0);
+          wo.y = on1 ? e[3] * rb : T(0);
+          reinterpret_cast<T2*>(k.ww)[g] = wo;
+          if (on0) r2a += static_cast<double>(ra) * static_cast<double>(ra);
+          if (on1) r2b += static_cast<double>(rb) * static_cast<double>(rb);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r2a += __shfl_xor_sync(0xffffffffu, r2a, o);
+        r2b += __shfl_xor_sync(0xffffffffu, r2b, o);
+      }
+      const int warp = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) {
+        red[0][warp] = r2a;
+        red[1][warp] = r2b;
+      }
+      __syncthreads();
+      if (threadIdx.x < 2) {
+        double t = 0.0;
+        for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
+        k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
+      }
+    }
+    grid_sync(bar);
+    // ---- ||r|| and the stop test, identically in every CTA (finish_norms order)
+    for (int q = 0; q < 2; ++q) {
+      const bool on = q ? on1 : on0;
+      if (!on) {
+        if (threadIdx.x == 0) go[q] = 0;
+        continue;
+      }
+      double t = 0.0;
+      const volatile double* part = k.partial + q * gridDim.x;
+      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kThreads) t += part[b];
+      sh[threadIdx.x] = t;
+      __syncthreads();
+      for (int o = kThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        const double res = sqrt(sh[0]);
+        const bool stop = res <= k.tol * k.pnorm[q];
+        go[q] = stop ? 0 : 1;
+        if (blockIdx.x == 0) {
+          k.history[q * k.hstride + it] = res;
+          if (stop) {
+            k.state[4 * q + 0] = 1;
+            k.state[4 * q + 1] = it;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const bool u0 = go[0] != 0, u1 = go[1] != 0;
+    if (!u0 && !u1) break;  // both stopped (CTA 0 recorded it)
+    // ---- K2 phase: x += lambda col_inv (A^T w)
+    {
+      const int lane = threadIdx.x & (VSB - 1);
+      const unsigned mask = group_mask<VSB>();
+      const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VSB);
+      for (int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VSB);
+           g < ncol; g += gstep) {
+        const int beg = __ldg(k.tpb + g), end = __ldg(k.tpb + g + 1), tf = __ldg(k.tfb + g);
+        int eb = 0, ee = 0;
+        if (k.epb) {
+          eb = __ldg(k.epb + g);
+          ee = __ldg(k.epb + g + 1);
+        }
+        T2 xo, ci;
+        xo.x = xo.y = ci.x = ci.y = T(0);
+        if (lane == 0) {
+          xo = reinterpret_cast<const T2*>(k.xx)[g];
+          ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
+        }
+        T ua, ub;
+        seg_dot2m<T, VSB, UF, false, U16, false>(k.tob, k.tib, k.thb, tf, k.cv2,
+                                                reinterpret_cast<const T2*>(k.ww), beg, end, eb,
+                                                ee, k.eib, k.evb, lane, mask, ua, ub);
+        if (lane == 0) {
+          if (u0) xo.x = upd(xo.x, k.relax, ua, ci.x);
+          if (u1) xo.y = upd(xo.y, k.relax, ub, ci.y);
+          reinterpret_cast<T2*>(k.xx)[g] = xo;
+          if (u0 && !isfinite(static_cast<double>(xo.x))) atomicCAS(&k.state[2], 0, it + 1);
+          if (u1 && !isfinite(static_cast<double>(xo.y))) atomicCAS(&k.state[4 + 2], 0, it + 1);
+        }
+      }
+    }
+    grid_sync(bar);
   }
 }
 
@@ -2502,8 +2672,45 @@ void launch_xchg_final(Plan& P) {
 }
 
 template <class T>
+using PersistFn = void (*)(SartK<T>, int, int, unsigned*);
+
+// the persistent kernel of a paired plan's shape, or nullptr (not instantiated)
+template <class T>
+PersistFn<T> persistent_kernel(const Plan& P) {
+  const bool u16 = P.c16f && P.c16b;
+  if (!(P.mir_f && P.mir_b) || !u16 || P.c16f != P.c16b || P.stream_cs) return nullptr;
+#define SSB_PERSIST(F, B) \
+  if (P.vs_fwd == F && P.vs_back == B) return sart_persistent_pair_kernel<T, F, B, 2, 4>;
+  SSB_PERSIST(8, 4) SSB_PERSIST(8, 8) SSB_PERSIST(8, 16)
+  SSB_PERSIST(16, 4) SSB_PERSIST(16, 8) SSB_PERSIST(16, 16)
+  SSB_PERSIST(32, 4) SSB_PERSIST(32, 8) SSB_PERSIST(32, 16)
+#undef SSB_PERSIST
+  return nullptr;
+}
+
+// one cooperative launch runs passes [first, first + count) (all CTAs resident)
+template <class T>
+void launch_persistent(Plan& P, const SartK<T>& k, int first, int count) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.pgrid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = P.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, persistent_kernel<T>(P), k, first, count, P.gbar.get()));
+  P.ctx->check_launch("sart_persistent_pair_kernel");
+}
+
+template <class T>
 void do_iterations(Plan& P, int first, int count) {
   const SartK<T> k = make_args<T>(P);
+  if (P.persistent) {
+    launch_persistent<T>(P, k, first, count);
+    return;
+  }
   for (int it = first; it < first + count; ++it) {
     if (P.px) {  // K1x over local rows, K2x with the fused peer exchange
       launch_xchg<T>(P, k, it, true);
@@ -2618,7 +2825,7 @@ void Plan::build_graph() {
   // NCCL calls stay out of the captured graph; a peer-exchange plan is captured
   // when the pass count is fixed (an emulated group launches rank by rank)
   if (graph || (sharded && !(px && !px->emulated && !(opts.tol > 0.0)))) return;
-  if (!(opts.tol > 0.0)) {
+  if (!(opts.tol > 0.0) || persistent) {
     // fixed iteration count (tol = 0 can never stop early): every pass
     // unrolled into the graph, the cheapest replay (a WHILE node's per-pass
     // scheduling costs ~5% on config 3)
@@ -2698,8 +2905,9 @@ void Plan::launch() {
   SSB_CUDA(cudaEventRecord(ev0, ctx->stream));
   if (graph) {
     SSB_CUDA(cudaGraphLaunch(graph, ctx->stream));
-    ctx->launches += static_cast<std::int64_t>(px ? 3 : 1 + nband) * opts.max_iters +
-                     (paired || px ? 1 : 0);
+    ctx->launches += persistent ? 2
+                                : static_cast<std::int64_t>(px ? 3 : 1 + nband) * opts.max_iters +
+                                      (paired || px ? 1 : 0);
   } else {
     enqueue_reset();
     enqueue_iterations(0, opts.max_iters);
@@ -3036,15 +3244,20 @@ std::string Plan::describe() const {
     bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + std::to_string(layout_mode(false)) + ">";
   }
+  std::string pk = persistent ? "sart_persistent_pair_kernel<" + std::string(t) + ", " +
+                                    std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
+                                    ", 2, 4>"
+                              : "";
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
-  char buf[768];
+  char buf[1024];
   std::snprintf(buf, sizeof buf,
                 "{\"layout\": \"%s\", \"dtype\": \"%s\", \"nsys\": %d, \"nrhs\": %d, "
                 "\"vs_fwd\": %d, \"uf_fwd\": %d, \"vs_back\": %d, \"uf_back\": %d, "
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
-                "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s}",
+                "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s, "
+                "\"persistent_kernel\": \"%s\", \"persistent_grid\": %d}",
                 sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
                         : (paired ? (tiled ? (mir_f || mir_b ? "paired-tiled-u16-mirror"
                                                                     : (c16f || c16b ? "paired-tiled-u16" : "paired-tiled"))
@@ -3053,7 +3266,7 @@ std::string Plan::describe() const {
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
-                graph ? "true" : "false");
+                graph ? "true" : "false", pk.c_str(), persistent ? pgrid : 0);
   return buf;
 }
 
@@ -3334,6 +3547,29 @@ void build_single(Plan& P) {
 }
 }  // namespace
 
+// Persistent loop of a paired plan (see sart_persistent_pair_kernel): the
+// grid is every co-resident CTA the work can use; the barrier words are
+// zeroed once (the barrier leaves its count at 0).
+template <class T>
+void setup_persistent(Plan& P) {
+  PersistFn<T> fn = persistent_kernel<T>(P);
+  if (!fn) return;
+  int per_sm = 0;
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+  if (per_sm < 1) return;
+  const long long need = std::max<long long>(static_cast<long long>(P.rows[0]) * P.vs_fwd,
+                                             static_cast<long long>(P.cols[0]) * P.vs_back);
+  P.pgrid = static_cast<int>(std::max<long long>(1, std::min<long long>(
+      static_cast<long long>(per_sm) * P.ctx->sm_count, (need + kThreads - 1) / kThreads)));
+  const int cap = env_int("SSB_PGRID", 0);
+  if (cap > 0) P.pgrid = std::min(P.pgrid, cap);
+  P.gbar.alloc(2);
+  SSB_CUDA(cudaMemsetAsync(P.gbar.get(), 0, 2 * sizeof(unsigned), P.ctx->stream));
+  if (static_cast<std::size_t>(P.pgrid) * 2 > P.partial.size()) P.partial.alloc(2 * P.pgrid);
+  P.ctx->sync();
+  P.persistent = true;
+}
+
 Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o, int nrhs,
                 bool reusable) {
   if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
@@ -3493,6 +3729,16 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     if (P->l2_window) {
       SSB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
                                   static_cast<std::size_t>(env_int("SSB_L2WIN_MB", 16)) << 20));
+    }
+    // L2-resident pairs (configs 1-2) run the loop as one persistent kernel
+    // (SSB_PERSIST=0: the two launches per pass; 1: whenever the shape allows)
+    {
+      const int want = env_int("SSB_PERSIST", -1);
+      const bool small = static_cast<std::size_t>(fb + bb) * 2 <= ctx->l2_bytes;
+      if (want != 0 && (want == 1 || small)) {
+        if (o.dtype == SS_F32) setup_persistent<float>(*P);
+        else setup_persistent<double>(*P);
+      }
     }
     tr.mark("paired streams");
   } else if (P->nsys == 1 && nrhs == 1) {
