@@ -291,11 +291,11 @@ int ss_plan_create_sharded(ss_ctx_t ctx, ss_matrix_t a, int64_t row_begin, int64
 
 /* How the ranks of a row-sharded system combine their back-projections.
  * SS_XCHG_NCCL: K2 writes the partial A_g^T w_g, then ncclAllReduce + update.
- * SS_XCHG_PEER: fused exchange over NVLink peer memory. K2 stores each chunk
- *   of columns straight into the owning rank's receive buffer; the last rank
- *   to arrive on a chunk sums the G partials in rank order, applies the
- *   update and stores the new x chunk into every rank's replica; the next K1
- *   waits (device-side) for all chunks. No NCCL call on the data path; the
+ * SS_XCHG_PEER: fused exchange over NVLink peer memory. K2 stores each
+ *   column's partial straight into its owner's receive row; each owner sums
+ *   the G partials of its own columns in rank order, applies the update and
+ *   stores its new x range into every rank's replica; the next K1 waits
+ *   (device-side) for all ranges. No NCCL call on the data path; the
  *   regions are mapped with CUDA IPC (handles exchanged once over the
  *   context's NCCL communicator). Replaces the same reference loop as
  *   ss_plan_create_sharded (solvers.cpp:173-192). */
@@ -307,6 +307,19 @@ int ss_exchange_owned_columns(int64_t cols, int parts, int rank, int64_t* col_be
                               int64_t* col_end);
 int ss_plan_create_sharded_x(ss_ctx_t ctx, ss_matrix_t a, int64_t row_begin, int64_t row_end,
                              const ss_solve_options* opts, int exchange, ss_plan_t* out);
+/* The folded PAIR row-sharded over all ranks of the context's communicator
+ * (the B200 layout for N >= 2): each rank keeps rows [row_begin, row_end) of
+ * BOTH folded systems on the paired mirror-coded streams (one index stream,
+ * both systems per launch) and exchanges {u1, u2} back-projection pairs through
+ * the fused peer exchange (SS_XCHG_PEER); each system keeps its own stop /
+ * divergence state. Replaces the reference's two-branch solve_split
+ * (solvers.cpp:212-233) run over N devices. */
+int ss_plan_create_sharded_pair(ss_ctx_t ctx, ss_matrix_t a1, ss_matrix_t a2, int64_t row_begin,
+                                int64_t row_end, const ss_solve_options* opts, ss_plan_t* out);
+/* one-device emulation of `parts` ranks of the row-sharded pair (tests) */
+int ss_plan_create_sharded_pair_group(ss_ctx_t ctx, ss_matrix_t a1, ss_matrix_t a2, int parts,
+                                      const int64_t* bounds, const ss_solve_options* opts,
+                                      ss_plan_t* plans);
 /* One-device emulation of `parts` peer-exchange ranks (tests and single-GPU
  * measurement of the fused exchange): plans[g] keeps rows
  * [bounds[g], bounds[g+1]) and the plans' regions are linked directly. Set

@@ -138,6 +138,10 @@ SIGNATURES = {
                                            C.POINTER(vp)]),
     "ss_plan_create_sharded_group": (C.c_int, [vp, vp, C.c_int, i64p, C.POINTER(SolveOptionsC),
                                                C.POINTER(vp)]),
+    "ss_plan_create_sharded_pair": (C.c_int, [vp, vp, vp, i64, i64, C.POINTER(SolveOptionsC),
+                                              C.POINTER(vp)]),
+    "ss_plan_create_sharded_pair_group": (C.c_int, [vp, vp, vp, C.c_int, i64p,
+                                                    C.POINTER(SolveOptionsC), C.POINTER(vp)]),
     "ss_plan_group_run": (C.c_int, [C.POINTER(vp), C.c_int]),
     "ss_read_matrix_market": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
     "ss_write_matrix_market": (C.c_int, [vp, C.c_char_p]),

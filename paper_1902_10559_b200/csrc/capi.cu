@@ -1172,6 +1172,39 @@ int ss_exchange_owned_columns(int64_t cols, int parts, int rank, int64_t* col_be
   });
 }
 
+int ss_plan_create_sharded_pair(ss_ctx_t h, ss_matrix_t a1, ss_matrix_t a2, int64_t row_begin,
+                                int64_t row_end, const ss_solve_options* opts, ss_plan_t* out) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(out, "out");
+    use_device(ctx);
+    *out = wrap(ssb::make_sharded_pair_plan(ctx, M(a1), M(a2), row_begin, row_end, *opts));
+  });
+}
+
+int ss_plan_create_sharded_pair_group(ss_ctx_t h, ss_matrix_t a1, ss_matrix_t a2, int parts,
+                                      const int64_t* bounds, const ss_solve_options* opts,
+                                      ss_plan_t* plans) {
+  return guarded([&] {
+    ssb::Context* ctx = CX(h);
+    need(opts, "opts");
+    need(bounds, "bounds");
+    need(plans, "plans");
+    if (parts < 1) ssb::fail("plan: parts must be >= 1");
+    use_device(ctx);
+    std::vector<std::unique_ptr<ssb::Plan>> made;
+    for (int g = 0; g < parts; ++g) {
+      made.emplace_back(ssb::make_sharded_pair_plan(ctx, M(a1), M(a2), bounds[g], bounds[g + 1],
+                                                    *opts, parts, g));
+    }
+    std::vector<ssb::Plan*> raw;
+    for (auto& p : made) raw.push_back(p.get());
+    ssb::link_group(raw.data(), parts);
+    for (int g = 0; g < parts; ++g) plans[g] = wrap(made[g].release());
+  });
+}
+
 int ss_plan_create_sharded_x(ss_ctx_t h, ss_matrix_t a, int64_t row_begin, int64_t row_end,
                              const ss_solve_options* opts, int exchange, ss_plan_t* out) {
   return guarded([&] {

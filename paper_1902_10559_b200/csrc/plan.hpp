@@ -47,6 +47,7 @@ struct Plan {
   Matrix* a[2] = {nullptr, nullptr};
   // Row-sharded plans own a row-block copy of the (single) system.
   Matrix* own = nullptr;
+  Matrix* own2 = nullptr;  // row-sharded pair: the local block of A2
   std::int64_t rows[2] = {0, 0}, cols[2] = {0, 0};
   // per system, plan dtype (T) buffers in bytes
   DBuf<char> x[2], w[2], p[2], rinv[2], cinv[2];
@@ -100,7 +101,7 @@ struct Plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;
   float group_ms = -1.0f;
-  double pn_local = -1.0;  // emulated exchange rank: local ||p_g|| (run_group combines)  // emulated exchange group: time of the whole group's solve
+  double pn_local[2] = {-1.0, -1.0};  // emulated exchange rank: local ||p_g|| (run_group combines)  // emulated exchange group: time of the whole group's solve
   bool launched = false;
   bool empty_rows[2] = {false, false};  // all row sums zero (reference throws)
 
@@ -132,6 +133,11 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
                 bool reusable = true);
 // exchange: SS_XCHG_NCCL or SS_XCHG_PEER. emul_parts > 0 builds rank
 // emul_rank of a one-device emulation (no communicator; see run_group).
+// The folded pair row-sharded over all ranks (peer exchange, paired streams);
+// emul_parts > 0: rank emul_rank of a one-device emulation.
+Plan* make_sharded_pair_plan(Context* ctx, Matrix* a1, Matrix* a2, std::int64_t row_begin,
+                             std::int64_t row_end, const ss_solve_options& o, int emul_parts = 0,
+                             int emul_rank = 0);
 Plan* make_sharded_plan(Context* ctx, Matrix* a, std::int64_t row_begin, std::int64_t row_end,
                         const ss_solve_options& o, int exchange = SS_XCHG_NCCL,
                         int emul_parts = 0, int emul_rank = 0);

@@ -2129,6 +2129,277 @@ __global__ void xchg_final_kernel(SartK<T> k, XK<T> x) {
   x.local[3] = 0;
 }
 
+// ---------------------------------------------------------- paired peer exchange
+// The folded pair row-sharded over all G ranks (not one system per GPU half):
+// rank `me` keeps rows [rb, re) of A1 and A2 on the paired mirror-coded
+// streams, so every rank streams 1/G of the bytes of the single-GPU paired
+// plan. Same protocol as the single-system exchange above, with both systems
+// in every message: receive rows hold {u1, u2} pairs ([G][cols][2]), the x
+// replica is the interleaved iterate ([cols][2]), the ||r_g||^2 slots are
+// [2 parity][G][2 systems], the divergence flags one per system. Each system
+// keeps its own stop / divergence state (the two branches of solve_split stay
+// independent solves, solvers.cpp:212-233); a pass runs while either is on.
+
+// K1x-pair prologue (thread 0 of every block; every block decides alike):
+// settle the previous iteration of each system, return the systems to run
+// (bit 0: system 1, bit 1: system 2; 0 = nothing this pass)
+template <class T>
+__device__ int xchg_enter_pair(const SartK<T>& k, const XK<T>& x, int it) {
+  volatile int* st = k.state;
+  if (x.inline_signal && blockIdx.x == 0 && it > 0 && x.local[1] == it) {
+    signal_all(x, x.off_xready);
+    x.local[3] = it;
+  }
+  bool on[2] = {st[0] == 0 && st[2] == 0, st[4] == 0 && st[6] == 0};
+  if (!on[0] && !on[1]) return 0;
+  const long long base = x.local[0];
+  if (!wait_geq(xready(x, x.me), xready_target(x, base + it), x.local + 2)) return 0;
+  if (it > 0) {
+    const double* r2 = xr2(x, x.me) + ((base + it - 1) & 1) * 2 * x.G;
+    for (int q = 0; q < 2; ++q) {
+      if (!on[q]) continue;
+      const int d = ld_sys(xdflag(x, x.me) + q);
+      if (d != 0) {
+        if (blockIdx.x == 0) st[4 * q + 2] = d;
+        on[q] = false;
+        continue;
+      }
+      double t = 0.0;
+      for (int g = 0; g < x.G; ++g) t += ld_sys(r2 + 2 * g + q);
+      const double res = sqrt(t);
+      if (blockIdx.x == 0) k.history[q * k.hstride + it - 1] = res;
+      if (res <= k.tol * k.pnorm[q]) {
+        if (blockIdx.x == 0) {
+          st[4 * q + 0] = 1;
+          st[4 * q + 1] = it - 1;
+        }
+        on[q] = false;
+      }
+    }
+  }
+  if (!on[0] && !on[1]) return 0;
+  if (blockIdx.x == 0) x.local[1] = it + 1;
+  return (on[0] ? 1 : 0) | (on[1] ? 2 : 0);
+}
+
+template <class T, int VS, int UF, int TL>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
+    sart_fwd_xchg_pair_kernel(SartK<T> k, XK<T> x, int it) {
+  using T2 = typename Vec2<T>::type;
+  cudaGridDependencySynchronize();
+  __shared__ double red[2][kWarps];
+  __shared__ int go;
+  if (threadIdx.x == 0) go = xchg_enter_pair(k, x, it);
+  __syncthreads();
+  if (!go) return;
+  const bool on0 = (go & 1) != 0, on1 = (go & 2) != 0;
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.rows0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  double r2a = 0.0, r2b = 0.0;
+  for (int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS); g < n;
+       g += gstep) {
+    const int beg = __ldg(k.tpf + g), end = __ldg(k.tpf + g + 1), tf = __ldg(k.tff + g);
+    int eb = 0, ee = 0;
+    if (k.epf) {
+      eb = __ldg(k.epf + g);
+      ee = __ldg(k.epf + g + 1);
+    }
+    T e[4] = {T(0), T(0), T(0), T(0)};
+    if (lane == 0) load4(k.pe + 4 * static_cast<long long>(g), e);
+    T da, db;
+    seg_dot2m<T, VS, UF, TL == 5, TL != 6>(k.tof, k.tif, k.thf, tf, k.rv2,
+                                            reinterpret_cast<const T2*>(k.xx), beg, end, eb, ee,
+                                            k.eif, k.evf, lane, mask, da, db);
+    if (lane == 0) {
+      const T ra = e[0] - da, rb = e[1] - db;
+      T2 wo;
+      wo.x = on0 ? e[2] * ra : T(0);
+      wo.y = on1 ? e[3] * rb : T(0);
+      reinterpret_cast<T2*>(k.ww)[g] = wo;
+      if (on0) r2a += static_cast<double>(ra) * static_cast<double>(ra);
+      if (on1) r2b += static_cast<double>(rb) * static_cast<double>(rb);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r2a += __shfl_xor_sync(0xffffffffu, r2a, o);
+    r2b += __shfl_xor_sync(0xffffffffu, r2b, o);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][warp] = r2a;
+    red[1][warp] = r2b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
+    k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+  if (last_block(k.ticket)) {
+    // fixed-order ||r_me||^2 of both systems into slot [parity][me][q] of every rank
+    __shared__ double sh[kThreads];
+    __shared__ double tot[2];
+    for (int q = 0; q < 2; ++q) {
+      double s = 0.0;
+      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += kThreads)
+        s += k.partial[q * gridDim.x + b];
+      sh[threadIdx.x] = s;
+      __syncthreads();
+      for (int o = kThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) tot[q] = sh[0];
+      __syncthreads();
+    }
+    const long long e = x.local[0] + it;
+    if (threadIdx.x < x.G) {
+      double* slot = xr2(x, threadIdx.x) + (e & 1) * 2 * x.G + 2 * x.me;
+      slot[0] = tot[0];
+      slot[1] = tot[1];
+    }
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
+template <class T, int VS, int UF, int TL>
+__global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
+    sart_back_xchg_pair_kernel(SartK<T> k, XK<T> x, int it) {
+  using T2 = typename Vec2<T>::type;
+  cudaGridDependencySynchronize();
+  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  if (!on0 && !on1) return;
+  const int lane = threadIdx.x & (VS - 1);
+  const unsigned mask = group_mask<VS>();
+  const int n = static_cast<int>(k.cols0);
+  const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
+  const long long row = static_cast<long long>(x.me) * x.cols;
+  for (int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS); g < n;
+       g += gstep) {
+    const int beg = __ldg(k.tpb + g), end = __ldg(k.tpb + g + 1), tf = __ldg(k.tfb + g);
+    int eb = 0, ee = 0;
+    if (k.epb) {
+      eb = __ldg(k.epb + g);
+      ee = __ldg(k.epb + g + 1);
+    }
+    T ua, ub;
+    seg_dot2m<T, VS, UF, TL == 5, TL != 6>(k.tob, k.tib, k.thb, tf, k.cv2,
+                                            reinterpret_cast<const T2*>(k.ww), beg, end, eb, ee,
+                                            k.eib, k.evb, lane, mask, ua, ub);
+    if (lane == 0) {  // {u1, u2} into the owner's receive row (NVLink store)
+      T2 u;
+      u.x = ua;
+      u.y = ub;
+      T2* recv = reinterpret_cast<T2*>(
+          xrecv(x, static_cast<int>(static_cast<unsigned>(g) / static_cast<unsigned>(x.own))));
+      recv[row + g] = u;
+    }
+  }
+}
+
+// Owner side, both systems: rank-order sums of the G partial pairs of this
+// rank's columns, per-system update (unless that system stopped this pass),
+// the new {x1, x2} range pushed into every replica.
+template <class T>
+__global__ void __launch_bounds__(kThreads) xchg_reduce_pair_kernel(SartK<T> k, XK<T> x, int it) {
+  using T2 = typename Vec2<T>::type;
+  cudaGridDependencySynchronize();
+  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  if (!on0 && !on1) return;
+  __shared__ int go;
+  const long long e = x.local[0] + it;
+  if (threadIdx.x == 0) {
+    if (x.inline_signal && blockIdx.x == 0) signal_all(x, x.off_done);
+    go = wait_geq(xdone(x, x.me), static_cast<unsigned long long>(x.G) * (e + 1), x.local + 2);
+  }
+  __syncthreads();
+  if (!go) return;
+  bool up[2] = {on0, on1};
+  const double* r2 = xr2(x, x.me) + (e & 1) * 2 * x.G;
+  for (int q = 0; q < 2; ++q) {
+    if (!up[q]) continue;
+    double t = 0.0;
+    for (int g = 0; g < x.G; ++g) t += ld_sys(r2 + 2 * g + q);
+    if (sqrt(t) <= k.tol * k.pnorm[q]) up[q] = false;  // check before update
+  }
+  if (!up[0] && !up[1]) return;
+  const long long j0 = x.me * x.own, j1 = min(j0 + x.own, x.cols);
+  const T* src = xrecv(x, x.me);
+  const T* xl = xrep(x, x.me);
+  const T2* ci = reinterpret_cast<const T2*>(k.cc);
+  bool bad[2] = {false, false};
+  for (long long j = j0 + blockIdx.x * (long long)kThreads + threadIdx.x; j < j1;
+       j += (long long)gridDim.x * kThreads) {
+    T sa = ld_sys(src + 2 * j), sb = ld_sys(src + 2 * j + 1);
+    for (int g = 1; g < x.G; ++g) {
+      sa += ld_sys(src + 2 * (g * x.cols + j));
+      sb += ld_sys(src + 2 * (g * x.cols + j) + 1);
+    }
+    T2 xo;
+    xo.x = ld_sys(xl + 2 * j);
+    xo.y = ld_sys(xl + 2 * j + 1);
+    const T2 c = __ldg(ci + j);
+    if (up[0]) xo.x = upd(xo.x, k.relax, sa, c.x);
+    if (up[1]) xo.y = upd(xo.y, k.relax, sb, c.y);
+    for (int r = 0; r < x.G; ++r) reinterpret_cast<T2*>(xrep(x, r))[j] = xo;  // local + NVLink
+    bad[0] |= up[0] && !isfinite(static_cast<double>(xo.x));
+    bad[1] |= up[1] && !isfinite(static_cast<double>(xo.y));
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (bad[q]) {
+      for (int r = 0; r < x.G; ++r) atomicCAS_system(xdflag(x, r) + q, 0, it + 1);
+    }
+  }
+}
+
+// Emulated group, pairs: the announcements the kernels make inline on real ranks.
+template <class T>
+__global__ void xchg_announce_pair_kernel(SartK<T> k, XK<T> x, int it, int kind) {
+  if (threadIdx.x != 0) return;
+  if (kind == 0 && it > 0 && x.local[1] == it) {
+    signal_all(x, x.off_xready);
+    x.local[3] = it;
+  }
+  if (kind == 1 && (sys_on(k.state, 0) || sys_on(k.state, 1))) signal_all(x, x.off_done);
+  if (kind == 2 && x.local[3] < x.local[1]) signal_all(x, x.off_xready);
+}
+
+// After the last pass, pairs: wait for the final x, settle each system's last
+// residual / stop / divergence, advance the epoch base.
+template <class T>
+__global__ void xchg_final_pair_kernel(SartK<T> k, XK<T> x) {
+  if (threadIdx.x != 0) return;
+  volatile int* st = k.state;
+  const long long base = x.local[0], L = x.local[1];
+  if (x.inline_signal && x.local[3] < L) signal_all(x, x.off_xready);
+  if (!wait_geq(xready(x, x.me), xready_target(x, base + L), x.local + 2)) return;
+  if (L > 0) {
+    const double* r2 = xr2(x, x.me) + ((base + L - 1) & 1) * 2 * x.G;
+    for (int q = 0; q < 2; ++q) {
+      if (st[4 * q] != 0 || st[4 * q + 2] != 0) continue;
+      const int d = ld_sys(xdflag(x, x.me) + q);
+      if (d != 0) {
+        st[4 * q + 2] = d;
+        continue;
+      }
+      double t = 0.0;
+      for (int g = 0; g < x.G; ++g) t += ld_sys(r2 + 2 * g + q);
+      const double res = sqrt(t);
+      k.history[q * k.hstride + L - 1] = res;
+      if (res <= k.tol * k.pnorm[q]) {
+        st[4 * q] = 1;
+        st[4 * q + 1] = static_cast<int>(L - 1);
+      }
+    }
+  }
+  x.local[0] = base + L;
+  x.local[1] = 0;
+  x.local[3] = 0;
+}
+
 // Column-band boundaries inside every CSR row (columns ascending): out[b][i] =
 // first position of row i whose column is >= b*cols/nband (b = nband: row end).
 __global__ void band_ptr_kernel(const int* __restrict__ rp, const int* __restrict__ ci,
@@ -2306,7 +2577,12 @@ SartK<T> make_args(Plan& P) {
   if (P.sharded && !P.px) {
     k.bp_out = reinterpret_cast<T*>(P.bp.get());
   }
-  if (P.px) k.s[0].x = reinterpret_cast<T*>(static_cast<char*>(P.px->region) + P.px->off_x);
+  if (P.px && !P.paired) {
+    k.s[0].x = reinterpret_cast<T*>(static_cast<char*>(P.px->region) + P.px->off_x);
+  }
+  if (P.px && P.paired) {  // the interleaved iterate is this rank's replica
+    k.xx = reinterpret_cast<T*>(static_cast<char*>(P.px->region) + P.px->off_x);
+  }
   if (P.while_capture) {
     k.iter = P.iter_dev.get();
     k.cond = P.cond;
@@ -2658,7 +2934,59 @@ void launch_xchg(Plan& P, const SartK<T>& k, int it, bool fwd, bool with_reduce 
 }
 
 template <class T>
+XchgFn<T> xchg_pair_kernel(const Plan& P, bool fwd) {
+  const int vs = fwd ? P.vs_fwd : P.vs_back;
+  const int uf = fwd ? P.uf_fwd : P.uf_back;
+  const int tl = P.layout_mode(fwd);
+#define SSB_XP(V, U)                                                                          \
+  if (vs == V && uf == U) {                                                                   \
+    if (tl == 4) return fwd ? sart_fwd_xchg_pair_kernel<T, V, U, 4> : sart_back_xchg_pair_kernel<T, V, U, 4>; \
+    if (tl == 5) return fwd ? sart_fwd_xchg_pair_kernel<T, V, U, 5> : sart_back_xchg_pair_kernel<T, V, U, 5>; \
+    if (tl == 6) return fwd ? sart_fwd_xchg_pair_kernel<T, V, U, 6> : sart_back_xchg_pair_kernel<T, V, U, 6>; \
+  }
+  SSB_XP(4, 2) SSB_XP(8, 2) SSB_XP(16, 2) SSB_XP(32, 2)
+  SSB_XP(4, 4) SSB_XP(8, 4) SSB_XP(16, 4) SSB_XP(32, 4)
+#undef SSB_XP
+  fail("plan: unsupported paired peer-exchange kernel shape");
+  return nullptr;
+}
+
+// paired variant of launch_xchg (same phases)
+template <class T>
+void launch_xchg_pair(Plan& P, const SartK<T>& k, int it, bool fwd, bool with_reduce = true,
+                      bool with_back = true) {
+  const XK<T> x = make_xargs<T>(P);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(fwd ? P.fwd_blocks : P.back_blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = P.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (!with_back) {
+    cfg.gridDim = dim3(P.px->rgrid);
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_reduce_pair_kernel<T>, k, x, it));
+    P.ctx->check_launch("xchg_reduce_pair_kernel");
+    return;
+  }
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_pair_kernel<T>(P, fwd), k, x, it));
+  P.ctx->check_launch(fwd ? "sart_fwd_xchg_pair_kernel" : "sart_back_xchg_pair_kernel");
+  if (fwd || !with_reduce) return;
+  cfg.gridDim = dim3(P.px->rgrid);
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, xchg_reduce_pair_kernel<T>, k, x, it));
+  P.ctx->check_launch("xchg_reduce_pair_kernel");
+}
+
+template <class T>
 void launch_announce(Plan& P, int it, int kind) {
+  if (P.paired) {
+    xchg_announce_pair_kernel<T><<<1, 32, 0, P.ctx->stream>>>(make_args<T>(P), make_xargs<T>(P),
+                                                              it, kind);
+    P.ctx->check_launch("xchg_announce_pair_kernel");
+    return;
+  }
   xchg_announce_kernel<T><<<1, 32, 0, P.ctx->stream>>>(make_args<T>(P), make_xargs<T>(P), it,
                                                        kind);
   P.ctx->check_launch("xchg_announce_kernel");
@@ -2667,6 +2995,11 @@ void launch_announce(Plan& P, int it, int kind) {
 template <class T>
 void launch_xchg_final(Plan& P) {
   const SartK<T> k = make_args<T>(P);
+  if (P.paired) {
+    xchg_final_pair_kernel<T><<<1, 32, 0, P.ctx->stream>>>(k, make_xargs<T>(P));
+    P.ctx->check_launch("xchg_final_pair_kernel");
+    return;
+  }
   xchg_final_kernel<T><<<1, 32, 0, P.ctx->stream>>>(k, make_xargs<T>(P));
   P.ctx->check_launch("xchg_final_kernel");
 }
@@ -2712,6 +3045,11 @@ void do_iterations(Plan& P, int first, int count) {
     return;
   }
   for (int it = first; it < first + count; ++it) {
+    if (P.px && P.paired) {  // the row-sharded pair: K1x, K2x + reduce, both systems
+      launch_xchg_pair<T>(P, k, it, true);
+      launch_xchg_pair<T>(P, k, it, false);
+      continue;
+    }
     if (P.px) {  // K1x over local rows, K2x with the fused peer exchange
       launch_xchg<T>(P, k, it, true);
       launch_xchg<T>(P, k, it, false);
@@ -2770,6 +3108,7 @@ Plan::~Plan() {
   if (ev1) cudaEventDestroy(ev1);
   delete px;
   delete own;
+  delete own2;
   delete pair_own[0];
   delete pair_own[1];
 }
@@ -2782,8 +3121,9 @@ void Plan::enqueue_reset() {
   if (px) {  // own replica and divergence flag only: peers never touch them
     // before this rank's first arrival of the solve (see sart.cu peer exchange)
     char* r = static_cast<char*>(px->region);
-    SSB_CUDA(cudaMemsetAsync(r + px->off_x, 0, cols[0] * tsize(), ctx->stream));
-    SSB_CUDA(cudaMemsetAsync(r + px->off_dflag, 0, sizeof(int), ctx->stream));
+    const std::size_t ns = paired ? 2 : 1;
+    SSB_CUDA(cudaMemsetAsync(r + px->off_x, 0, cols[0] * tsize() * ns, ctx->stream));
+    SSB_CUDA(cudaMemsetAsync(r + px->off_dflag, 0, ns * sizeof(int), ctx->stream));
     SSB_CUDA(cudaMemsetAsync(px->local.get() + 1, 0, sizeof(long long), ctx->stream));
     SSB_CUDA(cudaMemsetAsync(px->local.get() + 3, 0, sizeof(long long), ctx->stream));
   }
@@ -2800,9 +3140,14 @@ void Plan::enqueue_epilogue() {
   if (px) {  // settle the last iteration, then the replica is the solution
     if (dtype == SS_F32) launch_xchg_final<float>(*this);
     else launch_xchg_final<double>(*this);
-    SSB_CUDA(cudaMemcpyAsync(x[0].get(), static_cast<char*>(px->region) + px->off_x,
-                             cols[0] * tsize(), cudaMemcpyDeviceToDevice, ctx->stream));
-    return;
+    if (paired) {  // interleaved replica -> xx -> x1, x2 (below)
+      SSB_CUDA(cudaMemcpyAsync(xx.get(), static_cast<char*>(px->region) + px->off_x,
+                               2 * cols[0] * tsize(), cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      SSB_CUDA(cudaMemcpyAsync(x[0].get(), static_cast<char*>(px->region) + px->off_x,
+                               cols[0] * tsize(), cudaMemcpyDeviceToDevice, ctx->stream));
+      return;
+    }
   }
   if (!paired) return;
   const int g = grid1(ctx, cols[0]);
@@ -2976,7 +3321,7 @@ void Plan::finish_rhs(int which) {
   ctx->check_launch("pnorm_kernel");
   if (sharded && px && px->emulated) {
     // emulated ranks: run_group combines the ranks' local ||p_g||
-    ctx->copy(&pn_local, pn, sizeof(double));
+    ctx->copy(&pn_local[which], pn, sizeof(double));
   } else if (sharded) {
     // ||p||^2 = sum over ranks of the local ||p_g||^2
     square_kernel<<<1, 32, 0, ctx->stream>>>(pn, nrhs);
@@ -3815,6 +4160,7 @@ std::vector<unsigned char> exchange_table(Context* ctx, int G, int me,
 // every rank derives the same ones.
 void setup_exchange(Plan& P, int G, int me, bool emulated, bool* joined) {
   Context* ctx = P.ctx;
+  const std::size_t ns = P.paired ? 2 : 1;  // systems per message (paired: {s1, s2} pairs)
   auto X = std::make_unique<PeerExchange>();
   X->G = G;
   X->me = me;
@@ -3826,9 +4172,9 @@ void setup_exchange(Plan& P, int G, int me, bool emulated, bool* joined) {
       8LL * ctx->sm_count, std::max<std::int64_t>(ctx->sm_count, (X->own + 255) / 256)));
   const std::size_t tb = P.tsize();
   X->off_recv = 0;
-  X->off_x = align256(static_cast<std::size_t>(G) * X->cols * tb + kSlackBytes);
-  X->off_r2 = align256(X->off_x + X->cols * tb + kSlackBytes);
-  X->off_done = align256(X->off_r2 + 2 * G * sizeof(double));
+  X->off_x = align256(static_cast<std::size_t>(G) * X->cols * tb * ns + kSlackBytes);
+  X->off_r2 = align256(X->off_x + X->cols * tb * ns + kSlackBytes);
+  X->off_done = align256(X->off_r2 + 2 * G * ns * sizeof(double));
   X->off_xready = X->off_done + 64;
   X->off_dflag = X->off_xready + 64;
   X->bytes = align256(X->off_dflag + 64);
@@ -3913,17 +4259,21 @@ void run_group(Plan* const* plans, int parts) {
     }
   }
   Context* ctx = P0.ctx;
-  // ||p||^2 = sum of the ranks' local ||p_g||^2, in rank order
-  double sq = 0.0;
-  for (int g = 0; g < parts; ++g) {
-    const double v = plans[g]->pn_local;
-    if (v < 0.0) fail("plan: group rank " + std::to_string(g) + " has no rhs");
-    sq += v * v;
+  // ||p||^2 = sum of the ranks' local ||p_g||^2, in rank order (per system)
+  const int ns = P0.paired ? 2 : 1;
+  double pn[2] = {0.0, 0.0};
+  for (int q = 0; q < ns; ++q) {
+    double sq = 0.0;
+    for (int g = 0; g < parts; ++g) {
+      const double v = plans[g]->pn_local[q];
+      if (v < 0.0) fail("plan: group rank " + std::to_string(g) + " has no rhs");
+      sq += v * v;
+    }
+    pn[q] = std::sqrt(sq);
   }
-  const double pn = std::sqrt(sq);
   for (int g = 0; g < parts; ++g) {
-    SSB_CUDA(cudaMemcpyAsync(plans[g]->pnorm.get(), &pn, sizeof pn, cudaMemcpyHostToDevice,
-                             ctx->stream));
+    SSB_CUDA(cudaMemcpyAsync(plans[g]->pnorm.get(), pn, ns * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->stream));
   }
   ctx->sync();
   for (int g = 0; g < parts; ++g) plans[g]->enqueue_reset();
@@ -3938,22 +4288,23 @@ void run_group(Plan* const* plans, int parts) {
   };
   for (int it = 0; it < P0.opts.max_iters; ++it) {
     announce(it, 0);
-    for (int g = 0; g < parts; ++g) {
-      Plan& P = *plans[g];
-      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, true);
-      else launch_xchg<double>(P, make_args<double>(P), it, true);
-    }
-    for (int g = 0; g < parts; ++g) {
-      Plan& P = *plans[g];
-      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, false, false);
-      else launch_xchg<double>(P, make_args<double>(P), it, false, false);
-    }
+    // phase: 0 K1x, 1 K2x, 2 reduce
+    const auto phase = [&](Plan& P, int ph) {
+      const bool fwd = ph == 0, red = ph == 2;
+      if (P.dtype == SS_F32) {
+        const SartK<float> k = make_args<float>(P);
+        if (P.paired) launch_xchg_pair<float>(P, k, it, fwd, false, !red);
+        else launch_xchg<float>(P, k, it, fwd, false, !red);
+      } else {
+        const SartK<double> k = make_args<double>(P);
+        if (P.paired) launch_xchg_pair<double>(P, k, it, fwd, false, !red);
+        else launch_xchg<double>(P, k, it, fwd, false, !red);
+      }
+    };
+    for (int g = 0; g < parts; ++g) phase(*plans[g], 0);
+    for (int g = 0; g < parts; ++g) phase(*plans[g], 1);
     announce(it, 1);
-    for (int g = 0; g < parts; ++g) {
-      Plan& P = *plans[g];
-      if (P.dtype == SS_F32) launch_xchg<float>(P, make_args<float>(P), it, false, true, false);
-      else launch_xchg<double>(P, make_args<double>(P), it, false, true, false);
-    }
+    for (int g = 0; g < parts; ++g) phase(*plans[g], 2);
   }
   announce(P0.opts.max_iters, 2);
   for (int g = 0; g < parts; ++g) plans[g]->enqueue_epilogue();
@@ -4086,6 +4437,105 @@ Plan* make_sharded_plan_local(Context* ctx, Matrix* a, std::int64_t rb, std::int
   }
   ctx->sync();
   return P.release();
+}
+
+// Rows [rb, re) of matrix a as a local matrix on ctx (host-side CSR slice).
+Matrix* row_block(Context* ctx, Matrix* a, std::int64_t rb, std::int64_t re) {
+  std::vector<int> ptr(a->rows + 1);
+  ctx->copy(ptr.data(), a->rowptr.get(), ptr.size() * sizeof(int));
+  const std::int64_t k0 = ptr[rb], k1 = ptr[re], nloc = k1 - k0, rloc = re - rb;
+  std::vector<int> lcol(nloc), lrow(nloc);
+  std::vector<double> lval(nloc);
+  ctx->copy(lcol.data(), a->colidx.get() + k0, nloc * sizeof(int));
+  ctx->copy(lval.data(), a->val.get() + k0, nloc * sizeof(double));
+  for (std::int64_t r = 0; r < rloc; ++r) {
+    for (int k = ptr[rb + r]; k < ptr[rb + r + 1]; ++k) lrow[k - k0] = static_cast<int>(r);
+  }
+  return matrix_from_triplets_host(ctx, rloc, a->cols, nloc, lrow.data(), lcol.data(),
+                                   lval.data());
+}
+
+// The folded pair row-sharded over all ranks of the exchange (see "paired
+// peer exchange"): rows [rb, re) of A1 and A2 on the paired mirror-coded
+// streams of an ordinary paired plan over the local row blocks; the column
+// normalisers come from the full matrices (every rank holds the same ones).
+Plan* make_sharded_pair_plan_local(Context* ctx, Matrix* a1, Matrix* a2, std::int64_t rb,
+                                   std::int64_t re, const ss_solve_options& o, int emul_parts,
+                                   int emul_rank, bool* joined) {
+  if (!a2 || a1->rows != a2->rows || a1->cols != a2->cols) {
+    fail("plan: folded systems must have equal shapes");
+  }
+  if (rb < 0 || re > a1->rows || rb > re) fail("plan: row range out of bounds");
+  if (o.relaxation <= 0 || o.relaxation > 2) fail("sart_solve: relaxation must be in (0, 2]");
+  if (o.max_iters < 1) fail("sart_solve: max_iters must be >= 1");
+  std::unique_ptr<Matrix> l1(row_block(ctx, a1, rb, re)), l2(row_block(ctx, a2, rb, re));
+  std::unique_ptr<Plan> P(make_plan(ctx, l1.get(), l2.get(), o, 1, false));
+  if (!P->paired || !P->tiled || !P->mir_f || !P->mir_b) {
+    fail("plan: the row-sharded pair needs the paired mirror-coded streams");
+  }
+  P->own = l1.release();
+  P->own2 = l2.release();
+  P->persistent = false;  // the exchange kernels run the loop
+  P->sharded = true;
+  P->row_begin = rb;
+  P->row_end = re;
+  // column normalisers of the full matrices, then the interleaved {cinv1, cinv2}
+  const std::int64_t cols = a1->cols;
+  for (int s = 0; s < 2; ++s) {
+    Matrix* a = s ? a2 : a1;
+    DBuf<double> rs_full(a->rows), cs_full(cols);
+    ctx->sync();
+    abs_sums(*a, rs_full.get(), cs_full.get());
+    a->ctx->sync();
+    const int gc = grid1(ctx, cols);
+    if (o.dtype == SS_F32) {
+      inv_kernel<float><<<gc, 256, 0, ctx->stream>>>(
+          cs_full.get(), reinterpret_cast<float*>(P->cinv[s].get()), cols);
+      interleave_kernel<float, float><<<gc, 256, 0, ctx->stream>>>(
+          reinterpret_cast<const float*>(P->cinv[s].get()), reinterpret_cast<float*>(P->cc.get()),
+          cols, 2, s);
+    } else {
+      inv_kernel<double><<<gc, 256, 0, ctx->stream>>>(
+          cs_full.get(), reinterpret_cast<double*>(P->cinv[s].get()), cols);
+      interleave_kernel<double, double><<<gc, 256, 0, ctx->stream>>>(
+          reinterpret_cast<const double*>(P->cinv[s].get()),
+          reinterpret_cast<double*>(P->cc.get()), cols, 2, s);
+    }
+    ctx->check_launch("inv_kernel(full columns)");
+    if (!(max_dev(ctx, rs_full.get(), a->rows) > 0.0)) P->empty_rows[s] = true;
+    else P->empty_rows[s] = false;
+  }
+  ctx->sync();
+  if (emul_parts > 0) setup_exchange(*P, emul_parts, emul_rank, true, joined);
+  else setup_exchange(*P, ctx->nranks, ctx->rank, false, joined);
+  ctx->sync();
+  // real ranks, fixed pass count: the 3 launches per pass replay from one
+  // captured graph (the host would otherwise pace a many-GPU loop)
+  if (emul_parts == 0 && env_int("SSB_GRAPH", 1) != 0) P->build_graph();
+  return P.release();
+}
+
+Plan* make_sharded_pair_plan(Context* ctx, Matrix* a1, Matrix* a2, std::int64_t rb,
+                             std::int64_t re, const ss_solve_options& o, int emul_parts,
+                             int emul_rank) {
+  if (emul_parts > 0) {
+    if (emul_rank < 0 || emul_rank >= emul_parts) fail("plan: emulated rank out of range");
+  } else if (!ctx->comm) {
+    fail("plan: context has no NCCL communicator");
+  }
+  const bool joins = emul_parts == 0 && ctx->nranks > 1;
+  bool joined = false;
+  try {
+    return make_sharded_pair_plan_local(ctx, a1, a2, rb, re, o, emul_parts, emul_rank, &joined);
+  } catch (...) {
+    if (joins && !joined) {
+      try {
+        exchange_table(ctx, ctx->nranks, ctx->rank, nullptr);
+      } catch (...) {
+      }
+    }
+    throw;
+  }
 }
 
 // ====================================================================== paired CGLS

@@ -1,5 +1,11 @@
 """Multi-GPU layouts of the folded-SART path, one process per GPU.
 
+Default (bench.py, N >= 2): the folded PAIR row-sharded over all N ranks
+(make_sharded_pair_plan): every rank keeps the same row block of A1 and A2 on
+the paired mirror-coded streams, so each GPU streams 1/N of the single-GPU
+bytes; {u1, u2} back-projection pairs travel through the fused peer-memory
+exchange. The SURVEY layouts below stay as the fallback (SSB_LAYOUT=halves):
+
 world == 2: rank r solves folded system r; no data-path collective.
 world >= 4 (even): ranks [0, W/2) hold A1, ranks [W/2, W) hold A2; each
 group splits its system into nnz-balanced row blocks and combines the
@@ -39,3 +45,21 @@ def make_sharded_plan(P, ctx, split, opts, rank: int, world: int, exchange: str 
     plan = P.symsplit.ShardedSartPlan(ctx, a, rb, re, opts, exchange=exchange)
     plan.set_rhs(0, p[rb:re])
     return plan
+
+
+def make_sharded_pair_plan(P, ctx, split, opts, rank: int, world: int):
+    """Rows [rb, re) of both folded systems on this rank (nnz-balanced row
+    blocks of the shared pattern); one NCCL communicator over all ranks carries
+    only the one-time IPC handle exchange. Returns (plan, (rb, re))."""
+    import torch.distributed as tdist
+
+    obj = [P.symsplit.nccl_unique_id() if rank == 0 else None]
+    grp = tdist.new_group(list(range(world)), backend="gloo")
+    tdist.broadcast_object_list(obj, src=0, group=grp)
+    P.symsplit.attach_nccl(ctx, obj[0], world, rank)
+    bounds = P.symsplit.partition_rows(split.a1.to_csr()[0], world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    plan = P.symsplit.ShardedPairPlan(ctx, split.a1, split.a2, rb, re, opts)
+    plan.set_rhs(0, split.p1[rb:re])
+    plan.set_rhs(1, split.p2[rb:re])
+    return plan, (rb, re)

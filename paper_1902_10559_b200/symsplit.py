@@ -813,15 +813,38 @@ class ShardedSartPlan(SartPlan):
         self.cols = a.shape[1]
 
 
+class ShardedPairPlan(SartPlan):
+    """Rows [row_begin, row_end) of BOTH folded systems on this rank (the
+    row-sharded pair: every rank streams 1/N of the paired mirror-coded
+    streams); {u1, u2} back-projection pairs travel through the fused
+    peer-memory exchange. solution(0 / 1) and recombine() give the full
+    iterates (every rank holds a replica)."""
+
+    def __init__(self, ctx: Context, a1: Matrix, a2: Matrix, row_begin: int, row_end: int,
+                 opts: Optional[SolveOptions] = None):
+        self.opts = opts or SolveOptions()
+        self.ctx = ctx
+        self.nsys = 2
+        self.nrhs = 1
+        self.a = (a1, a2)
+        h = N.vp()
+        o = self.opts._c()
+        _check(_lib().ss_plan_create_sharded_pair(ctx.h, a1.h, a2.h, row_begin, row_end,
+                                                  C.byref(o), C.byref(h)))
+        self.h = h
+        self.rows = row_end - row_begin
+        self.cols = a1.shape[1]
+
+
 class _GroupMember(SartPlan):
     """One emulated rank of a ShardGroup (owns its ss_plan_t)."""
 
-    def __init__(self, ctx, a, h, rows, opts):
+    def __init__(self, ctx, a, h, rows, opts, a2=None):
         self.opts = opts
         self.ctx = ctx
-        self.nsys = 1
+        self.nsys = 2 if a2 is not None else 1
         self.nrhs = 1
-        self.a = (a, None)
+        self.a = (a, a2)
         self.h = h
         self.rows = rows
         self.cols = a.shape[1]
@@ -865,3 +888,47 @@ class ShardGroup:
 
     def history(self, rank=0):
         return self.ranks[rank].history(0)
+
+
+class ShardPairGroup:
+    """One-device emulation of `parts` ranks of the row-sharded PAIR
+    (ss_plan_create_sharded_pair_group / ss_plan_group_run): both folded
+    systems row-sharded over all ranks on the paired streams, {u1, u2}
+    exchanged through the same arrival counters and rank-order reductions as
+    on real ranks."""
+
+    def __init__(self, a1: Matrix, a2: Matrix, parts: int,
+                 opts: Optional[SolveOptions] = None, bounds=None):
+        self.opts = opts or SolveOptions()
+        self.parts = parts
+        if bounds is None:
+            bounds = partition_rows(a1.to_csr()[0], parts)
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        hs = (N.vp * parts)()
+        o = self.opts._c()
+        _check(_lib().ss_plan_create_sharded_pair_group(a1.ctx.h, a1.h, a2.h, parts,
+                                                        self.bounds.ctypes.data_as(N.i64p),
+                                                        C.byref(o), hs))
+        self.hs = hs
+        self.ranks = [_GroupMember(a1.ctx, a1, N.vp(hs[g]),
+                                   int(self.bounds[g + 1] - self.bounds[g]), self.opts, a2)
+                      for g in range(parts)]
+
+    def set_rhs(self, p1, p2):
+        p1, p2 = _f64(p1), _f64(p2)
+        for g, r in enumerate(self.ranks):
+            r.set_rhs(0, p1[self.bounds[g]:self.bounds[g + 1]])
+            r.set_rhs(1, p2[self.bounds[g]:self.bounds[g + 1]])
+
+    def run(self):
+        _check(_lib().ss_plan_group_run(self.hs, self.parts))
+        return [r.finish() for r in self.ranks]
+
+    def solution(self, which, rank=0):
+        return self.ranks[rank].solution(which)
+
+    def history(self, which, rank=0):
+        return self.ranks[rank].history(which)
+
+    def recombine(self, rank=0):
+        return self.ranks[rank].recombine()

@@ -126,6 +126,101 @@ def peer_sharded_sart(rank, world, ptr, idx, val, p, iters, relax, tol):
     return x, hist, own
 
 
+def peer_pair_sharded_sart(rank, world, m1, m2, p1, p2, iters, relax, tol):
+    """The row-sharded PAIR (ss_plan_create_sharded_pair): both folded systems
+    split into the same row blocks (partition_rows of the shared pattern), one
+    {u1, u2} receive row per rank and owner, ||r_g||^2 pairs summed in rank
+    order, each system with its own check-before-update stop."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1902_10559_b200 as P
+    mats = [m1, m2]
+    ps = [p1, p2]
+    ptr0 = mats[0][0]
+    rows, ncols = len(ptr0) - 1, int(max(m[1].max() for m in mats)) + 1
+    bounds = P.symsplit.partition_rows(ptr0, world)
+    rb, re = int(bounds[rank]), int(bounds[rank + 1])
+    own = [P.symsplit.exchange_owned_columns(ncols, world, g) for g in range(world)]
+    j0, j1 = own[rank]
+    loc, rinv, cinv, pl, pnorm = [], [], [], [], []
+    for (ptr, idx, val), p in zip(mats, ps):
+        loc.append((ptr[rb:re + 1] - ptr[rb], idx[ptr[rb]:ptr[re]], val[ptr[rb]:ptr[re]]))
+        rsum = np.add.reduceat(np.abs(val), ptr[:-1])
+        rsum[np.diff(ptr) == 0] = 0.0
+        csum = np.bincount(idx, weights=np.abs(val), minlength=ncols)
+        rinv.append(np.where(rsum > 0, 1.0 / np.where(rsum > 0, rsum, 1.0), 0.0)[rb:re])
+        cinv.append(np.where(csum > 0, 1.0 / np.where(csum > 0, csum, 1.0), 0.0))
+        pl.append(p[rb:re])
+        g2 = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(g2, torch.tensor([float(p[rb:re] @ p[rb:re])], dtype=torch.float64))
+        pnorm.append(float(np.sqrt(sum(float(t.item()) for t in g2))))
+    x = [np.zeros(ncols), np.zeros(ncols)]
+    hist = [[], []]
+    on = [True, True]
+    for it in range(iters):
+        if not any(on):
+            break
+        part = np.zeros((ncols, 2))
+        r2 = np.zeros(2)
+        for q in range(2):
+            if not on[q]:
+                continue
+            lp, li, lv = loc[q]
+            r = pl[q] - csr_matvec(lp, li, lv, x[q])
+            part[:, q] = csr_rmatvec(lp, li, lv, rinv[q] * r, ncols)
+            r2[q] = float(r @ r)
+        recv = [torch.zeros(ncols * 2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(recv, torch.from_numpy(part.reshape(-1)))  # {u1, u2} rows
+        r2s = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(r2s, torch.from_numpy(r2))
+        width = max(e - b for b, e in own)
+        for q in range(2):
+            if not on[q]:
+                continue
+            t = 0.0
+            for g in range(world):                        # rank order
+                t += float(r2s[g][q].item())
+            res = np.sqrt(t)
+            hist[q].append(res)
+            if res <= tol * pnorm[q]:
+                on[q] = False                             # this system stops here
+                continue
+            s_ = recv[0].numpy().reshape(ncols, 2)[j0:j1, q].copy()
+            for g in range(1, world):
+                s_ = s_ + recv[g].numpy().reshape(ncols, 2)[j0:j1, q]
+            mine = x[q][j0:j1] + relax * (s_ * cinv[q][j0:j1])
+            buf = torch.zeros(width, dtype=torch.float64)
+            buf[:j1 - j0] = torch.from_numpy(mine)
+            pushed = [torch.zeros(width, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(pushed, buf)
+            x[q] = np.concatenate([pushed[g].numpy()[:own[g][1] - own[g][0]]
+                                   for g in range(world)])
+    return x, hist, (rb, re)
+
+
+def peer_pair_worker(rank, world, port, q, iters, tol):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    import pyoracle as O
+    from helpers import oracle_workload
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, cfg, a, csr, f_true, p = oracle_workload(1, literal=True)
+        f1, f2 = O.fold_rows_csr(csr)
+        p1, p2 = O.split_rhs(p)
+        q.put((rank, peer_pair_sharded_sart(rank, world, f1.arrays(), f2.arrays(), p1, p2,
+                                            iters, w.relaxation, tol)))
+    finally:
+        dist.destroy_process_group()
+
+
 def peer_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
@@ -255,3 +350,56 @@ def test_group_layout():
         group_layout(0, 2)
     with pytest.raises(ValueError):
         group_layout(0, 6 + 1)
+
+
+def run_pair_protocol(world, iters, tol):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=peer_pair_worker, args=(r, world, port, q, iters, tol))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    return results
+
+
+def test_pair_exchange_protocol_matches_oracle():
+    """The row-sharded pair over gloo at world size 2: both systems' iterates
+    and histories equal the oracle's per-system sart_solve, replicas agree bit
+    for bit, and the recombined f equals the oracle's solve_split."""
+    import pyoracle as O
+    from helpers import oracle_workload
+    world = 2
+    results = run_pair_protocol(world, 30, 0.0)
+    w, cfg, a, csr, f_true, p = oracle_workload(1, literal=True)
+    split = O.split_system(a, p, 0.0)
+    (xa, ha, ra), (xb, hb, rb) = results[0], results[1]
+    assert ra[0] == 0 and ra[1] == rb[0] and rb[1] == split.a1.shape[0]
+    for q, (m, pp) in enumerate(((split.a1, split.p1), (split.a2, split.p2))):
+        want = O.sart_solve(m, pp, max_iters=30, tol=0.0, relaxation=w.relaxation)
+        assert xa[q].tobytes() == xb[q].tobytes() and ha[q] == hb[q]
+        assert np.linalg.norm(xa[q] - want.f) <= 1e-10 * np.linalg.norm(want.f)
+        assert np.allclose(ha[q], want.residual_history, rtol=1e-10, atol=0)
+    f = O.recombine_solution(xa[0], xa[1])
+    full = O.solve_split(a, p, 0.0, 30, 0.0, w.relaxation)
+    assert np.linalg.norm(f - full.f) <= 1e-10 * np.linalg.norm(full.f)
+
+
+def test_pair_exchange_protocol_independent_stops():
+    """tol > 0: each system stops at the oracle's iteration for that system."""
+    import pyoracle as O
+    from helpers import oracle_workload
+    w, cfg, a, csr, f_true, p = oracle_workload(1, literal=True)
+    split = O.split_system(a, p, 0.0)
+    tol = 0.05
+    results = run_pair_protocol(2, 200, tol)
+    for q, (m, pp) in enumerate(((split.a1, split.p1), (split.a2, split.p2))):
+        want = O.sart_solve(m, pp, max_iters=200, tol=tol, relaxation=w.relaxation)
+        x, h, _ = results[0]
+        assert len(h[q]) == len(want.residual_history)
+        assert np.linalg.norm(x[q] - want.f) <= 1e-10 * np.linalg.norm(want.f)

@@ -131,3 +131,95 @@ def test_peer_plan_single_rank_nccl():
         assert sh.solution(0).tobytes() == first.tobytes()
         assert rel_err(first, f_ref) <= tol
         assert np.allclose(sh.history(0), h_ref, rtol=tol)
+
+
+# ---------------------------------------------------------------- the row-sharded pair
+def unsharded_pair(gs, opts):
+    ref = P.SartPlan(gs.a1, gs.a2, opts)
+    ref.set_rhs(0, gs.p1)
+    ref.set_rhs(1, gs.p2)
+    rep = ref.run()
+    return ref, rep.iterations
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("parts", [1, 2, 3, 4])
+def test_pair_group_matches_unsharded_pair(dtype, parts):
+    """Both folded systems row-sharded over G ranks on the paired streams:
+    the unsharded paired plan within 1e-12 (fp64) / 1e-5 (fp32), every rank's
+    replica bitwise identical."""
+    w, gs = folded(2)
+    opts = P.SolveOptions(max_iters=20, tol=0.0, relaxation=w.relaxation, dtype=dtype)
+    ref, _ = unsharded_pair(gs, opts)
+    grp = P.symsplit.ShardPairGroup(gs.a1, gs.a2, parts, opts)
+    grp.set_rhs(gs.p1, gs.p2)
+    reps = grp.run()
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    assert all(r.iterations == 20 for r in reps)
+    for which in (0, 1):
+        f0 = grp.solution(which)
+        assert rel_err(f0, ref.solution(which)) <= tol
+        for g in range(parts):
+            assert grp.solution(which, g).tobytes() == f0.tobytes()
+            h = grp.history(which, g)
+            assert len(h) == 20 and np.allclose(h, ref.history(which), rtol=tol, atol=0)
+    assert rel_err(grp.recombine(parts - 1), ref.recombine()) <= tol
+
+
+def test_pair_group_matches_oracle_and_repeats():
+    """config 1 at its full 50 iterations against the oracle solve_split
+    (north-star 1e-10); repeated solves are bitwise identical."""
+    w, gs = folded(1)
+    opts = P.SolveOptions(max_iters=w.iters, tol=0.0, relaxation=w.relaxation, dtype="f64")
+    grp = P.symsplit.ShardPairGroup(gs.a1, gs.a2, 4, opts)
+    grp.set_rhs(gs.p1, gs.p2)
+    grp.run()
+    a, p = _cache[1][2:]
+    want = O.solve_split(a, p, 0.0, w.iters, 0.0, w.relaxation)
+    f = grp.recombine(0)
+    assert rel_err(f, want.f) <= 1e-10
+    for _ in range(2):
+        grp.run()
+        assert grp.recombine(3).tobytes() == f.tobytes()
+
+
+def test_pair_group_independent_stops():
+    """tol > 0: each system stops at its own iteration (check before update),
+    as in the unsharded pair plan; the other system keeps iterating."""
+    w, gs = folded(2)
+    probe = P.SolveOptions(max_iters=60, tol=0.0, relaxation=w.relaxation, dtype="f64")
+    ref, _ = unsharded_pair(gs, probe)
+    h1, h2 = ref.history(0), ref.history(1)
+    # a tolerance between the two systems' relative residual curves
+    r1, r2 = h1 / np.linalg.norm(gs.p1), h2 / np.linalg.norm(gs.p2)
+    tol = float(max(r1[9], r2[9]))
+    opts = P.SolveOptions(max_iters=60, tol=tol, relaxation=w.relaxation, dtype="f64")
+    ref, it_ref = unsharded_pair(gs, opts)
+    grp = P.symsplit.ShardPairGroup(gs.a1, gs.a2, 3, opts)
+    grp.set_rhs(gs.p1, gs.p2)
+    reps = grp.run()
+    assert all(r.iterations == it_ref for r in reps)
+    for which in (0, 1):
+        assert len(grp.history(which, 1)) == len(ref.history(which))
+        assert rel_err(grp.solution(which, 2), ref.solution(which)) <= 1e-12
+
+
+def test_pair_plan_single_rank_nccl():
+    """The real setup path of the row-sharded pair with a one-rank communicator."""
+    import torch  # noqa: F401
+    w, gs = folded(2)
+    ctx = P.Context(0)
+    P.symsplit.attach_nccl(ctx, P.symsplit.nccl_unique_id(), 1, 0)
+    for dtype in ("f64", "f32"):
+        opts = P.SolveOptions(max_iters=20, tol=0.0, relaxation=w.relaxation, dtype=dtype)
+        ref, _ = unsharded_pair(gs, opts)
+        rows = gs.a1.shape[0]
+        sh = P.symsplit.ShardedPairPlan(ctx, gs.a1, gs.a2, 0, rows, opts)
+        sh.set_rhs(0, gs.p1)
+        sh.set_rhs(1, gs.p2)
+        sh.run()
+        first = sh.recombine()
+        sh.run()
+        tol = 1e-12 if dtype == "f64" else 1e-5
+        assert sh.recombine().tobytes() == first.tobytes()
+        assert rel_err(first, ref.recombine()) <= tol
