@@ -61,6 +61,13 @@ struct Plan {
   DBuf<char> xx, ww;      // paired: interleaved x [cols][2] and w [rows][2]
   DBuf<char> rv2, cv2;    // paired: CSR / CSC values interleaved [nnz][2]
   DBuf<char> pe, cc;      // paired: {p1,p2,rinv1,rinv2} per row, {cinv1,cinv2} per column
+  // multi-RHS block-merged streams (sart_*_block_kernel): per direction the
+  // union list of every block of kBlockR vectors over both folded systems
+  bool blocked_f = false, blocked_b = false;
+  int block_e_f = 4, block_e_b = 2;  // union entries' gathers in flight per lane
+  DBuf<int> bptr_f, bidx_f, bptr_b, bidx_b;
+  DBuf<char> bval_f, bval_b;
+  std::int64_t nblk_f = 0, nblk_b = 0, nu_f = 0, nu_b = 0;
   int nband = 1;          // multi-RHS K1 passes over column bands
   DBuf<int> band_ptr[2];  // per system [nband + 1][rows] positions inside the CSR rows
   // paired + tiled: rows/columns padded to 4 entries and permuted within tiles

@@ -1720,6 +1720,225 @@ __global__ void __launch_bounds__(kThreads, Q == 1 ? 4 : 1) sart_back_multi_kern
   }
 }
 
+// ------------------------------------------------------------ block-merged multi-RHS
+// Adjacent rays (rows) share most of their voxels, and adjacent voxels most of
+// their rays: a block of R consecutive vectors touches ~2.2x fewer distinct
+// indices than its R vectors together (config 4: 1,161 columns for 4 rows of
+// 624). The plan merges each block's R vectors of BOTH folded systems into one
+// sorted union list: per union index its 2R values (zero where a vector has no
+// entry). A warp owns one block: it stages 32 union entries at a time in
+// shared memory (read back as broadcasts), gathers each S-wide record of the
+// dense operand once and applies it to all R vectors of both systems, whose
+// accumulators stay in registers ([R][2][V] per lane, V slices per lane). The
+// X (K1) / W (K2) record of an index is thus read once per block instead of
+// once per vector and system. Summation order per vector: union order (=
+// ascending index, as the vector's own CSR/CSC order), one product at a time.
+template <class T>
+struct BlockK {
+  const int* ptr;  // [nblk + 1] union range of block b
+  const int* idx;  // [nu] union indices
+  const T* val;    // [nu][2][R] values: system s, vector r of the block
+  long long nblk;
+};
+
+template <class T, int V>
+__device__ __forceinline__ void ldv(const T* __restrict__ p, T (&o)[V], bool nc) {
+  if (nc) {
+    loadv<T, V>(p, o);
+  } else {
+#pragma unroll
+    for (int t = 0; t < V; ++t) o[t] = p[t];
+  }
+}
+
+constexpr int kBlockR = 4;     // vectors per block
+constexpr int kBlockStage = 32;  // union entries staged per warp at a time
+
+// acc[r][s][t] += sum over the block's union of val[s][r] * D_s[idx][slice t]
+template <class T, int V, int E>
+__device__ __forceinline__ void block_dot(const BlockK<T>& b, const T* __restrict__ d0,
+                                          const T* __restrict__ d1, int u0, int u1, int lane,
+                                          int S, int sl, int* sidx, T* sval,
+                                          T (&acc)[kBlockR][2][V]) {
+  constexpr int R = kBlockR;
+  for (int ub = u0; ub < u1; ub += kBlockStage) {
+    const int cnt = min(kBlockStage, u1 - ub);
+    // stage: lane t copies entry ub + t (index + 2R values); zeros past the end
+    {
+      const int u = ub + lane;
+      const bool on = lane < cnt;
+      sidx[lane] = on ? __ldg(b.idx + u) : 0;
+#pragma unroll
+      for (int q = 0; q < 2 * R; ++q) {
+        sval[lane * (2 * R) + q] = on ? __ldg(b.val + static_cast<long long>(u) * 2 * R + q) : T(0);
+      }
+    }
+    __syncwarp();
+    const bool act = sl < S;
+    for (int t = 0; t < cnt; t += E) {  // E union entries' gathers in flight
+      T g[E][2][V];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const long long o = static_cast<long long>(sidx[t + e]) * S + sl;
+        if (act) {
+          loadv<T, V>(d0 + o, g[e][0]);
+          loadv<T, V>(d1 + o, g[e][1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) g[e][0][v] = g[e][1][v] = T(0);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const T* vv = sval + (t + e) * (2 * R);
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const T a = vv[sy * R + r];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[r][sy][v] += a * g[e][sy][v];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <class T, int V, int E>
+__global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_fwd_block_kernel(SartK<T> k, BlockK<T> b, int it) {
+  constexpr int R = kBlockR;
+  it = pass_index(k, it, true);
+  if (loop_over(k)) return;
+  extern __shared__ double mred[];  // [kWarps][2*S] then the staging buffers
+  __shared__ int sidx_all[kWarps][kBlockStage];
+  __shared__ T sval_all[kWarps][kBlockStage * 2 * R];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int S = k.nrhs;
+  const int Q = (S + 32 * V - 1) / (32 * V);
+  const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+  const int nsr = 2 * S;
+  for (int t = threadIdx.x; t < kWarps * nsr; t += kThreads) mred[t] = 0.0;
+  __syncthreads();
+  const long long rows = k.rows0;
+  for (int q = 0; q < Q; ++q) {
+    const int sl = (q * 32 + lane) * V;
+    bool on[2][V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      on[0][v] = sl + v < S && sys_on(k.state, sl + v);
+      on[1][v] = sl + v < S && sys_on(k.state, S + sl + v);
+    }
+    double r2[2][V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) r2[0][v] = r2[1][v] = 0.0;
+    for (long long blk = gw; blk < b.nblk; blk += nw) {
+      T acc[R][2][V];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][sy][v] = T(0);
+      block_dot<T, V, E>(b, k.s[0].x, k.s[1].x, __ldg(b.ptr + blk), __ldg(b.ptr + blk + 1), lane, S,
+                      sl, sidx_all[warp], sval_all[warp], acc);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long i = blk * R + r;
+        if (i >= rows) break;
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy) {
+          const SysK<T>& Sy = k.s[sy];
+          const T ri = Sy.rinv[i];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (!on[sy][v]) continue;
+            const long long o = i * S + sl + v;
+            const T rr = Sy.p[o] - acc[r][sy][v];
+            Sy.w[o] = ri * rr;
+            r2[sy][v] += static_cast<double>(rr) * static_cast<double>(rr);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (sl + v < S) {
+        mred[warp * nsr + sl + v] = r2[0][v];
+        mred[warp * nsr + S + sl + v] = r2[1][v];
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nsr; t += kThreads) {
+    double a = 0.0;
+    for (int q = 0; q < kWarps; ++q) a += mred[q * nsr + t];
+    k.partial[static_cast<long long>(t) * gridDim.x + blockIdx.x] = a;
+  }
+  if (last_block(k.ticket)) {
+    finish_norms(k.partial, gridDim.x, nsr, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    loop_next(k, it);
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
+template <class T, int V, int E>
+__global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_back_block_kernel(SartK<T> k, BlockK<T> b, int it) {
+  constexpr int R = kBlockR;
+  it = pass_index(k, it, false);
+  if (loop_over(k)) return;
+  __shared__ int sidx_all[kWarps][kBlockStage];
+  __shared__ T sval_all[kWarps][kBlockStage * 2 * R];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int S = k.nrhs;
+  const int Q = (S + 32 * V - 1) / (32 * V);
+  const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+  const long long cols = k.cols0;
+  for (int q = 0; q < Q; ++q) {
+    const int sl = (q * 32 + lane) * V;
+    bool on[2][V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      on[0][v] = sl + v < S && sys_on(k.state, sl + v);
+      on[1][v] = sl + v < S && sys_on(k.state, S + sl + v);
+    }
+    for (long long blk = gw; blk < b.nblk; blk += nw) {
+      T acc[R][2][V];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][sy][v] = T(0);
+      block_dot<T, V, E>(b, k.s[0].w, k.s[1].w, __ldg(b.ptr + blk), __ldg(b.ptr + blk + 1), lane, S,
+                      sl, sidx_all[warp], sval_all[warp], acc);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long j = blk * R + r;
+        if (j >= cols) break;
+#pragma unroll
+        for (int sy = 0; sy < 2; ++sy) {
+          const SysK<T>& Sy = k.s[sy];
+          const T ci = Sy.cinv[j];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (!on[sy][v]) continue;
+            const long long o = j * S + sl + v;
+            const T xn = upd(Sy.x[o], k.relax, acc[r][sy][v], ci);
+            Sy.x[o] = xn;
+            if (!isfinite(static_cast<double>(xn))) {
+              atomicCAS(&k.state[4 * (sy * S + sl + v) + 2], 0, it + 1);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ sharded update
 // After the all-reduce of [A_g^T w_g | ||r_g||^2] every rank applies the same
 // update (SURVEY §8e level 3) with the reference's check-before-update order.
@@ -2760,7 +2979,44 @@ void launch_multi_fwd(Plan& P, const SartK<T>& k, int it) {
 }
 
 template <class T>
+BlockK<T> block_args(const Plan& P, bool fwd) {
+  BlockK<T> b{};
+  b.ptr = fwd ? P.bptr_f.get() : P.bptr_b.get();
+  b.idx = fwd ? P.bidx_f.get() : P.bidx_b.get();
+  b.val = reinterpret_cast<const T*>(fwd ? P.bval_f.get() : P.bval_b.get());
+  b.nblk = fwd ? P.nblk_f : P.nblk_b;
+  return b;
+}
+
+template <class T>
+using BlockFn = void (*)(SartK<T>, BlockK<T>, int);
+
+template <class T>
+BlockFn<T> block_kernel(const Plan& P, bool fwd) {
+  const int S = P.nrhs;
+  const int v = S % 4 == 0 && S >= 128 ? 4 : (S % 2 == 0 && S >= 64 ? 2 : 1);
+  const int e = fwd ? P.block_e_f : P.block_e_b;
+#define SSB_BLK(V, E) \
+  if (v == V && e == E) return fwd ? sart_fwd_block_kernel<T, V, E> : sart_back_block_kernel<T, V, E>;
+  SSB_BLK(4, 2) SSB_BLK(4, 4) SSB_BLK(2, 2) SSB_BLK(2, 4) SSB_BLK(1, 2) SSB_BLK(1, 4)
+#undef SSB_BLK
+  fail("plan: unsupported block-merged kernel shape");
+  return nullptr;
+}
+
+template <class T>
+void launch_block(Plan& P, const SartK<T>& k, int it, bool fwd) {
+  const std::size_t sh = fwd ? sizeof(double) * kWarps * 2 * P.nrhs : 0;
+  block_kernel<T>(P, fwd)<<<fwd ? P.fwd_blocks : P.back_blocks, kThreads, sh, P.ctx->stream>>>(
+      k, block_args<T>(P, fwd), it);
+}
+
+template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
+  if (P.blocked_f) {
+    launch_block<T>(P, k, it, true);
+    return;
+  }
   if (P.paired) {
     launch_pair<T>(P, k, it, true);
     return;
@@ -2783,6 +3039,10 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
 
 template <class T>
 void launch_back(Plan& P, const SartK<T>& k, int it) {
+  if (P.blocked_b) {
+    launch_block<T>(P, k, it, false);
+    return;
+  }
   if (P.paired) {
     launch_pair<T>(P, k, it, false);
     return;
@@ -3557,6 +3817,13 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
       k = nb * ((c16b ? 2 : 4) + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
           (nexc_b ? nexc_b * (4 + 2 * b) + 4 * (cols[0] + 1) : 0);
     }
+  } else if (blocked_f || blocked_b) {  // union indices + 2R values per entry + pointers
+    for (int s2 = 0; s2 < nsys; ++s2) {
+      f += a[s2]->nnz * (4 + b) + 4 * (rows[s2] + 1);
+      k += a[s2]->nnz * (4 + b) + 4 * (cols[s2] + 1);
+    }
+    if (blocked_f) f = nu_f * (4 + 2 * kBlockR * b) + 4 * (nblk_f + 1);
+    if (blocked_b) k = nu_b * (4 + 2 * kBlockR * b) + 4 * (nblk_b + 1);
   } else if (tiled && nsys == 1 && nrhs == 1) {
     f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
              : tnnz_f * (4 + b) + 4 * (rows[0] + 1);
@@ -3581,8 +3848,9 @@ std::string Plan::describe() const {
     bk = "sart_back_tiled_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + (c16b ? "true" : "false") + ">";
   } else if (sharded || nrhs > 1 || !paired) {
-    fk = nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel";
-    bk = nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel";
+    fk = blocked_f ? "sart_fwd_block_kernel" : (nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel");
+    bk = blocked_b ? "sart_back_block_kernel"
+                   : (nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel");
   } else {
     fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
          std::to_string(uf_fwd) + ", " + std::to_string(layout_mode(true)) + ">";
@@ -3892,6 +4160,102 @@ void build_single(Plan& P) {
 }
 }  // namespace
 
+// Block-merged multi-RHS streams of one direction (see sart_fwd_block_kernel):
+// vectors of both folded systems in blocks of kBlockR, each block's sorted
+// union of indices with its 2*kBlockR values per index (zero where absent).
+template <class T>
+void build_blocks_dir(Plan& P, bool fwd) {
+  constexpr int R = kBlockR;
+  const std::int64_t n = fwd ? P.rows[0] : P.cols[0];
+  std::vector<int> ptr[2], idx[2];
+  std::vector<double> val[2];
+  for (int s = 0; s < 2; ++s) {
+    Matrix* a = P.a[s];
+    a->ensure_csc();
+    const std::int64_t nnz = a->nnz;
+    ptr[s].resize(n + 1);
+    idx[s].resize(nnz);
+    val[s].resize(nnz);
+    P.ctx->copy(ptr[s].data(), fwd ? a->rowptr.get() : a->colptr.get(), (n + 1) * sizeof(int));
+    P.ctx->copy(idx[s].data(), fwd ? a->colidx.get() : a->rowidx.get(), nnz * sizeof(int));
+    P.ctx->copy(val[s].data(), fwd ? a->val.get() : a->cval.get(), nnz * sizeof(double));
+  }
+  const std::int64_t nblk = (n + R - 1) / R;
+  std::vector<int> bptr(nblk + 1, 0), bidx;
+  std::vector<T> bval;
+  std::vector<int> uni;
+  for (std::int64_t b = 0; b < nblk; ++b) {
+    uni.clear();
+    for (int s = 0; s < 2; ++s) {
+      for (int r = 0; r < R && b * R + r < n; ++r) {
+        const std::int64_t v = b * R + r;
+        uni.insert(uni.end(), idx[s].begin() + ptr[s][v], idx[s].begin() + ptr[s][v + 1]);
+      }
+    }
+    std::sort(uni.begin(), uni.end());
+    uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+    const std::size_t base = bidx.size();
+    bidx.insert(bidx.end(), uni.begin(), uni.end());
+    bval.resize(bidx.size() * 2 * R, T(0));
+    for (int s = 0; s < 2; ++s) {
+      for (int r = 0; r < R && b * R + r < n; ++r) {
+        const std::int64_t v = b * R + r;
+        std::size_t u = 0;  // both lists ascending: one merge walk
+        for (int q = ptr[s][v]; q < ptr[s][v + 1]; ++q) {
+          while (uni[u] != idx[s][q]) ++u;
+          bval[(base + u) * 2 * R + s * R + r] = static_cast<T>(val[s][q]);
+        }
+      }
+    }
+    if (bidx.size() >= (std::size_t{1} << 31)) fail("plan: block-merged stream exceeds int32");
+    bptr[b + 1] = static_cast<int>(bidx.size());
+  }
+  DBuf<int>& dp = fwd ? P.bptr_f : P.bptr_b;
+  DBuf<int>& di = fwd ? P.bidx_f : P.bidx_b;
+  DBuf<char>& dv = fwd ? P.bval_f : P.bval_b;
+  dp.alloc(nblk + 1);
+  di.alloc(bidx.size());
+  dv.alloc(bval.size() * sizeof(T));
+  SSB_CUDA(cudaMemcpyAsync(dp.get(), bptr.data(), bptr.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, P.ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(di.get(), bidx.data(), bidx.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, P.ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(dv.get(), bval.data(), bval.size() * sizeof(T),
+                           cudaMemcpyHostToDevice, P.ctx->stream));
+  P.ctx->sync();
+  (fwd ? P.nblk_f : P.nblk_b) = nblk;
+  (fwd ? P.nu_f : P.nu_b) = static_cast<std::int64_t>(bidx.size());
+}
+
+// multi-RHS plans over the folded pair use the block-merged kernels
+// (SSB_BLOCKED=0: the per-vector multi kernels)
+template <class T>
+void build_blocks(Plan& P) {
+  if (P.nrhs < 2 || P.nsys != 2 || P.nband > 1) return;
+  // measured on config 4 (profiles/r02_notes.md): the merged blocks win for
+  // K2 (0.61 -> 0.43 ms), the per-vector kernel stays faster for K1
+  const int all = env_int("SSB_BLOCKED", -1);
+  P.blocked_f = all >= 0 ? all != 0 : env_int("SSB_BLOCKED_FWD", 0) != 0;
+  P.blocked_b = all >= 0 ? all != 0 : env_int("SSB_BLOCKED_BACK", 1) != 0;
+  P.block_e_f = env_int("SSB_BLOCK_E_FWD", 4) <= 2 ? 2 : 4;
+  P.block_e_b = env_int("SSB_BLOCK_E_BACK", 2) <= 2 ? 2 : 4;
+  for (int f = 0; f < 2; ++f) {
+    const bool fwd = f == 0;
+    if (!(fwd ? P.blocked_f : P.blocked_b)) continue;
+    build_blocks_dir<T>(P, fwd);
+    int per_sm = 0;
+    const std::size_t sh = fwd ? sizeof(double) * kWarps * 2 * P.nrhs : 0;
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_kernel<T>(P, fwd),
+                                                           kThreads, sh));
+    const long long warps = fwd ? P.nblk_f : P.nblk_b;
+    (fwd ? P.fwd_blocks : P.back_blocks) = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(static_cast<long long>(std::max(1, per_sm)) * P.ctx->sm_count,
+                               (warps + kWarps - 1) / kWarps)));
+  }
+  const std::size_t need = static_cast<std::size_t>(P.fwd_blocks) * 2 * P.nrhs;
+  if (need > P.partial.size()) P.partial.alloc(need);
+}
+
 // Persistent loop of a paired plan (see sart_persistent_pair_kernel): the
 // grid is every co-resident CTA the work can use; the barrier words are
 // zeroed once (the barrier leaves its count at 0).
@@ -4050,6 +4414,8 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     P->empty_rows[s] = !(mx > 0.0);
   }
   tr.mark("normalisers");
+  if (o.dtype == SS_F32) build_blocks<float>(*P);
+  else build_blocks<double>(*P);
   if (P->paired) {
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);
