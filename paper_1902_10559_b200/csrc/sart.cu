@@ -4270,8 +4270,6 @@ void setup_persistent(Plan& P) {
                                              static_cast<long long>(P.cols[0]) * P.vs_back);
   P.pgrid = static_cast<int>(std::max<long long>(1, std::min<long long>(
       static_cast<long long>(per_sm) * P.ctx->sm_count, (need + kThreads - 1) / kThreads)));
-  const int cap = env_int("SSB_PGRID", 0);
-  if (cap > 0) P.pgrid = std::min(P.pgrid, cap);
   P.gbar.alloc(2);
   SSB_CUDA(cudaMemsetAsync(P.gbar.get(), 0, 2 * sizeof(unsigned), P.ctx->stream));
   if (static_cast<std::size_t>(P.pgrid) * 2 > P.partial.size()) P.partial.alloc(2 * P.pgrid);
