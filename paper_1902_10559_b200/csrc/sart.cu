@@ -238,6 +238,28 @@ __device__ __forceinline__ bool sys_on(const int* state, int idx) {
 __device__ void finish_norms(double* partial, int nblk, int nsr, const double* pnorm, double tol,
                              double* history, int hstride, int* state, int it) {
   __shared__ double sh[kThreads];  // every caller runs kThreads-thread CTAs
+  if (nsr <= kWarps) {
+    // one warp per system (single-RHS plans), all in parallel and without
+    // block barriers -- this runs on the critical path between K1 and K2:
+    // lane l sums partials l, l+32, ... in order, then a fixed xor tree
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (q < nsr && sys_on(state, q)) {
+      double s = 0.0;
+      for (int b = lane; b < nblk; b += 32) s += partial[q * nblk + b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        const double res = sqrt(s);
+        history[q * hstride + it] = res;
+        if (res <= tol * pnorm[q]) {
+          state[4 * q + 0] = 1;
+          state[4 * q + 1] = it;
+        }
+      }
+    }
+    __syncthreads();
+    return;
+  }
   for (int q = 0; q < nsr; ++q) {
     if (!sys_on(state, q)) continue;
     double s = 0.0;
