@@ -98,6 +98,11 @@ struct Plan {
   // solve, grid barriers between the K1 and K2 phases
   bool persistent = false;
   int pgrid = 0;
+  // cluster-persistent loop (sart_cluster_pair_kernel): the grid is one
+  // thread-block cluster of ccluster CTAs, hardware cluster barriers
+  bool cluster = false;
+  int ccluster = 0;
+  int csmem = 0;  // its dynamic shared memory per CTA (staged streams)
   DBuf<unsigned> gbar;  // {arrivals, generation}
   DBuf<int> tptr_f, tptr_b, tidx_f, tidx_b;
   std::int64_t tnnz_f = 0, tnnz_b = 0;

@@ -117,9 +117,20 @@ __device__ __forceinline__ int pass_index(const SartK<T>& k, int it, bool fwd) {
   return fwd ? c : c - 1;
 }
 
+// iter[1]: 0 while the loop runs; 1 once K1's last block ended it (the K2 of
+// that same pass still runs: it applies the final update of every system still
+// on -- sart_solve updates x on every one of its max_iters iterations); 2 once
+// a later K1 of the unrolled body found the loop over, so the K2 after it
+// returns too.
 template <class T>
-__device__ __forceinline__ bool loop_over(const SartK<T>& k) {
-  return k.iter && *(volatile const int*)(k.iter + 1) != 0;
+__device__ __forceinline__ bool loop_over(const SartK<T>& k, bool fwd) {
+  if (!k.iter) return false;
+  const int o = *(volatile const int*)(k.iter + 1);
+  if (fwd) {
+    if (o != 0 && blockIdx.x == 0 && threadIdx.x == 0) k.iter[1] = 2;
+    return o != 0;
+  }
+  return o == 2;
 }
 
 // last block of K1 in WHILE-loop mode: advance the pass counter and run
@@ -371,7 +382,7 @@ __device__ __forceinline__ void back_cols(const SartK<T>& k, long long group, lo
 template <class T, int VS, int UF>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, true);
-  if (loop_over(k)) return;
+  if (loop_over(k, true)) return;
   __shared__ double red[2][kWarps];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_kernel(Sa
 template <class T, int VS, int UF>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, false);
-  if (loop_over(k)) return;
+  if (loop_over(k, false)) return;
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
   const int split = k.sys_blocks[1];
@@ -800,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_pair_kern
   }
   cudaGridDependencySynchronize();
   it = pass_index(k, it, true);
-  if (loop_over(k)) return;
+  if (loop_over(k, true)) return;
   const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
   double r2a = 0.0, r2b = 0.0;
   if (on0 || on1) {
@@ -876,7 +887,7 @@ template <class T, int VS, int UF, int TL>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_kernel(SartK<T> k, int it) {
   cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, false);
-  if (loop_over(k)) return;
+  if (loop_over(k, false)) return;
   using T2 = typename Vec2<T>::type;
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -1108,6 +1119,451 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ------------------------------------------------------------ cluster-persistent paired loop
+// The smallest folded pairs (config 1: 640 x 2048 per system, ~1 MB of paired
+// streams) are bound by per-pass latency, not bytes: the grid-persistent
+// kernel re-reads its stream from L2 every pass and synchronises through a
+// global atomic barrier (~10 us per pass). Here the whole grid is ONE
+// thread-block cluster (16 CTAs of 512 threads where the device allows it,
+// else 8), and nothing crosses the cluster through global memory inside the
+// loop:
+//  * each CTA owns an even share of the rows (K1) and of the columns (K2) --
+//    one vector per lane group -- and copies its share of the mirror-coded
+//    streams (offsets, values, tile headers, exception lists, bounds, per-row
+//    {p, rinv}, per-column cinv) into shared memory once per solve;
+//  * every CTA keeps full replicas of x and w in shared memory: K1 gathers x
+//    and K2 gathers w from shared memory only;
+//  * each new w row / x column and each CTA's ||r||^2 pair is pushed into every
+//    CTA's replica with st.async, whose bytes complete on the receiver's
+//    mbarrier (expected bytes per pass: all rows + one pair per CTA / all
+//    columns). A pass waits on its own mbarrier only: no cluster-wide barrier,
+//    no release fence on the producer side, no L1 invalidation (measured on
+//    B200: a barrier.cluster after global stores costs ~1,700 cycles,
+//    tools/cluster_probe.cu);
+//  * every CTA sums the ||r||^2 pairs in rank order and takes the same stop
+//    decision (solvers.cpp:180-182); CTA 0 records the history and the stop in
+//    global state; a CTA that saw a non-finite update sends -1 as its partial,
+//    which turns that system off everywhere (its iteration is recorded in the
+//    state word as in the other kernels).
+// Ordering: a CTA sends pass i+1's w only after receiving every column of pass
+// i, which each CTA sends after its own reads of w -- so replicas are never
+// overwritten while read (and symmetrically for x). Row and column dot
+// products keep the pair kernels' tile order: bitwise the same iterates as the
+// two-launch loop for the same lane-group widths. Config 1 fp64: 96K -> 178K
+// it/s.
+constexpr int kClusterThreads = 512;
+constexpr int kMaxCluster = 16;
+constexpr int kClusterSmemMax = 200 * 1024;  // staged streams per CTA (dynamic smem)
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// block of CTA b: vectors [b*per, min((b+1)*per, n)) and the stream ranges
+// they cover (entries, tiles, exceptions)
+struct CBlock {
+  int v0, v1, e0, e1, t0, t1, x0, x1;
+};
+
+__device__ __forceinline__ CBlock cblock(const int* tp, const int* tfst, const int* ep, int n,
+                                         int per, int b) {
+  CBlock c;
+  c.v0 = min(b * per, n);
+  c.v1 = min(c.v0 + per, n);
+  c.e0 = tp[c.v0];
+  c.e1 = tp[c.v1];
+  c.t0 = tfst[c.v0];
+  c.t1 = tfst[c.v1];
+  c.x0 = ep ? ep[c.v0] : 0;
+  c.x1 = ep ? ep[c.v1] : 0;
+  return c;
+}
+
+// byte sizes of a block's staged arrays (16-byte aligned sections)
+template <class T>
+__host__ __device__ __forceinline__ long long cstage_bytes(const CBlock& c, int hw, int per_vec) {
+  const auto al = [](long long x) { return (x + 15) & ~15ll; };
+  const long long nv = c.v1 - c.v0, ne = c.e1 - c.e0, nt = c.t1 - c.t0, nx = c.x1 - c.x0;
+  return al(ne * sizeof(T)) + al(nx * 2 * sizeof(T)) + al(nv * per_vec * sizeof(T)) +
+         al(nt * hw * 4ll) + 3 * al((nv + 1) * 4) + al(nx * 4) + al(ne * 2);
+}
+
+// staged arrays of one direction in shared memory (indices relative to the block)
+template <class T>
+struct CStage {
+  const T* val;
+  const T* exv;
+  const T* pv;  // per-vector operands: {p1, p2, rinv1, rinv2} (K1) / {cinv1, cinv2} (K2)
+  const unsigned* hdr;
+  const int* tp;
+  const int* tf;
+  const int* ep;
+  const int* exi;
+  const unsigned short* off;
+};
+
+template <class V>
+__device__ __forceinline__ void ccopy(V* dst, const V* src, long long n) {
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// copy one block's stream share into shared memory at `base`; returns the bytes used
+template <class T>
+__device__ long long cstage_load(char* base, const CBlock& c, int hw, int per_vec,
+                                 const unsigned short* off, const T* val, const unsigned* hdr,
+                                 const int* tp, const int* tfst, const int* ep, const int* exi,
+                                 const T* exv, const T* pv, CStage<T>& st) {
+  const auto al = [](long long x) { return (x + 15) & ~15ll; };
+  const long long nv = c.v1 - c.v0, ne = c.e1 - c.e0, nt = c.t1 - c.t0, nx = c.x1 - c.x0;
+  char* p = base;
+  T* sval = reinterpret_cast<T*>(p);
+  p += al(ne * sizeof(T));
+  T* sexv = reinterpret_cast<T*>(p);
+  p += al(nx * 2 * sizeof(T));
+  T* spv = reinterpret_cast<T*>(p);
+  p += al(nv * per_vec * sizeof(T));
+  unsigned* shdr = reinterpret_cast<unsigned*>(p);
+  p += al(nt * hw * 4ll);
+  int* stp = reinterpret_cast<int*>(p);
+  p += al((nv + 1) * 4);
+  int* stf = reinterpret_cast<int*>(p);
+  p += al((nv + 1) * 4);
+  int* sep = reinterpret_cast<int*>(p);
+  p += al((nv + 1) * 4);
+  int* sexi = reinterpret_cast<int*>(p);
+  p += al(nx * 4);
+  unsigned short* soff = reinterpret_cast<unsigned short*>(p);
+  p += al(ne * 2);
+  // values: whole quads (entries start on multiples of 4)
+  if constexpr (sizeof(T) == 4) {
+    ccopy(reinterpret_cast<float4*>(sval), reinterpret_cast<const float4*>(val + c.e0), ne / 4);
+  } else {
+    ccopy(reinterpret_cast<double2*>(sval), reinterpret_cast<const double2*>(val + c.e0), ne / 2);
+  }
+  ccopy(reinterpret_cast<uint2*>(soff), reinterpret_cast<const uint2*>(off + c.e0), ne / 4);
+  ccopy(reinterpret_cast<uint2*>(shdr), reinterpret_cast<const uint2*>(hdr + 1ll * c.t0 * hw),
+        nt * hw / 2);
+  ccopy(sexv, exv + 2ll * c.x0, 2 * nx);
+  ccopy(sexi, exi + c.x0, nx);
+  ccopy(spv, pv + 1ll * per_vec * c.v0, nv * per_vec);
+  for (long long i = threadIdx.x; i <= nv; i += blockDim.x) {
+    stp[i] = tp[c.v0 + i] - c.e0;
+    stf[i] = tfst[c.v0 + i] - c.t0;
+    sep[i] = ep ? ep[c.v0 + i] - c.x0 : 0;
+  }
+  st.val = sval;
+  st.exv = sexv;
+  st.pv = spv;
+  st.hdr = shdr;
+  st.tp = stp;
+  st.tf = stf;
+  st.ep = sep;
+  st.exi = sexi;
+  st.off = soff;
+  return p - base;
+}
+
+// seg_dot2m over a staged (shared-memory) stream; x / w gathered from global
+// with plain loads (rewritten by other CTAs between passes)
+template <class T, int VS, int UF>
+__device__ __forceinline__ void seg_dot2m_s(const CStage<T>& st, int tf,
+                                            const typename Vec2<T>::type* xv, int beg, int end,
+                                            int eb, int ee, int lane, unsigned mask, T& acc_a,
+                                            T& acc_b) {
+  using T2 = typename Vec2<T>::type;
+  T sa = T(0), sb = T(0);
+  const int nvec = (end - beg) >> 2;
+  const auto hdr = [&](int t, int& base, unsigned& nib) {
+    if constexpr (VS <= 8) {
+      const uint2 w = reinterpret_cast<const uint2*>(st.hdr)[t];
+      base = static_cast<int>(w.x);
+      nib = w.y >> (4 * lane);
+    } else if constexpr (VS == 16) {
+      const uint4 w = reinterpret_cast<const uint4*>(st.hdr)[t];
+      base = static_cast<int>(w.x);
+      nib = (lane < 8 ? w.y : w.z) >> (4 * (lane & 7));
+    } else {
+      base = static_cast<int>(st.hdr[8 * t]);
+      nib = st.hdr[8 * t + 1 + (lane >> 3)] >> (4 * (lane & 7));
+    }
+  };
+  const auto vals = [&](int k0, T (&v)[4]) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 t = *reinterpret_cast<const float4*>(st.val + k0);
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+      const double2 a = *reinterpret_cast<const double2*>(st.val + k0);
+      const double2 b = *(reinterpret_cast<const double2*>(st.val + k0) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+  };
+  int q = lane;
+  for (; q + (UF - 1) * VS < nvec; q += UF * VS) {
+    int4 c[UF];
+    unsigned s[UF];
+    T v[UF][4];
+    const int t0 = tf + (q - lane) / VS;
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int k0 = beg + ((q + u * VS) << 2);
+      int b;
+      hdr(t0 + u, b, s[u]);
+      c[u] = decode16(*reinterpret_cast<const uint2*>(st.off + k0), b);
+      vals(k0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const T2 g0 = xv[c[u].x], g1 = xv[c[u].y], g2 = xv[c[u].z], g3 = xv[c[u].w];
+      sa += flip(v[u][0], s[u], 0) * g0.x + flip(v[u][1], s[u], 1) * g1.x +
+            flip(v[u][2], s[u], 2) * g2.x + flip(v[u][3], s[u], 3) * g3.x;
+      sb += v[u][0] * g0.y + v[u][1] * g1.y + v[u][2] * g2.y + v[u][3] * g3.y;
+    }
+  }
+  for (; q < nvec; q += VS) {
+    const int k0 = beg + (q << 2);
+    int b;
+    unsigned s;
+    hdr(tf + (q - lane) / VS, b, s);
+    const int4 c = decode16(*reinterpret_cast<const uint2*>(st.off + k0), b);
+    T v[4];
+    vals(k0, v);
+    const T2 g0 = xv[c.x], g1 = xv[c.y], g2 = xv[c.z], g3 = xv[c.w];
+    sa += flip(v[0], s, 0) * g0.x + flip(v[1], s, 1) * g1.x + flip(v[2], s, 2) * g2.x +
+          flip(v[3], s, 3) * g3.x;
+    sb += v[0] * g0.y + v[1] * g1.y + v[2] * g2.y + v[3] * g3.y;
+  }
+  for (int e = eb + lane; e < ee; e += VS) {  // exception buckets (rare)
+    const int c = st.exi[e];
+    const T2 a = reinterpret_cast<const T2*>(st.exv)[e];
+    const T2 g = xv[c];
+    sa += a.x * g.x;
+    sb += a.y * g.y;
+  }
+#pragma unroll
+  for (int off2 = VS / 2; off2 > 0; off2 >>= 1) {
+    sa += __shfl_xor_sync(mask, sa, off2, VS);
+    sb += __shfl_xor_sync(mask, sb, off2, VS);
+  }
+  acc_a = sa;
+  acc_b = sb;
+}
+
+// copy n interleaved pairs global -> shared (one round of L2 latency: every
+// thread's loads are in flight together)
+template <class T2>
+__device__ __forceinline__ void crefresh(T2* dst, const T2* src, int n, int t = threadIdx.x,
+                                         int nt = kClusterThreads) {
+  for (int i = t; i < n; i += nt) dst[i] = __ldcg(src + i);  // L2 only: nothing left in L1
+}
+
+// sum of v over the 32 lanes of a warp in a fixed butterfly order
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- point-to-point exchange inside the cluster: st.async into the peer's
+// shared memory, completion counted in bytes on the peer's mbarrier (no
+// cluster-wide barrier, no release fence on the producer, no L1 invalidation
+// on the consumer)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cl_map(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(unsigned mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+               : "memory");
+}
+// wait for the phase of parity `par` (bounded: a lost peer traps, ~2 s)
+__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned par) {
+  unsigned done = 0;
+  const long long t0 = clock64();
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb), "r"(par)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > kBarrierSpinCycles) __trap();
+  }
+}
+__device__ __forceinline__ void st_async(unsigned ra, double2 v, unsigned rmb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(ra), "d"(v.x), "d"(v.y), "r"(rmb) : "memory");
+}
+__device__ __forceinline__ void st_async(unsigned ra, float2 v, unsigned rmb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+               ::"r"(ra), "f"(v.x), "f"(v.y), "r"(rmb) : "memory");
+}
+
+template <class T, int VSF, int VSB, int UF>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    sart_cluster_pair_kernel(SartK<T> k, int first, int count) {
+  using T2 = typename Vec2<T>::type;
+  constexpr int NW = kClusterThreads / 32;
+  constexpr int HWF = VSF <= 8 ? 2 : (VSF == 16 ? 4 : 8);
+  constexpr int HWB = VSB <= 8 ? 2 : (VSB == 16 ? 4 : 8);
+  static_assert(NW <= 32, "one partial per lane of warp 0");
+  extern __shared__ __align__(16) char cl_smem[];
+  __shared__ double red[2][NW];
+  __shared__ __align__(16) double2 part[kMaxCluster];  // {||r1||^2, ||r2||^2} of each CTA
+  __shared__ __align__(8) unsigned long long mbar[2];  // [0]: w + partials, [1]: x
+  __shared__ int ldiv[2];  // this CTA saw a non-finite update of system q
+  __shared__ int go[2];
+  const int nrow = static_cast<int>(k.rows0), ncol = static_cast<int>(k.cols0);
+  const unsigned nct = gridDim.x;
+  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+  // ---- stage this CTA's stream share (once per solve) and the x / w replicas
+  // row / column blocks spread evenly over the cluster (<= one vector per lane group)
+  const CBlock bf = cblock(k.tpf, k.tff, k.epf, nrow, (nrow + nct - 1) / nct, blockIdx.x);
+  const CBlock bb = cblock(k.tpb, k.tfb, k.epb, ncol, (ncol + nct - 1) / nct, blockIdx.x);
+  // replicas first: the same shared-memory offsets in every CTA (st.async targets)
+  T2* sx = reinterpret_cast<T2*>(cl_smem);  // replica of the iterate {x1, x2}
+  T2* sw = sx + ncol;                       // replica of {w1, w2}
+  CStage<T> sf, sb;
+  long long used = (2ll * (ncol + nrow) * sizeof(T) + 15) & ~15ll;
+  used += cstage_load<T>(cl_smem + used, bf, HWF, 4, k.tof, k.rv2, k.thf, k.tpf, k.tff, k.epf,
+                         k.eif, k.evf, k.pe, sf);
+  cstage_load<T>(cl_smem + used, bb, HWB, 2, k.tob, k.cv2, k.thb, k.tpb, k.tfb, k.epb, k.eib,
+                 k.evb, k.cc, sb);
+  crefresh(sx, reinterpret_cast<const T2*>(k.xx), ncol);
+  const unsigned mb_w = smem_u32(&mbar[0]), mb_x = smem_u32(&mbar[1]);
+  const unsigned bytes_w = static_cast<unsigned>(nrow * sizeof(T2) + nct * sizeof(double2));
+  const unsigned bytes_x = static_cast<unsigned>(ncol * sizeof(T2));
+  if (threadIdx.x == 0) {
+    mbar_init(mb_w, 1);
+    mbar_init(mb_x, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 2) ldiv[threadIdx.x] = 0;
+  bool run0 = sys_on(k.state, 0), run1 = sys_on(k.state, 1);
+  const double thr0 = k.tol * k.pnorm[0], thr1 = k.tol * k.pnorm[1];
+  __syncthreads();
+  cluster_barrier();  // every CTA's mbarriers exist before any st.async lands
+  unsigned par = 0;
+  for (int it = first; it < first + count; ++it) {
+    if (!run0 && !run1) break;  // the same decision in every CTA
+    if (threadIdx.x == 0) mbar_expect(mb_w, bytes_w);
+    // ---- K1 phase over this CTA's rows: r = p - A x, w = row_inv r; each
+    // row's w goes to every CTA's replica
+    {
+      const int lane = threadIdx.x & (VSF - 1);
+      const unsigned mask = group_mask<VSF>();
+      const int li = threadIdx.x / VSF;
+      double r2a = 0.0, r2b = 0.0;
+      if (li < bf.v1 - bf.v0) {
+        T da, db;
+        seg_dot2m_s<T, VSF, UF>(sf, sf.tf[li], sx, sf.tp[li], sf.tp[li + 1], sf.ep[li],
+                                sf.ep[li + 1], lane, mask, da, db);
+        if (lane == 0) {
+          const T* e = sf.pv + 4 * li;
+          const T ra = e[0] - da, rb = e[1] - db;
+          T2 wo;
+          wo.x = run0 ? e[2] * ra : T(0);
+          wo.y = run1 ? e[3] * rb : T(0);
+          const unsigned la = smem_u32(sw + bf.v0 + li);
+          for (unsigned r = 0; r < nct; ++r) st_async(cl_map(la, r), wo, cl_map(mb_w, r));
+          if (run0) r2a = static_cast<double>(ra) * static_cast<double>(ra);
+          if (run1) r2b = static_cast<double>(rb) * static_cast<double>(rb);
+        }
+      }
+      r2a = warp_sum(r2a);
+      r2b = warp_sum(r2b);
+      if (wl == 0) {
+        red[0][warp] = r2a;
+        red[1][warp] = r2b;
+      }
+      __syncthreads();
+      if (warp == 0) {  // this CTA's partial pair -> every CTA (-1: it saw a divergence)
+        double2 t;
+        t.x = warp_sum(wl < NW ? red[0][wl] : 0.0);
+        t.y = warp_sum(wl < NW ? red[1][wl] : 0.0);
+        if (ldiv[0]) t.x = -1.0;
+        if (ldiv[1]) t.y = -1.0;
+        if (wl < static_cast<int>(nct)) {
+          st_async(cl_map(smem_u32(&part[blockIdx.x]), wl), t, cl_map(mb_w, wl));
+        }
+      }
+    }
+    mbar_wait(mb_w, par);
+    // ---- ||r|| and the stop test (warp q: system q), the same in every CTA
+    if (warp < 2) {
+      const bool on = warp ? run1 : run0;
+      const double v = wl < static_cast<int>(nct) ? (warp ? part[wl].y : part[wl].x) : 0.0;
+      const bool div = __any_sync(0xffffffffu, v < 0.0);
+      const double t = warp_sum(v);
+      if (wl == 0) {
+        int gq = 0;
+        if (on && !div) {
+          const double res = sqrt(t);
+          const bool stop = res <= (warp ? thr1 : thr0);
+          gq = stop ? 0 : 1;
+          if (blockIdx.x == 0) {
+            k.history[warp * k.hstride + it] = res;
+            if (stop) {
+              k.state[4 * warp + 0] = 1;
+              k.state[4 * warp + 1] = it;
+            }
+          }
+        }
+        go[warp] = gq;
+      }
+    } else if (threadIdx.x == 64) {
+      mbar_expect(mb_x, bytes_x);
+    }
+    __syncthreads();
+    run0 = go[0] != 0;
+    run1 = go[1] != 0;
+    if (!run0 && !run1) break;  // both stopped (CTA 0 recorded it)
+    // ---- K2 phase over this CTA's columns: x += lambda col_inv (A^T w); each
+    // column's x goes to every CTA's replica and to global memory
+    {
+      const int lane = threadIdx.x & (VSB - 1);
+      const unsigned mask = group_mask<VSB>();
+      const int li = threadIdx.x / VSB;
+      if (li < bb.v1 - bb.v0) {
+        const int g = bb.v0 + li;
+        T ua, ub;
+        seg_dot2m_s<T, VSB, UF>(sb, sb.tf[li], sw, sb.tp[li], sb.tp[li + 1], sb.ep[li],
+                                sb.ep[li + 1], lane, mask, ua, ub);
+        if (lane == 0) {
+          T2 xo = sx[g];
+          const T* ci = sb.pv + 2 * li;
+          if (run0) xo.x = upd(xo.x, k.relax, ua, ci[0]);
+          if (run1) xo.y = upd(xo.y, k.relax, ub, ci[1]);
+          reinterpret_cast<T2*>(k.xx)[g] = xo;
+          if (run0 && !isfinite(static_cast<double>(xo.x))) {
+            atomicCAS(&k.state[2], 0, it + 1);
+            ldiv[0] = 1;
+          }
+          if (run1 && !isfinite(static_cast<double>(xo.y))) {
+            atomicCAS(&k.state[4 + 2], 0, it + 1);
+            ldiv[1] = 1;
+          }
+          const unsigned la = smem_u32(sx + g);
+          for (unsigned r = 0; r < nct; ++r) st_async(cl_map(la, r), xo, cl_map(mb_x, r));
+        }
+      }
+    }
+    mbar_wait(mb_x, par);
+    par ^= 1u;
+    __syncthreads();  // ldiv of this pass visible to warp 0 of the next
+  }
+}
+
 // ------------------------------------------------------------ single-system tiled kernels
 // One system (sart_solve, the per-rank system of a 2-GPU run, a row shard) on
 // the same tiled stream layout as the folded pair: quads padded, entries
@@ -1160,7 +1616,7 @@ template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_kernel(SartK<T> k, int it) {
   cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, true);
-  if (loop_over(k)) return;
+  if (loop_over(k, true)) return;
   __shared__ double red[kWarps];
   const SysK<T>& S = k.s[0];
   const int lane = threadIdx.x & (VS - 1);
@@ -1222,7 +1678,7 @@ template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_tiled_kernel(SartK<T> k, int it) {
   cudaGridDependencySynchronize();  // PDL: launched while the previous pass drains
   it = pass_index(k, it, false);
-  if (loop_over(k)) return;
+  if (loop_over(k, false)) return;
   const SysK<T>& S = k.s[0];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -1594,7 +2050,7 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
   // band: 0 = the whole row in one pass; with column bands 1 = first pass
   // (w <- partial), 2 = middle (w += partial), 3 = last (r from w + partial)
   it = pass_index(k, it, true);
-  if (loop_over(k)) return;
+  if (loop_over(k, true)) return;
   extern __shared__ double mred[];  // [kWarps][nsys*S]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = k.nrhs;
@@ -1696,7 +2152,7 @@ __global__ void __launch_bounds__(kThreads) sart_fwd_multi_kernel(SartK<T> k, in
 template <class T, int V, int Q>
 __global__ void __launch_bounds__(kThreads, Q == 1 ? 4 : 1) sart_back_multi_kernel(SartK<T> k, int it) {
   it = pass_index(k, it, false);
-  if (loop_over(k)) return;
+  if (loop_over(k, false)) return;
   const int lane = threadIdx.x & 31;
   const int S = k.nrhs;
   const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
@@ -1832,7 +2288,7 @@ template <class T, int V, int E>
 __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_fwd_block_kernel(SartK<T> k, BlockK<T> b, int it) {
   constexpr int R = kBlockR;
   it = pass_index(k, it, true);
-  if (loop_over(k)) return;
+  if (loop_over(k, true)) return;
   extern __shared__ double mred[];  // [kWarps][2*S] then the staging buffers
   __shared__ int sidx_all[kWarps][kBlockStage];
   __shared__ T sval_all[kWarps][kBlockStage * 2 * R];
@@ -1910,7 +2366,7 @@ template <class T, int V, int E>
 __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_back_block_kernel(SartK<T> k, BlockK<T> b, int it) {
   constexpr int R = kBlockR;
   it = pass_index(k, it, false);
-  if (loop_over(k)) return;
+  if (loop_over(k, false)) return;
   __shared__ int sidx_all[kWarps][kBlockStage];
   __shared__ T sval_all[kWarps][kBlockStage * 2 * R];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -3303,6 +3759,124 @@ PersistFn<T> persistent_kernel(const Plan& P) {
   return nullptr;
 }
 
+template <class T>
+using ClusterFn = void (*)(SartK<T>, int, int);
+
+// the cluster-persistent kernel of a paired plan's shape, or nullptr
+template <class T>
+ClusterFn<T> cluster_kernel(int vsf, int vsb) {
+#define SSB_CLUSTER(F, B) \
+  if (vsf == F && vsb == B) return sart_cluster_pair_kernel<T, F, B, 2>;
+  SSB_CLUSTER(8, 4) SSB_CLUSTER(8, 8) SSB_CLUSTER(8, 16)
+  SSB_CLUSTER(16, 4) SSB_CLUSTER(16, 8) SSB_CLUSTER(16, 16)
+  SSB_CLUSTER(32, 4) SSB_CLUSTER(32, 8) SSB_CLUSTER(32, 16)
+#undef SSB_CLUSTER
+  return nullptr;
+}
+
+// largest cluster (16, else 8) of 1024-thread CTAs with `smem` bytes of
+// dynamic shared memory this device can co-schedule (0: none)
+template <class T>
+int cluster_size_for(ClusterFn<T> fn, int smem) {
+  if (!fn) return 0;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  for (int c = kMaxCluster; c >= 8; c /= 2) {
+    if (c > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                     cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n >= 1) return c;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+template <class T>
+void launch_cluster(Plan& P, const SartK<T>& k, int first, int count) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.ccluster);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = P.csmem;
+  cfg.stream = P.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.ccluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, cluster_kernel<T>(P.vs_fwd, P.vs_back), k, first, count));
+  P.ctx->check_launch("sart_cluster_pair_kernel");
+}
+
+// Cluster-persistent loop of a small paired plan (see sart_cluster_pair_kernel):
+// every CTA's staged share must fit kClusterSmemMax and one pass of the
+// cluster must cover every row and column; otherwise the plan keeps ccluster 0.
+template <class T>
+void setup_cluster(Plan& P) {
+  const int c0 = P.ccluster;
+  P.ccluster = 0;
+  ClusterFn<T> fn = cluster_kernel<T>(P.vs_fwd, P.vs_back);
+  if (!fn || c0 <= 0 || !P.mir_f || !P.mir_b || !P.c16f || !P.c16b || P.stream_cs) return;
+  const int nr = static_cast<int>(P.rows[0]), nc = static_cast<int>(P.cols[0]);
+  std::vector<int> tpf(nr + 1), tff(nr + 1), epf(nr + 1, 0), tpb(nc + 1), tfb(nc + 1),
+      epb(nc + 1, 0);
+  P.ctx->copy(tpf.data(), P.tptr_f.get(), (nr + 1) * sizeof(int));
+  P.ctx->copy(tff.data(), P.tfirst_f.get(), (nr + 1) * sizeof(int));
+  P.ctx->copy(tpb.data(), P.tptr_b.get(), (nc + 1) * sizeof(int));
+  P.ctx->copy(tfb.data(), P.tfirst_b.get(), (nc + 1) * sizeof(int));
+  if (P.eptr_f.get()) P.ctx->copy(epf.data(), P.eptr_f.get(), (nr + 1) * sizeof(int));
+  if (P.eptr_b.get()) P.ctx->copy(epb.data(), P.eptr_b.get(), (nc + 1) * sizeof(int));
+  const auto blk = [](const std::vector<int>& tp, const std::vector<int>& tf,
+                      const std::vector<int>& ep, int n, int per, int b) {
+    CBlock c;
+    c.v0 = std::min(b * per, n);
+    c.v1 = std::min(c.v0 + per, n);
+    c.e0 = tp[c.v0];
+    c.e1 = tp[c.v1];
+    c.t0 = tf[c.v0];
+    c.t1 = tf[c.v1];
+    c.x0 = ep[c.v0];
+    c.x1 = ep[c.v1];
+    return c;
+  };
+  for (int c = c0; c >= 8; c /= 2) {
+    const int pf = (nr + c - 1) / c, pb = (nc + c - 1) / c;  // the kernel's blocks
+    if (pf > kClusterThreads / P.vs_fwd || pb > kClusterThreads / P.vs_back) break;
+    long long need = 0;
+    for (int b = 0; b < c; ++b) {
+      need = std::max(need, cstage_bytes<T>(blk(tpf, tff, epf, nr, pf, b), P.hs_f, 4) +
+                                cstage_bytes<T>(blk(tpb, tfb, epb, nc, pb, b), P.hs_b, 2));
+    }
+    need += (2ll * sizeof(T) * (nr + nc) + 15) & ~15ll;  // x / w replicas
+    if (need > kClusterSmemMax) break;
+    const int smem = static_cast<int>(need);
+    if (cluster_size_for<T>(fn, smem) >= c) {
+      P.ccluster = c;
+      P.csmem = smem;
+      if (static_cast<std::size_t>(c) * 2 > P.partial.size()) P.partial.alloc(2 * c);
+      return;
+    }
+  }
+}
+
 // one cooperative launch runs passes [first, first + count) (all CTAs resident)
 template <class T>
 void launch_persistent(Plan& P, const SartK<T>& k, int first, int count) {
@@ -3322,6 +3896,10 @@ void launch_persistent(Plan& P, const SartK<T>& k, int first, int count) {
 template <class T>
 void do_iterations(Plan& P, int first, int count) {
   const SartK<T> k = make_args<T>(P);
+  if (P.cluster) {
+    launch_cluster<T>(P, k, first, count);
+    return;
+  }
   if (P.persistent) {
     launch_persistent<T>(P, k, first, count);
     return;
@@ -3879,10 +4457,13 @@ std::string Plan::describe() const {
     bk = "sart_back_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + std::to_string(layout_mode(false)) + ">";
   }
-  std::string pk = persistent ? "sart_persistent_pair_kernel<" + std::string(t) + ", " +
-                                    std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
-                                    ", 2, 4>"
-                              : "";
+  std::string pk = cluster ? "sart_cluster_pair_kernel<" + std::string(t) + ", " +
+                                 std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
+                                 ", 2>"
+                   : persistent ? "sart_persistent_pair_kernel<" + std::string(t) + ", " +
+                                      std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
+                                      ", 2, 4>"
+                                : "";
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
   char buf[1024];
@@ -3901,7 +4482,7 @@ std::string Plan::describe() const {
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
-                graph ? "true" : "false", pk.c_str(), persistent ? pgrid : 0);
+                graph ? "true" : "false", pk.c_str(), cluster ? ccluster : (persistent ? pgrid : 0));
   return buf;
 }
 
@@ -4371,6 +4952,30 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     }
     P->uf_fwd = env_int("SSB_UF_FWD", P->mir_f && o.dtype == SS_F64 ? 2 : 4);
     P->uf_back = env_int("SSB_UF_BACK", 2);
+    // the smallest pairs (one pass of 8-lane rows / 4-lane columns fits one
+    // 16-CTA cluster: config 1) run the whole loop in one cluster-persistent
+    // kernel; its lane groups are widened to cover every vector in one pass
+    // (SSB_PERSIST: -1 auto, 0 two launches per pass, 1 grid-persistent
+    // kernel, 2 cluster kernel whenever the shape allows)
+    const int want = env_int("SSB_PERSIST", -1);
+    if (P->mir_f && P->c16f && (want == 2 || want == -1)) {
+      const int c = o.dtype == SS_F32
+                        ? cluster_size_for<float>(cluster_kernel<float>(16, 8), kClusterSmemMax)
+                        : cluster_size_for<double>(cluster_kernel<double>(16, 8), kClusterSmemMax);
+      const long long cap = static_cast<long long>(c) * kClusterThreads;
+      if (c > 0 && (want == 2 || (P->rows[0] * 8 <= cap && P->cols[0] * 4 <= cap))) {
+        P->ccluster = c;
+        if (!std::getenv("SSB_VS_FWD")) {
+          P->vs_fwd = 8;
+          while (P->vs_fwd < 32 && P->rows[0] * P->vs_fwd * 2 <= cap) P->vs_fwd *= 2;
+        }
+        if (!std::getenv("SSB_VS_BACK")) {
+          P->vs_back = 4;
+          while (P->vs_back < 16 && P->cols[0] * P->vs_back * 2 <= cap) P->vs_back *= 2;
+        }
+        P->uf_fwd = P->uf_back = 2;
+      }
+    }
   }
   if (!P->paired) {
     P->uf_fwd = env_int("SSB_UF_FWD", 4);
@@ -4463,10 +5068,15 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     }
     // L2-resident pairs (configs 1-2) run the loop as one persistent kernel
     // (SSB_PERSIST=0: the two launches per pass; 1: whenever the shape allows)
-    {
+    if (P->ccluster > 0) {
+      if (o.dtype == SS_F32) setup_cluster<float>(*P);
+      else setup_cluster<double>(*P);
+      P->cluster = P->persistent = P->ccluster > 0;
+    }
+    if (!P->cluster) {
       const int want = env_int("SSB_PERSIST", -1);
       const bool small = static_cast<std::size_t>(fb + bb) * 2 <= ctx->l2_bytes;
-      if (want != 0 && (want == 1 || small)) {
+      if (want != 0 && want != 2 && (want == 1 || small)) {
         if (o.dtype == SS_F32) setup_persistent<float>(*P);
         else setup_persistent<double>(*P);
       }
@@ -4862,6 +5472,8 @@ Plan* make_sharded_pair_plan_local(Context* ctx, Matrix* a1, Matrix* a2, std::in
   P->own = l1.release();
   P->own2 = l2.release();
   P->persistent = false;  // the exchange kernels run the loop
+  P->cluster = false;
+  P->ccluster = 0;
   P->sharded = true;
   P->row_begin = rb;
   P->row_end = re;
