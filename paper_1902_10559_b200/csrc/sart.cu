@@ -248,49 +248,26 @@ __device__ __forceinline__ bool sys_on(const int* state, int idx) {
 // the reference's check-before-update stopping rule (solvers.cpp:180-182).
 __device__ void finish_norms(double* partial, int nblk, int nsr, const double* pnorm, double tol,
                              double* history, int hstride, int* state, int it) {
-  __shared__ double sh[kThreads];  // every caller runs kThreads-thread CTAs
-  if (nsr <= kWarps) {
-    // one warp per system (single-RHS plans), all in parallel and without
-    // block barriers -- this runs on the critical path between K1 and K2:
-    // lane l sums partials l, l+32, ... in order, then a fixed xor tree
-    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (q < nsr && sys_on(state, q)) {
-      double s = 0.0;
-      for (int b = lane; b < nblk; b += 32) s += partial[q * nblk + b];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) {
-        const double res = sqrt(s);
-        history[q * hstride + it] = res;
-        if (res <= tol * pnorm[q]) {
-          state[4 * q + 0] = 1;
-          state[4 * q + 1] = it;
-        }
-      }
-    }
-    __syncthreads();
-    return;
-  }
-  for (int q = 0; q < nsr; ++q) {
+  // one warp per system / slice, all in parallel and without block barriers
+  // (this runs on the critical path between K1 and K2): lane l sums partials
+  // l, l+32, ... in order, then a fixed xor tree
+  const int nw = static_cast<int>(blockDim.x) >> 5, lane = threadIdx.x & 31;
+  for (int q = threadIdx.x >> 5; q < nsr; q += nw) {
     if (!sys_on(state, q)) continue;
     double s = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partial[q * nblk + b];
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      const double res = sqrt(sh[0]);
+    for (int b = lane; b < nblk; b += 32) s += partial[static_cast<long long>(q) * nblk + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const double res = sqrt(s);
       history[q * hstride + it] = res;
       if (res <= tol * pnorm[q]) {
         state[4 * q + 0] = 1;
         state[4 * q + 1] = it;
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 __device__ __forceinline__ bool last_block(unsigned* ticket) {
@@ -2362,6 +2339,273 @@ __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_fwd_block_kerne
   }
 }
 
+// ------------------------------------------------------------ X-staged multi-RHS K1
+// Multi-RHS K1 with the gathered operand staged in shared memory by the bulk-
+// copy (TMA) engine. A CTA owns blocks of kStageR consecutive rows (rays of one
+// source, neighbouring detector bins) of one system. The rows of a block touch
+// a sorted union of columns U (config 4: 3,303 for 16 rows of ~624 entries,
+// reuse 3.0x). A producer warp walks U in chunks of kStageC columns and, per
+// column, issues one bulk copy of X[c][0..S) (S*sizeof(T) contiguous bytes of
+// the [n][S] layout) into a kStageNS-deep shared-memory ring whose slots
+// complete on mbarriers (bytes counted); it runs ahead across block
+// boundaries; consecutive union columns are one contiguous range of X, so a
+// chunk costs one bulk copy per run of columns (~2 per chunk on config 4).
+// Eight consumer warps (two rows each) apply every chunk: each
+// CSR entry carries its 16-bit position in U, so an entry is a shuffle-
+// broadcast (position, value) and one conflict-free shared-memory read of the
+// S-wide X record (V slices per lane). The X record of a column is read from
+// L2 once per block instead of once per row, never through L1; summation per
+// row and slice stays in CSR order (bitwise equal to the per-row multi kernel).
+constexpr int kStageR = 16;     // rows per block (2 per consumer warp)
+constexpr int kStageC = 64;     // union columns per chunk
+constexpr int kStageNS = 3;     // ring depth
+constexpr int kStageThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+
+template <class T>
+struct StageK {
+  const int* bptr;            // [nsys*nblk + 1] union range of each block (system-major)
+  const int* buni;            // union columns
+  const unsigned short* eu0;  // per CSR entry of system 0 / 1: its position in the block's union
+  const unsigned short* eu1;
+  long long nblk;             // blocks per system
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned mb) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+}
+
+template <class T, int V>
+__device__ __forceinline__ void lds_v(const T* p, T (&o)[V]) {
+  if constexpr (sizeof(T) * V == 16) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    const T* q = reinterpret_cast<const T*>(&t);
+#pragma unroll
+    for (int v = 0; v < V; ++v) o[v] = q[v];
+  } else if constexpr (sizeof(T) * V == 32) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *(reinterpret_cast<const float4*>(p) + 1);
+    const T* qa = reinterpret_cast<const T*>(&a);
+    const T* qb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+    for (int v = 0; v < V / 2; ++v) {
+      o[v] = qa[v];
+      o[V / 2 + v] = qb[v];
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) o[v] = p[v];
+  }
+}
+
+// one row's cursor over its CSR entries: a 32-entry window in the lanes'
+// registers (position, value) and the next window prefetched
+template <class T>
+struct RowCur {
+  int e, end, wb;  // next entry, row end, window base (absolute entry index)
+  unsigned wu, nu;
+  T wv, nv;
+};
+
+template <class T>
+__device__ __forceinline__ void cur_load(const unsigned short* eu, const T* val, int base, int end,
+                                         int lane, unsigned& u, T& v) {
+  const int e = base + lane;
+  u = e < end ? static_cast<unsigned>(__ldg(eu + e)) : 0xffffu;
+  v = e < end ? __ldg(val + e) : T(0);
+}
+
+// acc += the row's entries whose union position is below cend (the chunk
+// starting at position cu0, staged at xs); entries are sorted by position
+template <class T, int V>
+__device__ __forceinline__ void stage_row_chunk(RowCur<T>& c, const unsigned short* eu,
+                                                const T* val, unsigned cu0, unsigned cend,
+                                                const T* xs, int lane, T (&acc)[V]) {
+  while (c.e < c.end) {
+    int l = c.e - c.wb;
+    if (l >= 32) {  // advance the window; prefetch the one after it
+      c.wb += 32;
+      c.wu = c.nu;
+      c.wv = c.nv;
+      cur_load(eu, val, c.wb + 32, c.end, lane, c.nu, c.nv);
+      l -= 32;
+    }
+    unsigned u[4];
+    T a[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u[j] = __shfl_sync(0xffffffffu, c.wu, (l + j) & 31);
+      a[j] = __shfl_sync(0xffffffffu, c.wv, (l + j) & 31);
+    }
+    // entries of this chunk among the next four (sorted; window and row bounds)
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) n += (l + j < 32 && c.e + j < c.end && u[j] < cend) ? 1 : 0;
+    if (n == 0) break;
+    T g[4][V];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < n) lds_v<T, V>(xs + (u[j] - cu0) * (32 * V) + lane * V, g[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < n) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] += a[j] * g[j][v];
+      }
+    }
+    c.e += n;
+    if (n < 4 && l + n < 32) break;  // stopped at the chunk's end
+  }
+}
+
+template <class T, int V>
+__global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1) sart_fwd_stage_kernel(SartK<T> k, StageK<T> sk,
+                                                                           int it) {
+  it = pass_index(k, it, true);
+  if (loop_over(k, true)) return;
+  constexpr int RPW = kStageR / kWarps;  // rows per consumer warp
+  static_assert(RPW == 2, "two rows per consumer warp");
+  constexpr int S = 32 * V;               // slices (k.nrhs)
+  constexpr int REC = S * static_cast<int>(sizeof(T));
+  extern __shared__ __align__(128) char st_smem[];  // the ring; reused for the reductions
+  __shared__ __align__(8) unsigned long long full[kStageNS], empty[kStageNS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* ring = reinterpret_cast<T*>(st_smem);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStageNS; ++q) {
+      mbar_init(smem_u32(&full[q]), 1);
+      mbar_init(smem_u32(&empty[q]), kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long nb_total = sk.nblk * k.nsys;
+  const int sl = lane * V;
+  double r2a[V], r2b[V];  // per-slice ||r||^2 of system 0 / 1
+#pragma unroll
+  for (int v = 0; v < V; ++v) r2a[v] = r2b[v] = 0.0;
+  if (warp == kWarps) {
+    // ---- producer: every chunk of every block of this CTA, NS slots ahead
+    const unsigned ring_s = smem_u32(ring);
+    unsigned q = 0;
+    for (long long blk = blockIdx.x; blk < nb_total; blk += gridDim.x) {
+      const T* X = k.s[blk >= sk.nblk ? 1 : 0].x;
+      const int u0 = __ldg(sk.bptr + blk), u1 = __ldg(sk.bptr + blk + 1);
+      for (int cu = u0; cu < u1; cu += kStageC, ++q) {
+        const int nc = min(kStageC, u1 - cu);
+        const unsigned slot = q % kStageNS, use = q / kStageNS;
+        const unsigned fb = smem_u32(&full[slot]);
+        if (use > 0) mbar_wait(smem_u32(&empty[slot]), (use - 1) & 1u);
+        if (lane == 0) mbar_expect(fb, static_cast<unsigned>(nc * REC));
+        // consecutive union columns are contiguous X records (snake order:
+        // config 4 unions run ~23 columns): one bulk copy per run, per 32
+        for (int h = 0; h < nc; h += 32) {
+          const int m = min(32, nc - h);
+          const int col = lane < m ? __ldg(sk.buni + cu + h + lane) : 0;
+          const int prev = __shfl_up_sync(0xffffffffu, col, 1);
+          const bool head = lane < m && (lane == 0 || col != prev + 1);
+          const unsigned heads = __ballot_sync(0xffffffffu, head);
+          if (head) {
+            const unsigned later = heads & ~((2u << lane) - 1u);  // heads above this lane
+            const int len = (later ? __ffs(later) - 1 : m) - lane;
+            bulk_g2s(ring_s + (slot * kStageC + h + lane) * REC,
+                     X + static_cast<long long>(col) * S, static_cast<unsigned>(len * REC), fb);
+          }
+        }
+      }
+    }
+  } else {
+    // ---- consumers: warp w owns rows w and w + kWarps of each block
+    bool on0[V], on1[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      on0[v] = sys_on(k.state, sl + v);
+      on1[v] = k.nsys > 1 && sys_on(k.state, S + sl + v);
+    }
+    unsigned q = 0;
+    for (long long blk = blockIdx.x; blk < nb_total; blk += gridDim.x) {
+      const int sy = blk >= sk.nblk ? 1 : 0;
+      const SysK<T>& Sy = k.s[sy];
+      const unsigned short* eu = sy ? sk.eu1 : sk.eu0;
+      const T* rv = Sy.rv;
+      const int u0 = __ldg(sk.bptr + blk), u1 = __ldg(sk.bptr + blk + 1);
+      const int r0 = static_cast<int>((blk - sy * sk.nblk) * kStageR);
+      const int nr = min(kStageR, static_cast<int>(k.rows0) - r0);
+      RowCur<T> cur[RPW];
+      T acc[RPW][V];
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const int rl = warp + j * kWarps;
+        const int beg = rl < nr ? __ldg(Sy.rp + r0 + rl) : 0;
+        cur[j].end = rl < nr ? __ldg(Sy.rp + r0 + rl + 1) : 0;
+        cur[j].e = beg;
+        cur[j].wb = beg;
+        cur_load(eu, rv, beg, cur[j].end, lane, cur[j].wu, cur[j].wv);
+        cur_load(eu, rv, beg + 32, cur[j].end, lane, cur[j].nu, cur[j].nv);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[j][v] = T(0);
+      }
+      for (int cu = 0; cu < u1 - u0; cu += kStageC, ++q) {
+        const unsigned slot = q % kStageNS, use = q / kStageNS;
+        mbar_wait(smem_u32(&full[slot]), use & 1u);
+        const T* xs = ring + slot * kStageC * S;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          stage_row_chunk<T, V>(cur[r], eu, rv, static_cast<unsigned>(cu),
+                                static_cast<unsigned>(cu + kStageC), xs, lane, acc[r]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
+      }
+      // epilogue: r = p - A x, w = rinv r, per-slice ||r||^2
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const int rl = warp + r * kWarps;
+        if (rl >= nr) continue;
+        const long long i = r0 + rl;
+        const T ri = Sy.rinv[i];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (!(sy ? on1[v] : on0[v])) continue;
+          const long long o = i * S + sl + v;
+          const T rr = Sy.p[o] - acc[r][v];
+          Sy.w[o] = ri * rr;
+          const double d = static_cast<double>(rr) * static_cast<double>(rr);
+          if (sy) r2b[v] += d;
+          else r2a[v] += d;
+        }
+      }
+    }
+  }
+  __syncthreads();  // every chunk consumed: the ring is free
+  double* mred = reinterpret_cast<double*>(st_smem);  // [kWarps][nsys*S]
+  const int nsr = k.nsys * S;
+  if (warp < kWarps) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      mred[warp * nsr + sl + v] = r2a[v];
+      if (k.nsys > 1) mred[warp * nsr + S + sl + v] = r2b[v];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nsr; t += blockDim.x) {
+    double a = 0.0;
+    for (int w = 0; w < kWarps; ++w) a += mred[w * nsr + t];
+    k.partial[static_cast<long long>(t) * gridDim.x + blockIdx.x] = a;
+  }
+  if (last_block(k.ticket)) {
+    finish_norms(k.partial, gridDim.x, nsr, k.pnorm, k.tol, k.history, k.hstride, k.state, it);
+    loop_next(k, it);
+    if (threadIdx.x == 0) *k.ticket = 0;
+  }
+}
+
 template <class T, int V, int E>
 __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_back_block_kernel(SartK<T> k, BlockK<T> b, int it) {
   constexpr int R = kBlockR;
@@ -3490,7 +3734,36 @@ void launch_block(Plan& P, const SartK<T>& k, int it, bool fwd) {
 }
 
 template <class T>
+StageK<T> stage_args(const Plan& P) {
+  StageK<T> sk{};
+  sk.bptr = P.sbptr.get();
+  sk.buni = P.sbuni.get();
+  sk.eu0 = P.seu[0].get();
+  sk.eu1 = P.seu[1].get();
+  sk.nblk = P.snblk;
+  return sk;
+}
+
+template <class T>
+using StageFn = void (*)(SartK<T>, StageK<T>, int);
+
+template <class T>
+StageFn<T> stage_kernel(int nrhs) {
+  switch (nrhs) {
+    case 32: return sart_fwd_stage_kernel<T, 1>;
+    case 64: return sart_fwd_stage_kernel<T, 2>;
+    case 128: return sart_fwd_stage_kernel<T, 4>;
+    default: return nullptr;
+  }
+}
+
+template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
+  if (P.staged_f) {
+    stage_kernel<T>(P.nrhs)<<<P.fwd_blocks, kStageThreads, P.stage_smem, P.ctx->stream>>>(
+        k, stage_args<T>(P), it);
+    return;
+  }
   if (P.blocked_f) {
     launch_block<T>(P, k, it, true);
     return;
@@ -4417,12 +4690,16 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
       k = nb * ((c16b ? 2 : 4) + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
           (nexc_b ? nexc_b * (4 + 2 * b) + 4 * (cols[0] + 1) : 0);
     }
-  } else if (blocked_f || blocked_b) {  // union indices + 2R values per entry + pointers
+  } else if (blocked_f || blocked_b || staged_f) {  // union indices + 2R values per entry + pointers
     for (int s2 = 0; s2 < nsys; ++s2) {
       f += a[s2]->nnz * (4 + b) + 4 * (rows[s2] + 1);
       k += a[s2]->nnz * (4 + b) + 4 * (cols[s2] + 1);
     }
     if (blocked_f) f = nu_f * (4 + 2 * kBlockR * b) + 4 * (nblk_f + 1);
+    if (staged_f) {  // positions + values per entry, unions (X via L2)
+      f = 4 * snu + 4 * (snblk * nsys + 1);
+      for (int s2 = 0; s2 < nsys; ++s2) f += a[s2]->nnz * (2 + b) + 4 * (rows[s2] + 1);
+    }
     if (blocked_b) k = nu_b * (4 + 2 * kBlockR * b) + 4 * (nblk_b + 1);
   } else if (tiled && nsys == 1 && nrhs == 1) {
     f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
@@ -4448,7 +4725,9 @@ std::string Plan::describe() const {
     bk = "sart_back_tiled_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + (c16b ? "true" : "false") + ">";
   } else if (sharded || nrhs > 1 || !paired) {
-    fk = blocked_f ? "sart_fwd_block_kernel" : (nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel");
+    fk = staged_f ? "sart_fwd_stage_kernel"
+                  : (blocked_f ? "sart_fwd_block_kernel"
+                               : (nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel"));
     bk = blocked_b ? "sart_back_block_kernel"
                    : (nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel");
   } else {
@@ -4466,14 +4745,15 @@ std::string Plan::describe() const {
                                 : "";
   std::int64_t f = 0, b = 0;
   kernel_bytes(&f, &b);
-  char buf[1024];
+  char buf[2048];
   std::snprintf(buf, sizeof buf,
                 "{\"layout\": \"%s\", \"dtype\": \"%s\", \"nsys\": %d, \"nrhs\": %d, "
                 "\"vs_fwd\": %d, \"uf_fwd\": %d, \"vs_back\": %d, \"uf_back\": %d, "
                 "\"fwd_blocks\": %d, \"back_blocks\": %d, \"threads\": %d, "
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
                 "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s, "
-                "\"persistent_kernel\": \"%s\", \"persistent_grid\": %d}",
+                "\"persistent_kernel\": \"%s\", \"persistent_grid\": %d, "
+                "\"staged_union_columns\": %lld}",
                 sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
                         : (paired ? (tiled ? (mir_f || mir_b ? "paired-tiled-u16-mirror"
                                                                     : (c16f || c16b ? "paired-tiled-u16" : "paired-tiled"))
@@ -4482,7 +4762,8 @@ std::string Plan::describe() const {
                 t, nsys, nrhs, vs_fwd, uf_fwd, vs_back, uf_back, fwd_blocks, back_blocks, kThreads,
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
-                graph ? "true" : "false", pk.c_str(), cluster ? ccluster : (persistent ? pgrid : 0));
+                graph ? "true" : "false", pk.c_str(), cluster ? ccluster : (persistent ? pgrid : 0),
+                static_cast<long long>(staged_f ? snu : 0));
   return buf;
 }
 
@@ -4859,6 +5140,82 @@ void build_blocks(Plan& P) {
   if (need > P.partial.size()) P.partial.alloc(need);
 }
 
+// X-staged multi-RHS K1 (see sart_fwd_stage_kernel): blocks of kStageR rows
+// per system, each block's sorted column union, every CSR entry's position in
+// it, and per block and row the entry offset at each chunk boundary. Plans of
+// 32 / 64 / 128 slices without column bands use it (SSB_STAGED=0: the per-row
+// multi kernel); a block union beyond 65,535 columns disables it.
+template <class T>
+void build_stage_fwd(Plan& P) {
+  if (P.nrhs < 2 || P.nband > 1 || !stage_kernel<T>(P.nrhs) || env_int("SSB_STAGED", 1) == 0) {
+    return;
+  }
+  constexpr int R = kStageR;
+  const std::int64_t n = P.rows[0];
+  for (int s = 1; s < P.nsys; ++s) {
+    if (P.rows[s] != n) return;
+  }
+  const std::int64_t nblk = (n + R - 1) / R;
+  std::vector<int> bptr(1, 0), buni;
+  std::vector<int> uni;
+  for (int s = 0; s < P.nsys; ++s) {
+    Matrix* a = P.a[s];
+    std::vector<int> rp(n + 1), ci(a->nnz);
+    P.ctx->copy(rp.data(), a->rowptr.get(), (n + 1) * sizeof(int));
+    P.ctx->copy(ci.data(), a->colidx.get(), a->nnz * sizeof(int));
+    std::vector<unsigned short> eu(std::max<std::int64_t>(a->nnz, 1));
+    for (std::int64_t b = 0; b < nblk; ++b) {
+      const std::int64_t r0 = b * R, r1 = std::min<std::int64_t>(r0 + R, n);
+      uni.assign(ci.begin() + rp[r0], ci.begin() + rp[r1]);
+      std::sort(uni.begin(), uni.end());
+      uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+      if (uni.size() > 65535) return;  // positions are uint16
+      for (std::int64_t i = r0; i < r1; ++i) {
+        std::size_t u = 0;  // both ascending: one merge walk
+        for (int e = rp[i]; e < rp[i + 1]; ++e) {
+          while (uni[u] != ci[e]) ++u;
+          eu[e] = static_cast<unsigned short>(u);
+        }
+      }
+      buni.insert(buni.end(), uni.begin(), uni.end());
+      if (buni.size() >= (std::size_t{1} << 31)) return;
+      bptr.push_back(static_cast<int>(buni.size()));
+    }
+    P.seu[s].alloc(eu.size());
+    SSB_CUDA(cudaMemcpyAsync(P.seu[s].get(), eu.data(), eu.size() * 2, cudaMemcpyHostToDevice,
+                             P.ctx->stream));
+  }
+  P.sbptr.alloc(bptr.size());
+  P.sbuni.alloc(std::max<std::size_t>(buni.size(), 1));
+  SSB_CUDA(cudaMemcpyAsync(P.sbptr.get(), bptr.data(), bptr.size() * 4, cudaMemcpyHostToDevice,
+                           P.ctx->stream));
+  SSB_CUDA(cudaMemcpyAsync(P.sbuni.get(), buni.data(), buni.size() * 4, cudaMemcpyHostToDevice,
+                           P.ctx->stream));
+  P.ctx->sync();
+  P.snblk = nblk;
+  P.snu = static_cast<std::int64_t>(buni.size());
+  // the ring, reused for the per-slice reductions at the end
+  const long long rec = static_cast<long long>(P.nrhs) * sizeof(T);
+  P.stage_smem = static_cast<int>(std::max<long long>(kStageNS * kStageC * rec,
+                                                      8ll * kWarps * P.nsys * P.nrhs));
+  StageFn<T> fn = stage_kernel<T>(P.nrhs);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.stage_smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  int per_sm = 0;
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStageThreads,
+                                                         P.stage_smem));
+  if (per_sm < 1) return;
+  P.fwd_blocks = static_cast<int>(std::max<long long>(
+      1, std::min<long long>(static_cast<long long>(per_sm) * P.ctx->sm_count, nblk * P.nsys)));
+  const std::size_t need = static_cast<std::size_t>(P.fwd_blocks) * P.nsys * P.nrhs;
+  if (need > P.partial.size()) P.partial.alloc(need);
+  P.staged_f = true;
+  P.blocked_f = false;
+}
+
 // Persistent loop of a paired plan (see sart_persistent_pair_kernel): the
 // grid is every co-resident CTA the work can use; the barrier words are
 // zeroed once (the barrier leaves its count at 0).
@@ -5041,6 +5398,8 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   tr.mark("normalisers");
   if (o.dtype == SS_F32) build_blocks<float>(*P);
   else build_blocks<double>(*P);
+  if (o.dtype == SS_F32) build_stage_fwd<float>(*P);
+  else build_stage_fwd<double>(*P);
   if (P->paired) {
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);

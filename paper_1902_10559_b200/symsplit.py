@@ -739,7 +739,7 @@ class SartPlan:
     def describe(self) -> dict:
         """Kernel layout, VS/UF, grid and the kernel names ncu reports."""
         import json
-        buf = C.create_string_buffer(1024)
+        buf = C.create_string_buffer(2048)
         _check(_lib().ss_plan_describe(self.h, buf, len(buf)))
         return json.loads(buf.value.decode())
 

@@ -36,16 +36,18 @@ def slices(idx, S):
     return _cache[key]
 
 
-def plan_with(split, opts, S, blocked):
-    old = os.environ.get("SSB_BLOCKED")
-    os.environ["SSB_BLOCKED"] = str(blocked)
+def plan_with(split, opts, S, blocked, staged=0):
+    env = {"SSB_BLOCKED": str(blocked), "SSB_STAGED": str(staged)}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         pl = P.SartPlan(split.a1, split.a2, opts, nrhs=S)
     finally:
-        if old is None:
-            os.environ.pop("SSB_BLOCKED", None)
-        else:
-            os.environ["SSB_BLOCKED"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     return pl
 
 
