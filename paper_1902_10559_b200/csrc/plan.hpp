@@ -70,11 +70,13 @@ struct Plan {
   std::int64_t nblk_f = 0, nblk_b = 0, nu_f = 0, nu_b = 0;
   // multi-RHS K1 with X staged through a bulk-copy ring (sart_fwd_stage_kernel):
   // per block of kStageR rows of each system its column union, per CSR entry
-  // its position in that union
+  // the block's entries chunk-major with their position in the chunk
   bool staged_f = false;
-  DBuf<int> sbptr, sbuni;
-  DBuf<unsigned short> seu[2];
-  std::int64_t snblk = 0, snu = 0;
+  DBuf<int> sbptr, sbuni, sbch;
+  DBuf<long long> scofs;
+  DBuf<char> sent;
+  std::int64_t snblk = 0, snu = 0, sentb = 0;
+  int sslot = 0;
   int stage_smem = 0;
   int nband = 1;          // multi-RHS K1 passes over column bands
   DBuf<int> band_ptr[2];  // per system [nband + 1][rows] positions inside the CSR rows

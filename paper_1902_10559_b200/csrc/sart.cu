@@ -2343,31 +2343,41 @@ __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_fwd_block_kerne
 // Multi-RHS K1 with the gathered operand staged in shared memory by the bulk-
 // copy (TMA) engine. A CTA owns blocks of kStageR consecutive rows (rays of one
 // source, neighbouring detector bins) of one system. The rows of a block touch
-// a sorted union of columns U (config 4: 3,303 for 16 rows of ~624 entries,
-// reuse 3.0x). A producer warp walks U in chunks of kStageC columns and, per
-// column, issues one bulk copy of X[c][0..S) (S*sizeof(T) contiguous bytes of
-// the [n][S] layout) into a kStageNS-deep shared-memory ring whose slots
-// complete on mbarriers (bytes counted); it runs ahead across block
-// boundaries; consecutive union columns are one contiguous range of X, so a
-// chunk costs one bulk copy per run of columns (~2 per chunk on config 4).
-// Eight consumer warps (two rows each) apply every chunk: each
-// CSR entry carries its 16-bit position in U, so an entry is a shuffle-
-// broadcast (position, value) and one conflict-free shared-memory read of the
-// S-wide X record (V slices per lane). The X record of a column is read from
-// L2 once per block instead of once per row, never through L1; summation per
-// row and slice stays in CSR order (bitwise equal to the per-row multi kernel).
+// a sorted union U of columns (config 4: 3,303 for 16 rows of ~624 entries,
+// reuse 3.0x), cut into chunks of kStageC union positions. The plan stores
+// each block's entries chunk-major: per chunk a header of kStageR + 1 entry
+// offsets (one run per row) and the entries {value, position in the chunk}.
+// A producer warp fills a kStageNS-deep shared-memory ring: per chunk one bulk
+// copy of its entry record and one bulk copy per run of consecutive union
+// columns (contiguous X records [c][0..S) of the [n][S] layout; config 4
+// unions run ~23 columns), completing on the slot's mbarrier (bytes counted);
+// it runs ahead across block boundaries. Eight consumer warps (two rows each)
+// apply a chunk with one broadcast shared-memory read per entry and one
+// conflict-free read of its S-wide X record (V slices per lane). X records
+// thus move L2 -> shared memory once per block instead of once per row and
+// never through L1; each row and slice is summed in CSR order, one product at
+// a time (bitwise equal to the per-row multi kernel).
 constexpr int kStageR = 16;     // rows per block (2 per consumer warp)
-constexpr int kStageC = 64;     // union columns per chunk
+constexpr int kStageC = 64;     // union positions per chunk
 constexpr int kStageNS = 3;     // ring depth
 constexpr int kStageThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+constexpr int kStageHdr = 48;   // (kStageR + 1) uint16 run offsets, padded to 16 bytes
 
 template <class T>
 struct StageK {
-  const int* bptr;            // [nsys*nblk + 1] union range of each block (system-major)
-  const int* buni;            // union columns
-  const unsigned short* eu0;  // per CSR entry of system 0 / 1: its position in the block's union
-  const unsigned short* eu1;
-  long long nblk;             // blocks per system
+  const int* bptr;   // [nsys*nblk + 1] union range of each block (system-major)
+  const int* buni;   // union columns
+  const int* bch;    // [nsys*nblk] global index of each block's first chunk
+  const long long* cofs;  // [nchunks + 1] byte offset of each chunk's entry record
+  const char* ent;   // chunk records: header, then entries {T value, int position}
+  long long nblk;    // blocks per system
+  int slot_bytes;    // ring slot: kStageC X records + the largest entry record
+};
+
+template <class T>
+struct StageEnt {
+  T v;
+  int u;
 };
 
 __device__ __forceinline__ void mbar_arrive(unsigned mb) {
@@ -2403,70 +2413,9 @@ __device__ __forceinline__ void lds_v(const T* p, T (&o)[V]) {
   }
 }
 
-// one row's cursor over its CSR entries: a 32-entry window in the lanes'
-// registers (position, value) and the next window prefetched
-template <class T>
-struct RowCur {
-  int e, end, wb;  // next entry, row end, window base (absolute entry index)
-  unsigned wu, nu;
-  T wv, nv;
-};
-
-template <class T>
-__device__ __forceinline__ void cur_load(const unsigned short* eu, const T* val, int base, int end,
-                                         int lane, unsigned& u, T& v) {
-  const int e = base + lane;
-  u = e < end ? static_cast<unsigned>(__ldg(eu + e)) : 0xffffu;
-  v = e < end ? __ldg(val + e) : T(0);
-}
-
-// acc += the row's entries whose union position is below cend (the chunk
-// starting at position cu0, staged at xs); entries are sorted by position
 template <class T, int V>
-__device__ __forceinline__ void stage_row_chunk(RowCur<T>& c, const unsigned short* eu,
-                                                const T* val, unsigned cu0, unsigned cend,
-                                                const T* xs, int lane, T (&acc)[V]) {
-  while (c.e < c.end) {
-    int l = c.e - c.wb;
-    if (l >= 32) {  // advance the window; prefetch the one after it
-      c.wb += 32;
-      c.wu = c.nu;
-      c.wv = c.nv;
-      cur_load(eu, val, c.wb + 32, c.end, lane, c.nu, c.nv);
-      l -= 32;
-    }
-    unsigned u[4];
-    T a[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      u[j] = __shfl_sync(0xffffffffu, c.wu, (l + j) & 31);
-      a[j] = __shfl_sync(0xffffffffu, c.wv, (l + j) & 31);
-    }
-    // entries of this chunk among the next four (sorted; window and row bounds)
-    int n = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) n += (l + j < 32 && c.e + j < c.end && u[j] < cend) ? 1 : 0;
-    if (n == 0) break;
-    T g[4][V];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < n) lds_v<T, V>(xs + (u[j] - cu0) * (32 * V) + lane * V, g[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < n) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] += a[j] * g[j][v];
-      }
-    }
-    c.e += n;
-    if (n < 4 && l + n < 32) break;  // stopped at the chunk's end
-  }
-}
-
-template <class T, int V>
-__global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1) sart_fwd_stage_kernel(SartK<T> k, StageK<T> sk,
-                                                                           int it) {
+__global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
+    sart_fwd_stage_kernel(SartK<T> k, StageK<T> sk, int it) {
   it = pass_index(k, it, true);
   if (loop_over(k, true)) return;
   constexpr int RPW = kStageR / kWarps;  // rows per consumer warp
@@ -2476,7 +2425,6 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1) sart_fw
   extern __shared__ __align__(128) char st_smem[];  // the ring; reused for the reductions
   __shared__ __align__(8) unsigned long long full[kStageNS], empty[kStageNS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T* ring = reinterpret_cast<T*>(st_smem);
   if (threadIdx.x == 0) {
     for (int q = 0; q < kStageNS; ++q) {
       mbar_init(smem_u32(&full[q]), 1);
@@ -2491,34 +2439,80 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1) sart_fw
 #pragma unroll
   for (int v = 0; v < V; ++v) r2a[v] = r2b[v] = 0.0;
   if (warp == kWarps) {
-    // ---- producer: every chunk of every block of this CTA, NS slots ahead
-    const unsigned ring_s = smem_u32(ring);
-    unsigned q = 0;
-    for (long long blk = blockIdx.x; blk < nb_total; blk += gridDim.x) {
-      const T* X = k.s[blk >= sk.nblk ? 1 : 0].x;
-      const int u0 = __ldg(sk.bptr + blk), u1 = __ldg(sk.bptr + blk + 1);
-      for (int cu = u0; cu < u1; cu += kStageC, ++q) {
-        const int nc = min(kStageC, u1 - cu);
-        const unsigned slot = q % kStageNS, use = q / kStageNS;
-        const unsigned fb = smem_u32(&full[slot]);
-        if (use > 0) mbar_wait(smem_u32(&empty[slot]), (use - 1) & 1u);
-        if (lane == 0) mbar_expect(fb, static_cast<unsigned>(nc * REC));
-        // consecutive union columns are contiguous X records (snake order:
-        // config 4 unions run ~23 columns): one bulk copy per run, per 32
-        for (int h = 0; h < nc; h += 32) {
-          const int m = min(32, nc - h);
-          const int col = lane < m ? __ldg(sk.buni + cu + h + lane) : 0;
-          const int prev = __shfl_up_sync(0xffffffffu, col, 1);
-          const bool head = lane < m && (lane == 0 || col != prev + 1);
-          const unsigned heads = __ballot_sync(0xffffffffu, head);
-          if (head) {
-            const unsigned later = heads & ~((2u << lane) - 1u);  // heads above this lane
-            const int len = (later ? __ffs(later) - 1 : m) - lane;
-            bulk_g2s(ring_s + (slot * kStageC + h + lane) * REC,
-                     X + static_cast<long long>(col) * S, static_cast<unsigned>(len * REC), fb);
-          }
+    // ---- producer: every chunk of every block of this CTA, NS slots ahead;
+    // the next chunk's descriptors load while this one waits for its slot
+    const unsigned ring_s = smem_u32(st_smem);
+    struct Desc {
+      long long e0, e1;
+      int cu, nc, col0, col1;
+      const T* X;
+    };
+    long long blk = blockIdx.x;
+    int c = 0, nch = 0, u0 = 0, u1 = 0;
+    long long gc = 0;
+    const auto enter = [&]() {  // the block at blk (if any): its union and first chunk
+      if (blk >= nb_total) return;
+      u0 = __ldg(sk.bptr + blk);
+      u1 = __ldg(sk.bptr + blk + 1);
+      nch = (u1 - u0 + kStageC - 1) / kStageC;
+      gc = __ldg(sk.bch + blk);
+      c = 0;
+    };
+    const auto load = [&](Desc& d) {
+      d.cu = u0 + c * kStageC;
+      d.nc = min(kStageC, u1 - d.cu);
+      d.e0 = __ldg(sk.cofs + gc);
+      d.e1 = __ldg(sk.cofs + gc + 1);
+      d.col0 = lane < d.nc ? __ldg(sk.buni + d.cu + lane) : 0;
+      d.col1 = 32 + lane < d.nc ? __ldg(sk.buni + d.cu + 32 + lane) : 0;
+      d.X = k.s[blk >= sk.nblk ? 1 : 0].x;
+    };
+    const auto advance = [&]() {  // to the next chunk of this CTA
+      ++c;
+      ++gc;
+      while (blk < nb_total && c >= nch) {
+        blk += gridDim.x;
+        enter();
+      }
+    };
+    enter();
+    while (blk < nb_total && nch == 0) {
+      blk += gridDim.x;
+      enter();
+    }
+    Desc cur{};
+    if (blk < nb_total) load(cur);
+    for (unsigned q = 0; blk < nb_total; ++q) {
+      advance();
+      Desc nxt{};
+      const bool more = blk < nb_total;
+      if (more) load(nxt);
+      const unsigned slot = q % kStageNS, use = q / kStageNS;
+      const unsigned fb = smem_u32(&full[slot]);
+      const unsigned base = ring_s + slot * sk.slot_bytes;
+      if (use > 0) mbar_wait(smem_u32(&empty[slot]), (use - 1) & 1u);
+      if (lane == 0) {
+        mbar_expect(fb, static_cast<unsigned>(cur.nc * REC + (cur.e1 - cur.e0)));
+        bulk_g2s(base + kStageC * REC, sk.ent + cur.e0, static_cast<unsigned>(cur.e1 - cur.e0),
+                 fb);
+      }
+      // consecutive union columns are contiguous X records: one copy per run
+#pragma unroll
+      for (int h = 0; h < kStageC; h += 32) {
+        const int m = min(32, cur.nc - h);
+        const int col = h ? cur.col1 : cur.col0;
+        const int prev = __shfl_up_sync(0xffffffffu, col, 1);
+        const bool head = lane < m && (lane == 0 || col != prev + 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        if (head) {
+          const unsigned later = heads & ~((2u << lane) - 1u);  // heads above this lane
+          const int len = (later ? __ffs(later) - 1 : m) - lane;
+          bulk_g2s(base + (h + lane) * REC, cur.X + static_cast<long long>(col) * S,
+                   static_cast<unsigned>(len * REC), fb);
         }
       }
+      if (!more) break;
+      cur = nxt;
     }
   } else {
     // ---- consumers: warp w owns rows w and w + kWarps of each block
@@ -2532,33 +2526,44 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1) sart_fw
     for (long long blk = blockIdx.x; blk < nb_total; blk += gridDim.x) {
       const int sy = blk >= sk.nblk ? 1 : 0;
       const SysK<T>& Sy = k.s[sy];
-      const unsigned short* eu = sy ? sk.eu1 : sk.eu0;
-      const T* rv = Sy.rv;
       const int u0 = __ldg(sk.bptr + blk), u1 = __ldg(sk.bptr + blk + 1);
+      const int nch = (u1 - u0 + kStageC - 1) / kStageC;
       const int r0 = static_cast<int>((blk - sy * sk.nblk) * kStageR);
       const int nr = min(kStageR, static_cast<int>(k.rows0) - r0);
-      RowCur<T> cur[RPW];
       T acc[RPW][V];
 #pragma unroll
-      for (int j = 0; j < RPW; ++j) {
-        const int rl = warp + j * kWarps;
-        const int beg = rl < nr ? __ldg(Sy.rp + r0 + rl) : 0;
-        cur[j].end = rl < nr ? __ldg(Sy.rp + r0 + rl + 1) : 0;
-        cur[j].e = beg;
-        cur[j].wb = beg;
-        cur_load(eu, rv, beg, cur[j].end, lane, cur[j].wu, cur[j].wv);
-        cur_load(eu, rv, beg + 32, cur[j].end, lane, cur[j].nu, cur[j].nv);
+      for (int j = 0; j < RPW; ++j)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[j][v] = T(0);
-      }
-      for (int cu = 0; cu < u1 - u0; cu += kStageC, ++q) {
+      for (int c = 0; c < nch; ++c, ++q) {
         const unsigned slot = q % kStageNS, use = q / kStageNS;
         mbar_wait(smem_u32(&full[slot]), use & 1u);
-        const T* xs = ring + slot * kStageC * S;
+        const char* sb = st_smem + slot * sk.slot_bytes;
+        const T* xs = reinterpret_cast<const T*>(sb) + lane * V;
+        const unsigned short* hdr = reinterpret_cast<const unsigned short*>(sb + kStageC * REC);
+        const StageEnt<T>* ent = reinterpret_cast<const StageEnt<T>*>(sb + kStageC * REC + kStageHdr);
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
-          stage_row_chunk<T, V>(cur[r], eu, rv, static_cast<unsigned>(cu),
-                                static_cast<unsigned>(cu + kStageC), xs, lane, acc[r]);
+          const int rl = warp + r * kWarps;
+          const int eb = hdr[rl], ee = hdr[rl + 1];
+          for (int e = eb; e < ee; e += 4) {
+            StageEnt<T> en[4];
+            T g[4][V];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (e + j < ee) {
+                en[j] = ent[e + j];  // broadcast
+                lds_v<T, V>(xs + en[j].u * S, g[j]);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (e + j < ee) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[r][v] += en[j].v * g[j][v];
+              }
+            }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
@@ -3738,9 +3743,11 @@ StageK<T> stage_args(const Plan& P) {
   StageK<T> sk{};
   sk.bptr = P.sbptr.get();
   sk.buni = P.sbuni.get();
-  sk.eu0 = P.seu[0].get();
-  sk.eu1 = P.seu[1].get();
+  sk.bch = P.sbch.get();
+  sk.cofs = P.scofs.get();
+  sk.ent = P.sent.get();
   sk.nblk = P.snblk;
+  sk.slot_bytes = P.sslot;
   return sk;
 }
 
@@ -4696,10 +4703,7 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
       k += a[s2]->nnz * (4 + b) + 4 * (cols[s2] + 1);
     }
     if (blocked_f) f = nu_f * (4 + 2 * kBlockR * b) + 4 * (nblk_f + 1);
-    if (staged_f) {  // positions + values per entry, unions (X via L2)
-      f = 4 * snu + 4 * (snblk * nsys + 1);
-      for (int s2 = 0; s2 < nsys; ++s2) f += a[s2]->nnz * (2 + b) + 4 * (rows[s2] + 1);
-    }
+    if (staged_f) f = sentb + 4 * snu + 4 * (snblk * nsys + 1);  // chunk records + unions (X via L2)
     if (blocked_b) k = nu_b * (4 + 2 * kBlockR * b) + 4 * (nblk_b + 1);
   } else if (tiled && nsys == 1 && nrhs == 1) {
     f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
@@ -5150,53 +5154,92 @@ void build_stage_fwd(Plan& P) {
   if (P.nrhs < 2 || P.nband > 1 || !stage_kernel<T>(P.nrhs) || env_int("SSB_STAGED", 1) == 0) {
     return;
   }
-  constexpr int R = kStageR;
+  constexpr int R = kStageR, C = kStageC;
   const std::int64_t n = P.rows[0];
   for (int s = 1; s < P.nsys; ++s) {
     if (P.rows[s] != n) return;
   }
   const std::int64_t nblk = (n + R - 1) / R;
-  std::vector<int> bptr(1, 0), buni;
-  std::vector<int> uni;
+  std::vector<int> bptr(1, 0), buni, bch;
+  std::vector<long long> cofs(1, 0);
+  std::vector<char> ent;
+  std::vector<int> uni, pos;
+  long long maxrec = 0;
+  const auto put = [&](const void* p, std::size_t nb) {
+    const char* c = static_cast<const char*>(p);
+    ent.insert(ent.end(), c, c + nb);
+  };
   for (int s = 0; s < P.nsys; ++s) {
     Matrix* a = P.a[s];
     std::vector<int> rp(n + 1), ci(a->nnz);
+    std::vector<double> va(a->nnz);
     P.ctx->copy(rp.data(), a->rowptr.get(), (n + 1) * sizeof(int));
     P.ctx->copy(ci.data(), a->colidx.get(), a->nnz * sizeof(int));
-    std::vector<unsigned short> eu(std::max<std::int64_t>(a->nnz, 1));
+    P.ctx->copy(va.data(), a->val.get(), a->nnz * sizeof(double));
+    pos.resize(a->nnz);
     for (std::int64_t b = 0; b < nblk; ++b) {
       const std::int64_t r0 = b * R, r1 = std::min<std::int64_t>(r0 + R, n);
       uni.assign(ci.begin() + rp[r0], ci.begin() + rp[r1]);
       std::sort(uni.begin(), uni.end());
       uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
-      if (uni.size() > 65535) return;  // positions are uint16
       for (std::int64_t i = r0; i < r1; ++i) {
         std::size_t u = 0;  // both ascending: one merge walk
         for (int e = rp[i]; e < rp[i + 1]; ++e) {
           while (uni[u] != ci[e]) ++u;
-          eu[e] = static_cast<unsigned short>(u);
+          pos[e] = static_cast<int>(u);
         }
+      }
+      const int nch = (static_cast<int>(uni.size()) + C - 1) / C;
+      bch.push_back(static_cast<int>(cofs.size() - 1));
+      std::vector<int> cur(R, 0);  // next entry of each row
+      for (int rl = 0; rl < R; ++rl) cur[rl] = r0 + rl < r1 ? rp[r0 + rl] : 0;
+      for (int c = 0; c < nch; ++c) {
+        // header: kStageR + 1 run offsets, then {value, position - c*C} per entry
+        const std::size_t h0 = ent.size();
+        ent.resize(h0 + kStageHdr, 0);
+        unsigned short off = 0;
+        for (int rl = 0; rl < R; ++rl) {
+          std::memcpy(&ent[h0 + 2 * rl], &off, 2);
+          if (r0 + rl >= r1) continue;
+          const int end = rp[r0 + rl + 1];
+          for (int& e = cur[rl]; e < end && pos[e] < (c + 1) * C; ++e) {
+            StageEnt<T> se;
+            std::memset(&se, 0, sizeof se);
+            se.v = static_cast<T>(va[e]);
+            se.u = pos[e] - c * C;
+            put(&se, sizeof se);
+            ++off;
+          }
+        }
+        std::memcpy(&ent[h0 + 2 * R], &off, 2);
+        ent.resize((ent.size() + 15) & ~std::size_t{15}, 0);
+        maxrec = std::max<long long>(maxrec, static_cast<long long>(ent.size() - h0));
+        cofs.push_back(static_cast<long long>(ent.size()));
       }
       buni.insert(buni.end(), uni.begin(), uni.end());
       if (buni.size() >= (std::size_t{1} << 31)) return;
       bptr.push_back(static_cast<int>(buni.size()));
     }
-    P.seu[s].alloc(eu.size());
-    SSB_CUDA(cudaMemcpyAsync(P.seu[s].get(), eu.data(), eu.size() * 2, cudaMemcpyHostToDevice,
-                             P.ctx->stream));
   }
-  P.sbptr.alloc(bptr.size());
-  P.sbuni.alloc(std::max<std::size_t>(buni.size(), 1));
-  SSB_CUDA(cudaMemcpyAsync(P.sbptr.get(), bptr.data(), bptr.size() * 4, cudaMemcpyHostToDevice,
-                           P.ctx->stream));
-  SSB_CUDA(cudaMemcpyAsync(P.sbuni.get(), buni.data(), buni.size() * 4, cudaMemcpyHostToDevice,
-                           P.ctx->stream));
+  const auto up = [&](auto& dbuf, const auto& v) {
+    dbuf.alloc(std::max<std::size_t>(v.size(), 1));
+    SSB_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice,
+                             P.ctx->stream));
+  };
+  up(P.sbptr, bptr);
+  up(P.sbuni, buni);
+  up(P.sbch, bch);
+  up(P.scofs, cofs);
+  up(P.sent, ent);
   P.ctx->sync();
   P.snblk = nblk;
   P.snu = static_cast<std::int64_t>(buni.size());
-  // the ring, reused for the per-slice reductions at the end
+  P.sentb = static_cast<std::int64_t>(ent.size());
+  // ring slots: kStageC X records + the largest chunk record; the ring is
+  // reused for the per-slice reductions at the end
   const long long rec = static_cast<long long>(P.nrhs) * sizeof(T);
-  P.stage_smem = static_cast<int>(std::max<long long>(kStageNS * kStageC * rec,
+  P.sslot = static_cast<int>((C * rec + maxrec + 127) & ~127ll);
+  P.stage_smem = static_cast<int>(std::max<long long>(static_cast<long long>(kStageNS) * P.sslot,
                                                       8ll * kWarps * P.nsys * P.nrhs));
   StageFn<T> fn = stage_kernel<T>(P.nrhs);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.stage_smem) !=
