@@ -2346,22 +2346,26 @@ __global__ void __launch_bounds__(kThreads, E <= 2 ? 3 : 1) sart_fwd_block_kerne
 // a sorted union U of columns (config 4: 3,303 for 16 rows of ~624 entries,
 // reuse 3.0x), cut into chunks of kStageC union positions. The plan stores
 // each block's entries chunk-major: per chunk a header of kStageR + 1 entry
-// offsets (one run per row) and the entries {value, position in the chunk}.
+// offsets (one run per pair of neighbouring rows) and the pair's merged
+// entries {value of row a, value of row b (0 where absent), position in the
+// chunk}: one X record read serves both rays (config 4: 803 merged positions
+// per pair instead of 2 x 624 row entries).
 // A producer warp fills a kStageNS-deep shared-memory ring: per chunk one bulk
 // copy of its entry record and one bulk copy per run of consecutive union
 // columns (contiguous X records [c][0..S) of the [n][S] layout; config 4
 // unions run ~23 columns), completing on the slot's mbarrier (bytes counted);
 // it runs ahead across block boundaries. Eight consumer warps (two rows each)
-// apply a chunk with one broadcast shared-memory read per entry and one
-// conflict-free read of its S-wide X record (V slices per lane). X records
+// apply a chunk with one broadcast shared-memory read per merged entry and one
+// conflict-free read of its S-wide X record (V slices per lane) for two rows. X records
 // thus move L2 -> shared memory once per block instead of once per row and
 // never through L1; each row and slice is summed in CSR order, one product at
-// a time (bitwise equal to the per-row multi kernel).
+// a time, the padding adding exact zeros (bitwise equal to the per-row multi
+// kernel).
 constexpr int kStageR = 16;     // rows per block (2 per consumer warp)
 constexpr int kStageC = 64;     // union positions per chunk
 constexpr int kStageNS = 3;     // ring depth
 constexpr int kStageThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
-constexpr int kStageHdr = 48;   // (kStageR + 1) uint16 run offsets, padded to 16 bytes
+constexpr int kStageHdr = 32;   // (kStageR / 2 + 1) uint16 run offsets (row pairs), padded
 
 template <class T>
 struct StageK {
@@ -2374,9 +2378,11 @@ struct StageK {
   int slot_bytes;    // ring slot: kStageC X records + the largest entry record
 };
 
+// one union position of a row pair: both rows' values (0 where a row has no
+// entry) and the position within the chunk
 template <class T>
-struct StageEnt {
-  T v;
+struct alignas(16) StageEnt {
+  T va, vb;
   int u;
 };
 
@@ -2515,7 +2521,7 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
       cur = nxt;
     }
   } else {
-    // ---- consumers: warp w owns rows w and w + kWarps of each block
+    // ---- consumers: warp w owns the neighbouring rows 2w and 2w + 1 of each block
     bool on0[V], on1[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -2542,25 +2548,24 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
         const T* xs = reinterpret_cast<const T*>(sb) + lane * V;
         const unsigned short* hdr = reinterpret_cast<const unsigned short*>(sb + kStageC * REC);
         const StageEnt<T>* ent = reinterpret_cast<const StageEnt<T>*>(sb + kStageC * REC + kStageHdr);
+        const int eb = hdr[warp], ee = hdr[warp + 1];
+        for (int e = eb; e < ee; e += 4) {
+          StageEnt<T> en[4];
+          T g[4][V];
 #pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const int rl = warp + r * kWarps;
-          const int eb = hdr[rl], ee = hdr[rl + 1];
-          for (int e = eb; e < ee; e += 4) {
-            StageEnt<T> en[4];
-            T g[4][V];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              if (e + j < ee) {
-                en[j] = ent[e + j];  // broadcast
-                lds_v<T, V>(xs + en[j].u * S, g[j]);
-              }
+          for (int j = 0; j < 4; ++j) {
+            if (e + j < ee) {
+              en[j] = ent[e + j];  // broadcast
+              lds_v<T, V>(xs + en[j].u * S, g[j]);
             }
+          }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              if (e + j < ee) {
+          for (int j = 0; j < 4; ++j) {
+            if (e + j < ee) {
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[r][v] += en[j].v * g[j][v];
+              for (int v = 0; v < V; ++v) {
+                acc[0][v] += en[j].va * g[j][v];
+                acc[1][v] += en[j].vb * g[j][v];
               }
             }
           }
@@ -2571,7 +2576,7 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
       // epilogue: r = p - A x, w = rinv r, per-slice ||r||^2
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const int rl = warp + r * kWarps;
+        const int rl = 2 * warp + r;
         if (rl >= nr) continue;
         const long long i = r0 + rl;
         const T ri = Sy.rinv[i];
@@ -5194,24 +5199,33 @@ void build_stage_fwd(Plan& P) {
       std::vector<int> cur(R, 0);  // next entry of each row
       for (int rl = 0; rl < R; ++rl) cur[rl] = r0 + rl < r1 ? rp[r0 + rl] : 0;
       for (int c = 0; c < nch; ++c) {
-        // header: kStageR + 1 run offsets, then {value, position - c*C} per entry
+        // header: kStageR / 2 + 1 run offsets (row pairs), then per pair the
+        // merged positions {value a, value b, position - c*C}
         const std::size_t h0 = ent.size();
         ent.resize(h0 + kStageHdr, 0);
         unsigned short off = 0;
-        for (int rl = 0; rl < R; ++rl) {
-          std::memcpy(&ent[h0 + 2 * rl], &off, 2);
-          if (r0 + rl >= r1) continue;
-          const int end = rp[r0 + rl + 1];
-          for (int& e = cur[rl]; e < end && pos[e] < (c + 1) * C; ++e) {
+        for (int pr = 0; pr < R / 2; ++pr) {
+          std::memcpy(&ent[h0 + 2 * pr], &off, 2);
+          const int ra = 2 * pr, rb = ra + 1;
+          const int ea = r0 + ra < r1 ? rp[r0 + ra + 1] : 0;
+          const int ebd = r0 + rb < r1 ? rp[r0 + rb + 1] : 0;
+          int& ia = cur[ra];
+          int& ib = cur[rb];
+          while (true) {
+            const int pa = ia < ea && pos[ia] < (c + 1) * C ? pos[ia] : INT32_MAX;
+            const int pb = ib < ebd && pos[ib] < (c + 1) * C ? pos[ib] : INT32_MAX;
+            const int pm = std::min(pa, pb);
+            if (pm == INT32_MAX) break;
             StageEnt<T> se;
             std::memset(&se, 0, sizeof se);
-            se.v = static_cast<T>(va[e]);
-            se.u = pos[e] - c * C;
+            se.u = pm - c * C;
+            if (pa == pm) se.va = static_cast<T>(va[ia++]);
+            if (pb == pm) se.vb = static_cast<T>(va[ib++]);
             put(&se, sizeof se);
             ++off;
           }
         }
-        std::memcpy(&ent[h0 + 2 * R], &off, 2);
+        std::memcpy(&ent[h0 + 2 * (R / 2)], &off, 2);
         ent.resize((ent.size() + 15) & ~std::size_t{15}, 0);
         maxrec = std::max<long long>(maxrec, static_cast<long long>(ent.size() - h0));
         cofs.push_back(static_cast<long long>(ent.size()));
