@@ -68,16 +68,18 @@ struct Plan {
   DBuf<int> bptr_f, bidx_f, bptr_b, bidx_b;
   DBuf<char> bval_f, bval_b;
   std::int64_t nblk_f = 0, nblk_b = 0, nu_f = 0, nu_b = 0;
-  // multi-RHS K1 with X staged through a bulk-copy ring (sart_fwd_stage_kernel):
-  // per block of kStageR rows of each system its column union, per CSR entry
-  // the block's entries chunk-major with their position in the chunk
-  bool staged_f = false;
-  DBuf<int> sbptr, sbuni, sbch;
-  DBuf<long long> scofs;
-  DBuf<char> sent;
-  std::int64_t snblk = 0, snu = 0, sentb = 0;
-  int sslot = 0;
-  int stage_smem = 0;
+  // multi-RHS K1 / K2 with the gathered operand staged through a bulk-copy
+  // ring (sart_stage_kernel): per direction, per block of kStageR vectors of
+  // each system its index union and its entries chunk-major (row / column
+  // pairs merged) with their position in the chunk
+  struct StageBufs {
+    bool on = false;
+    DBuf<int> bptr, buni, bch;
+    DBuf<long long> cofs;
+    DBuf<char> ent;
+    std::int64_t nblk = 0, nu = 0, entb = 0;
+    int slot = 0, smem = 0, blocks = 0;
+  } stg[2];  // [0] K1 (rows, X), [1] K2 (columns, W)
   int nband = 1;          // multi-RHS K1 passes over column bands
   DBuf<int> band_ptr[2];  // per system [nband + 1][rows] positions inside the CSR rows
   // paired + tiled: rows/columns padded to 4 entries and permuted within tiles

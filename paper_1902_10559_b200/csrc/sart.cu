@@ -2419,11 +2419,11 @@ __device__ __forceinline__ void lds_v(const T* p, T (&o)[V]) {
   }
 }
 
-template <class T, int V>
+template <class T, int V, bool FWD>
 __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
-    sart_fwd_stage_kernel(SartK<T> k, StageK<T> sk, int it) {
-  it = pass_index(k, it, true);
-  if (loop_over(k, true)) return;
+    sart_stage_kernel(SartK<T> k, StageK<T> sk, int it) {
+  it = pass_index(k, it, FWD);
+  if (loop_over(k, FWD)) return;
   constexpr int RPW = kStageR / kWarps;  // rows per consumer warp
   static_assert(RPW == 2, "two rows per consumer warp");
   constexpr int S = 32 * V;               // slices (k.nrhs)
@@ -2471,7 +2471,7 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
       d.e1 = __ldg(sk.cofs + gc + 1);
       d.col0 = lane < d.nc ? __ldg(sk.buni + d.cu + lane) : 0;
       d.col1 = 32 + lane < d.nc ? __ldg(sk.buni + d.cu + 32 + lane) : 0;
-      d.X = k.s[blk >= sk.nblk ? 1 : 0].x;
+      d.X = FWD ? k.s[blk >= sk.nblk ? 1 : 0].x : k.s[blk >= sk.nblk ? 1 : 0].w;
     };
     const auto advance = [&]() {  // to the next chunk of this CTA
       ++c;
@@ -2535,7 +2535,7 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
       const int u0 = __ldg(sk.bptr + blk), u1 = __ldg(sk.bptr + blk + 1);
       const int nch = (u1 - u0 + kStageC - 1) / kStageC;
       const int r0 = static_cast<int>((blk - sy * sk.nblk) * kStageR);
-      const int nr = min(kStageR, static_cast<int>(k.rows0) - r0);
+      const int nr = min(kStageR, static_cast<int>(FWD ? k.rows0 : k.cols0) - r0);
       T acc[RPW][V];
 #pragma unroll
       for (int j = 0; j < RPW; ++j)
@@ -2573,26 +2573,40 @@ __global__ void __launch_bounds__(kStageThreads, sizeof(T) == 4 ? 2 : 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
       }
-      // epilogue: r = p - A x, w = rinv r, per-slice ||r||^2
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
         const int rl = 2 * warp + r;
         if (rl >= nr) continue;
         const long long i = r0 + rl;
-        const T ri = Sy.rinv[i];
+        if constexpr (FWD) {  // r = p - A x, w = rinv r, per-slice ||r||^2
+          const T ri = Sy.rinv[i];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if (!(sy ? on1[v] : on0[v])) continue;
-          const long long o = i * S + sl + v;
-          const T rr = Sy.p[o] - acc[r][v];
-          Sy.w[o] = ri * rr;
-          const double d = static_cast<double>(rr) * static_cast<double>(rr);
-          if (sy) r2b[v] += d;
-          else r2a[v] += d;
+          for (int v = 0; v < V; ++v) {
+            if (!(sy ? on1[v] : on0[v])) continue;
+            const long long o = i * S + sl + v;
+            const T rr = Sy.p[o] - acc[r][v];
+            Sy.w[o] = ri * rr;
+            const double d = static_cast<double>(rr) * static_cast<double>(rr);
+            if (sy) r2b[v] += d;
+            else r2a[v] += d;
+          }
+        } else {  // x += lambda * (u * cinv) (skipped for stopped slices)
+          const T ci = Sy.cinv[i];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (!(sy ? on1[v] : on0[v])) continue;
+            const long long o = i * S + sl + v;
+            const T xn = upd(Sy.x[o], k.relax, acc[r][v], ci);
+            Sy.x[o] = xn;
+            if (!isfinite(static_cast<double>(xn))) {
+              atomicCAS(&k.state[4 * (sy * S + sl + v) + 2], 0, it + 1);
+            }
+          }
         }
       }
     }
   }
+  if constexpr (!FWD) return;
   __syncthreads();  // every chunk consumed: the ring is free
   double* mred = reinterpret_cast<double*>(st_smem);  // [kWarps][nsys*S]
   const int nsr = k.nsys * S;
@@ -3744,15 +3758,16 @@ void launch_block(Plan& P, const SartK<T>& k, int it, bool fwd) {
 }
 
 template <class T>
-StageK<T> stage_args(const Plan& P) {
+StageK<T> stage_args(const Plan& P, bool fwd) {
+  const Plan::StageBufs& b = P.stg[fwd ? 0 : 1];
   StageK<T> sk{};
-  sk.bptr = P.sbptr.get();
-  sk.buni = P.sbuni.get();
-  sk.bch = P.sbch.get();
-  sk.cofs = P.scofs.get();
-  sk.ent = P.sent.get();
-  sk.nblk = P.snblk;
-  sk.slot_bytes = P.sslot;
+  sk.bptr = b.bptr.get();
+  sk.buni = b.buni.get();
+  sk.bch = b.bch.get();
+  sk.cofs = b.cofs.get();
+  sk.ent = b.ent.get();
+  sk.nblk = b.nblk;
+  sk.slot_bytes = b.slot;
   return sk;
 }
 
@@ -3760,20 +3775,26 @@ template <class T>
 using StageFn = void (*)(SartK<T>, StageK<T>, int);
 
 template <class T>
-StageFn<T> stage_kernel(int nrhs) {
+StageFn<T> stage_kernel(int nrhs, bool fwd) {
   switch (nrhs) {
-    case 32: return sart_fwd_stage_kernel<T, 1>;
-    case 64: return sart_fwd_stage_kernel<T, 2>;
-    case 128: return sart_fwd_stage_kernel<T, 4>;
+    case 32: return fwd ? sart_stage_kernel<T, 1, true> : sart_stage_kernel<T, 1, false>;
+    case 64: return fwd ? sart_stage_kernel<T, 2, true> : sart_stage_kernel<T, 2, false>;
+    case 128: return fwd ? sart_stage_kernel<T, 4, true> : sart_stage_kernel<T, 4, false>;
     default: return nullptr;
   }
 }
 
 template <class T>
+void launch_stage(Plan& P, const SartK<T>& k, int it, bool fwd) {
+  const Plan::StageBufs& b = P.stg[fwd ? 0 : 1];
+  stage_kernel<T>(P.nrhs, fwd)<<<b.blocks, kStageThreads, b.smem, P.ctx->stream>>>(
+      k, stage_args<T>(P, fwd), it);
+}
+
+template <class T>
 void launch_fwd(Plan& P, const SartK<T>& k, int it) {
-  if (P.staged_f) {
-    stage_kernel<T>(P.nrhs)<<<P.fwd_blocks, kStageThreads, P.stage_smem, P.ctx->stream>>>(
-        k, stage_args<T>(P), it);
+  if (P.stg[0].on) {
+    launch_stage<T>(P, k, it, true);
     return;
   }
   if (P.blocked_f) {
@@ -3802,6 +3823,10 @@ void launch_fwd(Plan& P, const SartK<T>& k, int it) {
 
 template <class T>
 void launch_back(Plan& P, const SartK<T>& k, int it) {
+  if (P.stg[1].on) {
+    launch_stage<T>(P, k, it, false);
+    return;
+  }
   if (P.blocked_b) {
     launch_block<T>(P, k, it, false);
     return;
@@ -4702,14 +4727,16 @@ void Plan::kernel_bytes(std::int64_t* fwd, std::int64_t* back) const {
       k = nb * ((c16b ? 2 : 4) + b) + 4 * hs_b * ntile_b + 8 * (cols[0] + 1) +
           (nexc_b ? nexc_b * (4 + 2 * b) + 4 * (cols[0] + 1) : 0);
     }
-  } else if (blocked_f || blocked_b || staged_f) {  // union indices + 2R values per entry + pointers
+  } else if (blocked_f || blocked_b || stg[0].on || stg[1].on) {  // union indices + 2R values per entry + pointers
     for (int s2 = 0; s2 < nsys; ++s2) {
       f += a[s2]->nnz * (4 + b) + 4 * (rows[s2] + 1);
       k += a[s2]->nnz * (4 + b) + 4 * (cols[s2] + 1);
     }
     if (blocked_f) f = nu_f * (4 + 2 * kBlockR * b) + 4 * (nblk_f + 1);
-    if (staged_f) f = sentb + 4 * snu + 4 * (snblk * nsys + 1);  // chunk records + unions (X via L2)
     if (blocked_b) k = nu_b * (4 + 2 * kBlockR * b) + 4 * (nblk_b + 1);
+    // staged: chunk records + unions (+ pointers); the operand moves via L2
+    if (stg[0].on) f = stg[0].entb + 4 * stg[0].nu + 4 * (stg[0].nblk * nsys + 1);
+    if (stg[1].on) k = stg[1].entb + 4 * stg[1].nu + 4 * (stg[1].nblk * nsys + 1);
   } else if (tiled && nsys == 1 && nrhs == 1) {
     f = c16f ? tnnz_f * (2 + b) + 4 * ntile_f + 8 * (rows[0] + 1)
              : tnnz_f * (4 + b) + 4 * (rows[0] + 1);
@@ -4734,11 +4761,12 @@ std::string Plan::describe() const {
     bk = "sart_back_tiled_kernel<" + std::string(t) + ", " + std::to_string(vs_back) + ", " +
          std::to_string(uf_back) + ", " + (c16b ? "true" : "false") + ">";
   } else if (sharded || nrhs > 1 || !paired) {
-    fk = staged_f ? "sart_fwd_stage_kernel"
-                  : (blocked_f ? "sart_fwd_block_kernel"
-                               : (nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel"));
-    bk = blocked_b ? "sart_back_block_kernel"
-                   : (nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel");
+    fk = stg[0].on ? "sart_stage_kernel<fwd>"
+                   : (blocked_f ? "sart_fwd_block_kernel"
+                                : (nrhs > 1 ? "sart_fwd_multi_kernel" : "sart_fwd_kernel"));
+    bk = stg[1].on ? "sart_stage_kernel<back>"
+                   : (blocked_b ? "sart_back_block_kernel"
+                                : (nrhs > 1 ? "sart_back_multi_kernel" : "sart_back_kernel"));
   } else {
     fk = "sart_fwd_pair_kernel<" + std::string(t) + ", " + std::to_string(vs_fwd) + ", " +
          std::to_string(uf_fwd) + ", " + std::to_string(layout_mode(true)) + ">";
@@ -4762,7 +4790,7 @@ std::string Plan::describe() const {
                 "\"fwd_kernel\": \"%s\", \"back_kernel\": \"%s\", \"fwd_bytes\": %lld, "
                 "\"back_bytes\": %lld, \"exceptions\": [%lld, %lld], \"graph\": %s, "
                 "\"persistent_kernel\": \"%s\", \"persistent_grid\": %d, "
-                "\"staged_union_columns\": %lld}",
+                "\"staged_union\": [%lld, %lld]}",
                 sharded ? (tiled ? "row-sharded-tiled" : "row-sharded")
                         : (paired ? (tiled ? (mir_f || mir_b ? "paired-tiled-u16-mirror"
                                                                     : (c16f || c16b ? "paired-tiled-u16" : "paired-tiled"))
@@ -4772,7 +4800,8 @@ std::string Plan::describe() const {
                 fk.c_str(), bk.c_str(), static_cast<long long>(f), static_cast<long long>(b),
                 static_cast<long long>(nexc_f), static_cast<long long>(nexc_b),
                 graph ? "true" : "false", pk.c_str(), cluster ? ccluster : (persistent ? pgrid : 0),
-                static_cast<long long>(staged_f ? snu : 0));
+                static_cast<long long>(stg[0].on ? stg[0].nu : 0),
+                static_cast<long long>(stg[1].on ? stg[1].nu : 0));
   return buf;
 }
 
@@ -5149,20 +5178,17 @@ void build_blocks(Plan& P) {
   if (need > P.partial.size()) P.partial.alloc(need);
 }
 
-// X-staged multi-RHS K1 (see sart_fwd_stage_kernel): blocks of kStageR rows
-// per system, each block's sorted column union, every CSR entry's position in
-// it, and per block and row the entry offset at each chunk boundary. Plans of
-// 32 / 64 / 128 slices without column bands use it (SSB_STAGED=0: the per-row
-// multi kernel); a block union beyond 65,535 columns disables it.
+// Staged multi-RHS streams of one direction (see sart_stage_kernel): blocks of
+// kStageR rows (K1) / columns (K2) per system, each block's sorted index union
+// and its entries chunk-major, neighbouring vector pairs merged.
 template <class T>
-void build_stage_fwd(Plan& P) {
-  if (P.nrhs < 2 || P.nband > 1 || !stage_kernel<T>(P.nrhs) || env_int("SSB_STAGED", 1) == 0) {
-    return;
-  }
+void build_stage_dir(Plan& P, bool fwd) {
+  Plan::StageBufs& B = P.stg[fwd ? 0 : 1];
+  B.on = false;
   constexpr int R = kStageR, C = kStageC;
-  const std::int64_t n = P.rows[0];
+  const std::int64_t n = fwd ? P.rows[0] : P.cols[0];
   for (int s = 1; s < P.nsys; ++s) {
-    if (P.rows[s] != n) return;
+    if ((fwd ? P.rows[s] : P.cols[s]) != n) return;
   }
   const std::int64_t nblk = (n + R - 1) / R;
   std::vector<int> bptr(1, 0), buni, bch;
@@ -5176,11 +5202,12 @@ void build_stage_fwd(Plan& P) {
   };
   for (int s = 0; s < P.nsys; ++s) {
     Matrix* a = P.a[s];
+    if (!fwd) a->ensure_csc();
     std::vector<int> rp(n + 1), ci(a->nnz);
     std::vector<double> va(a->nnz);
-    P.ctx->copy(rp.data(), a->rowptr.get(), (n + 1) * sizeof(int));
-    P.ctx->copy(ci.data(), a->colidx.get(), a->nnz * sizeof(int));
-    P.ctx->copy(va.data(), a->val.get(), a->nnz * sizeof(double));
+    P.ctx->copy(rp.data(), fwd ? a->rowptr.get() : a->colptr.get(), (n + 1) * sizeof(int));
+    P.ctx->copy(ci.data(), fwd ? a->colidx.get() : a->rowidx.get(), a->nnz * sizeof(int));
+    P.ctx->copy(va.data(), fwd ? a->val.get() : a->cval.get(), a->nnz * sizeof(double));
     pos.resize(a->nnz);
     for (std::int64_t b = 0; b < nblk; ++b) {
       const std::int64_t r0 = b * R, r1 = std::min<std::int64_t>(r0 + R, n);
@@ -5240,37 +5267,54 @@ void build_stage_fwd(Plan& P) {
     SSB_CUDA(cudaMemcpyAsync(dbuf.get(), v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice,
                              P.ctx->stream));
   };
-  up(P.sbptr, bptr);
-  up(P.sbuni, buni);
-  up(P.sbch, bch);
-  up(P.scofs, cofs);
-  up(P.sent, ent);
+  up(B.bptr, bptr);
+  up(B.buni, buni);
+  up(B.bch, bch);
+  up(B.cofs, cofs);
+  up(B.ent, ent);
   P.ctx->sync();
-  P.snblk = nblk;
-  P.snu = static_cast<std::int64_t>(buni.size());
-  P.sentb = static_cast<std::int64_t>(ent.size());
+  B.nblk = nblk;
+  B.nu = static_cast<std::int64_t>(buni.size());
+  B.entb = static_cast<std::int64_t>(ent.size());
   // ring slots: kStageC X records + the largest chunk record; the ring is
   // reused for the per-slice reductions at the end
   const long long rec = static_cast<long long>(P.nrhs) * sizeof(T);
-  P.sslot = static_cast<int>((C * rec + maxrec + 127) & ~127ll);
-  P.stage_smem = static_cast<int>(std::max<long long>(static_cast<long long>(kStageNS) * P.sslot,
-                                                      8ll * kWarps * P.nsys * P.nrhs));
-  StageFn<T> fn = stage_kernel<T>(P.nrhs);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.stage_smem) !=
+  B.slot = static_cast<int>((C * rec + maxrec + 127) & ~127ll);
+  B.smem = static_cast<int>(std::max<long long>(static_cast<long long>(kStageNS) * B.slot,
+                                                8ll * kWarps * P.nsys * P.nrhs));
+  StageFn<T> fn = stage_kernel<T>(P.nrhs, fwd);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, B.smem) !=
       cudaSuccess) {
     cudaGetLastError();
     return;
   }
   int per_sm = 0;
-  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStageThreads,
-                                                         P.stage_smem));
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStageThreads, B.smem));
   if (per_sm < 1) return;
-  P.fwd_blocks = static_cast<int>(std::max<long long>(
+  B.blocks = static_cast<int>(std::max<long long>(
       1, std::min<long long>(static_cast<long long>(per_sm) * P.ctx->sm_count, nblk * P.nsys)));
-  const std::size_t need = static_cast<std::size_t>(P.fwd_blocks) * P.nsys * P.nrhs;
-  if (need > P.partial.size()) P.partial.alloc(need);
-  P.staged_f = true;
-  P.blocked_f = false;
+  if (fwd) {
+    P.fwd_blocks = B.blocks;
+    const std::size_t need = static_cast<std::size_t>(B.blocks) * P.nsys * P.nrhs;
+    if (need > P.partial.size()) P.partial.alloc(need);
+    P.blocked_f = false;
+  } else {
+    P.back_blocks = B.blocks;
+    P.blocked_b = false;
+  }
+  B.on = true;
+}
+
+// multi-RHS plans of 32 / 64 / 128 slices without column bands stage the
+// gathered operand (SSB_STAGED=0: neither direction; SSB_STAGED_FWD /
+// SSB_STAGED_BACK per direction)
+template <class T>
+void build_stage(Plan& P) {
+  if (P.nrhs < 2 || P.nband > 1 || !stage_kernel<T>(P.nrhs, true)) return;
+  const int all = env_int("SSB_STAGED", -1);
+  if (all == 0) return;
+  if (all == 1 || env_int("SSB_STAGED_FWD", 1) != 0) build_stage_dir<T>(P, true);
+  if (all == 1 || env_int("SSB_STAGED_BACK", 1) != 0) build_stage_dir<T>(P, false);
 }
 
 // Persistent loop of a paired plan (see sart_persistent_pair_kernel): the
@@ -5455,8 +5499,8 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
   tr.mark("normalisers");
   if (o.dtype == SS_F32) build_blocks<float>(*P);
   else build_blocks<double>(*P);
-  if (o.dtype == SS_F32) build_stage_fwd<float>(*P);
-  else build_stage_fwd<double>(*P);
+  if (o.dtype == SS_F32) build_stage<float>(*P);
+  else build_stage<double>(*P);
   if (P->paired) {
     if (o.dtype == SS_F32) build_paired_t<float>(*P);
     else build_paired_t<double>(*P);

@@ -1,8 +1,10 @@
-"""X-staged multi-RHS K1 (sart_fwd_stage_kernel: blocks of 16 rays, their
-column union streamed chunk by chunk into a shared-memory ring by bulk copies,
-each CSR entry applied from the staged S-wide X record) against the per-row
-multi kernel (SSB_STAGED=0). Both sum every row and slice in CSR order, one
-product at a time, so the iterates are bitwise equal."""
+"""Staged multi-RHS kernels (sart_stage_kernel: blocks of 16 rays (K1) /
+voxels (K2), their index union streamed chunk by chunk into a shared-memory
+ring by bulk copies, neighbouring vector pairs merged, each entry applied from
+the staged S-wide X / W record) against the per-vector multi kernels
+(SSB_STAGED=0 SSB_BLOCKED=0). Both sum every vector and slice in CSR / CSC
+order, one product at a time (the pair merge adds exact zeros), so the
+iterates are bitwise equal."""
 import numpy as np
 import pytest
 
@@ -14,8 +16,9 @@ pytestmark = pytest.mark.gpu
 
 def run(split, opts, S, p1, p2, staged):
     pl = plan_with(split, opts, S, blocked=0, staged=staged)
-    name = pl.describe()["fwd_kernel"]
-    assert ("stage" in name) == bool(staged), name
+    d = pl.describe()
+    for name in (d["fwd_kernel"], d["back_kernel"]):
+        assert ("stage" in name) == bool(staged), d
     pl.set_rhs(0, p1)
     pl.set_rhs(1, p2)
     rep = pl.run()
@@ -53,4 +56,4 @@ def test_staged_not_used_for_other_slice_counts():
     w, split, p1, p2 = slices(2, 5)
     opts = P.SolveOptions(max_iters=3, tol=0.0, relaxation=w.relaxation, dtype="f64")
     pl = plan_with(split, opts, 5, blocked=0, staged=1)
-    assert "stage" not in pl.describe()["fwd_kernel"]
+    assert "stage" not in pl.describe()["fwd_kernel"] + pl.describe()["back_kernel"]
