@@ -62,3 +62,40 @@ def test_tolerance_not_reached_runs_every_update(idx, iters, persist):
         h = plan.history(which)
         assert len(h) == len(want.residual_history) == iters
         assert np.allclose(h, want.residual_history, rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("staged", ["1", "0"])
+def test_multi_rhs_tolerance_not_reached_runs_every_update(staged):
+    """the same for a multi-RHS plan (staged or per-vector kernels): every
+    slice equals its own oracle solve after all max_iters updates"""
+    w, sp, m1, m2 = folded(1)
+    S, iters, tol = 32, 11, 1e-9
+    rng = np.random.default_rng(5)
+    scale = rng.uniform(0.5, 1.5, size=S)
+    p1 = np.concatenate([np.asarray(sp.p1) * c for c in scale])
+    p2 = np.concatenate([np.asarray(sp.p2) * c for c in scale])
+    opts = P.SolveOptions(max_iters=iters, tol=tol, relaxation=w.relaxation, dtype="f64")
+    env = {"SSB_STAGED": staged, "SSB_BLOCKED": "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        plan = P.SartPlan(sp.a1, sp.a2, opts, nrhs=S)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    d = plan.describe()
+    assert ("stage" in d["fwd_kernel"]) == (staged == "1"), d
+    plan.set_rhs(0, p1)
+    plan.set_rhs(1, p2)
+    assert plan.run().iterations == iters
+    x1 = plan.solution(0).reshape(S, -1)
+    x2 = plan.solution(1).reshape(S, -1)
+    for sl in (0, 13, S - 1):
+        want1 = O.sart_solve(m1, np.asarray(sp.p1) * scale[sl], iters, tol, w.relaxation)
+        want2 = O.sart_solve(m2, np.asarray(sp.p2) * scale[sl], iters, tol, w.relaxation)
+        assert rel_err(x1[sl], want1.f) <= 1e-10
+        assert rel_err(x2[sl], want2.f) <= 1e-10
+        assert len(plan.history(0, sl)) == iters
