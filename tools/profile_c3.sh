@@ -2,7 +2,7 @@
 # Launch list + one ncu --set full capture of the paired SART kernels (config 3 fp32).
 # Each ncu command runs only after the same command exited 0 without ncu.
 mkdir -p gpurun_out
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-large"
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain.log; exit 1; }
 # direct launches for the list: ncu drops the K1 nodes of graph replays (measured)
 SSB_GRAPH=0 $CMD > gpurun_out/plain_nograph.log 2>&1 &&

@@ -5,7 +5,7 @@
 set -u
 mkdir -p gpurun_out
 RE=$1; TAG=$2; CFG=$3; DT=$4; shift 4
-CMD="python bench.py --config $CFG --dtype $DT --steps 2 --warmup 3 --no-cpu-baseline --no-f64"
+CMD="python bench.py --config $CFG --dtype $DT --steps 2 --warmup 3 --no-cpu-baseline --no-f64 --no-large"
 env "$@" $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain_$TAG.log; exit 1; }
 env "$@" ncu --set full --clock-control none --import-source on --graph-profiling node -k regex:"$RE" -s 2 -c ${NCU_COUNT:-1} \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_$TAG.log 2>&1

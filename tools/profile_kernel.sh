@@ -5,7 +5,7 @@
 set -u
 mkdir -p gpurun_out
 RE=$1; TAG=$2; shift 2
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-large"
 env SSB_GRAPH=0 "$@" $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain_$TAG.log; exit 1; }
 env SSB_GRAPH=0 "$@" ncu --set full --clock-control none --import-source on -k regex:"$RE" -s 20 -c 2 \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_$TAG.log 2>&1

@@ -13,6 +13,6 @@ i=0
 while read -r line; do
   [ -z "$line" ] && continue
   i=$((i+1))
-  env $line timeout 300 python bench.py --no-cpu-baseline --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/sweep_$i.log 2>&1
+  env $line timeout 300 python bench.py --no-cpu-baseline --no-large --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/sweep_$i.log 2>&1
   summ gpurun_out/sweep_$i.log "$line"
 done

@@ -6,7 +6,7 @@ import os
 import subprocess
 import sys
 
-base = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"]
+base = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-large"]
 extra = os.environ.get("SWEEP_ARGS", "").split()
 for spec in sys.argv[1:]:
     env = dict(os.environ)
