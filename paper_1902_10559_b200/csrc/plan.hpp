@@ -110,6 +110,9 @@ struct Plan {
   // solve, grid barriers between the K1 and K2 phases
   bool persistent = false;
   int pgrid = 0;
+  // stream-resident persistent loop (sart_resident_pair_kernel): one CTA per
+  // SM, both streams staged in shared memory once per launch (csmem bytes)
+  bool resident = false;
   // cluster-persistent loop (sart_cluster_pair_kernel): the grid is one
   // thread-block cluster of ccluster CTAs, hardware cluster barriers
   bool cluster = false;

@@ -946,25 +946,40 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_pair_ker
 // change inside the kernel); the gpu-scope fences of the barrier order them.
 constexpr long long kBarrierSpinCycles = 4000000000LL;  // ~2 s: a lost CTA traps
 
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+// Grid barrier of the persistent loops (all CTAs co-resident): every CTA adds 1 and CTA 0
+// adds 2^31 - (n - 1), so bit 31 of the word flips exactly when all n CTAs
+// have arrived and the low bits are back at 0 (no reset, no last-arriver hop,
+// no generation word). `phase` is the bit-31 value that ends the caller's
+// next barrier: thread 0 reads it from the word before its first arrival
+// (the bit cannot flip before this CTA arrives) and flips it per barrier.
+// One release-ordered reduction after the CTA's bar.sync (publishes every
+// thread's stores), acquire polling by thread 0, then bar.sync: the other
+// threads' weak loads are ordered after the acquire through the CTA barrier.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_sync_flip(unsigned* bar, unsigned& phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      const long long t0 = clock64();
-      while (*gen == g) {
-        __nanosleep(32);
-        if (clock64() - t0 > kBarrierSpinCycles) __trap();
-      }
+    phase ^= 0x80000000u;
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(inc) : "memory");
+    const long long t0 = clock64();
+    while ((ld_acquire_gpu(bar) & 0x80000000u) != phase) {
+      if (clock64() - t0 > kBarrierSpinCycles) __trap();
     }
-    __threadfence();
   }
+  __syncthreads();
+}
+
+// the two systems' run flags read by one thread per CTA and broadcast (every
+// thread reading the state words made one L2 line a hot spot: ~4.7 us per pass
+// with 148 x 32 warps)
+__device__ __forceinline__ void load_run_flags(const int* state, int* flags) {
+  if (threadIdx.x < 2) flags[threadIdx.x] = sys_on(state, threadIdx.x) ? 1 : 0;
   __syncthreads();
 }
 
@@ -976,9 +991,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ double red[2][kWarps];
   __shared__ double sh[kThreads];
   __shared__ int go[2];
+  __shared__ int run[2];
   const int nrow = static_cast<int>(k.rows0), ncol = static_cast<int>(k.cols0);
+  unsigned phase = threadIdx.x == 0 ? ld_acquire_gpu(bar) & 0x80000000u : 0u;
   for (int it = first; it < first + count; ++it) {
-    const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+    load_run_flags(k.state, run);
+    const bool on0 = run[0] != 0, on1 = run[1] != 0;
     if (!on0 && !on1) break;  // every CTA reads the same settled state
     // ---- K1 phase: r = p - A x, w = row_inv r, per-CTA ||r||^2 partials
     {
@@ -1027,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         k.partial[threadIdx.x * gridDim.x + blockIdx.x] = t;
       }
     }
-    grid_sync(bar);
+    grid_sync_flip(bar, phase);
     // ---- ||r|| and the stop test, identically in every CTA (finish_norms order)
     for (int q = 0; q < 2; ++q) {
       const bool on = q ? on1 : on0;
@@ -1092,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    grid_sync(bar);
+    grid_sync_flip(bar, phase);
   }
 }
 
@@ -1538,6 +1556,149 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     mbar_wait(mb_x, par);
     par ^= 1u;
     __syncthreads();  // ldiv of this pass visible to warp 0 of the next
+  }
+}
+
+// ------------------------------------------------------------ stream-resident persistent loop
+// Folded pairs whose mirror-coded streams fit the GPU's shared memory
+// (config 2 fp32: 23 MB over 148 SMs = 160 KB per CTA) but not one cluster:
+// the grid is one CTA per SM, every CTA owns a contiguous block of rows (K1)
+// and of columns (K2) and copies its share of both streams (offsets, values,
+// tile headers, exception lists, bounds, {p, rinv}, cinv) into shared memory
+// once per launch. A pass then reads no matrix byte from L2 or HBM: only the
+// gathers of x / w (L2) and the two grid barriers remain. Rows and columns
+// keep the pair kernels' tile order (seg_dot2m_s): bitwise the iterates of the
+// two-launch loop with the same lane-group widths; every CTA sums the per-CTA
+// ||r||^2 partials in the same fixed order and takes the same stop decision.
+constexpr int kResThreads = 1024;
+constexpr int kResSmemMax = 216 * 1024;  // staged streams per CTA (dynamic smem)
+#ifdef SSB_RES_TIMING
+__device__ unsigned long long res_ticks[8];
+#define RES_T(i) if (blockIdx.x == 0 && threadIdx.x == 0) { const long long t_ = clock64(); res_ticks[i] += t_ - tl_; tl_ = t_; }
+#else
+#define RES_T(i)
+#endif
+
+template <class T, int VSF, int VSB, int UF>
+__global__ void __launch_bounds__(kResThreads, 1)
+    sart_resident_pair_kernel(SartK<T> k, int first, int count, unsigned* bar) {
+  using T2 = typename Vec2<T>::type;
+  constexpr int NW = kResThreads / 32;
+  constexpr int HWF = VSF <= 8 ? 2 : (VSF == 16 ? 4 : 8);
+  constexpr int HWB = VSB <= 8 ? 2 : (VSB == 16 ? 4 : 8);
+  extern __shared__ __align__(16) char rs_smem[];
+  __shared__ double red[2][NW];
+  __shared__ int go[2];
+  __shared__ int run[2];
+  const int nrow = static_cast<int>(k.rows0), ncol = static_cast<int>(k.cols0);
+  const int nct = static_cast<int>(gridDim.x);
+  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+  const CBlock bf = cblock(k.tpf, k.tff, k.epf, nrow, (nrow + nct - 1) / nct, blockIdx.x);
+  const CBlock bb = cblock(k.tpb, k.tfb, k.epb, ncol, (ncol + nct - 1) / nct, blockIdx.x);
+  CStage<T> sf, sb;
+  const long long used = cstage_load<T>(rs_smem, bf, HWF, 4, k.tof, k.rv2, k.thf, k.tpf, k.tff,
+                                        k.epf, k.eif, k.evf, k.pe, sf);
+  cstage_load<T>(rs_smem + used, bb, HWB, 2, k.tob, k.cv2, k.thb, k.tpb, k.tfb, k.epb, k.eib,
+                 k.evb, k.cc, sb);
+  __syncthreads();
+  const T2* xg = reinterpret_cast<const T2*>(k.xx);
+  const T2* wg = reinterpret_cast<const T2*>(k.ww);
+  unsigned phase = threadIdx.x == 0 ? ld_acquire_gpu(bar) & 0x80000000u : 0u;
+#ifdef SSB_RES_TIMING
+  long long tl_ = clock64();
+#endif
+  for (int it = first; it < first + count; ++it) {
+    load_run_flags(k.state, run);
+    const bool on0 = run[0] != 0, on1 = run[1] != 0;
+    if (!on0 && !on1) break;  // every CTA reads the same settled state
+    RES_T(0)
+    // ---- K1 phase over this CTA's rows: r = p - A x, w = row_inv r
+    {
+      const int lane = threadIdx.x & (VSF - 1);
+      const unsigned mask = group_mask<VSF>();
+      double r2a = 0.0, r2b = 0.0;
+      for (int li = threadIdx.x / VSF; li < bf.v1 - bf.v0; li += kResThreads / VSF) {
+        T da, db;
+        seg_dot2m_s<T, VSF, UF>(sf, sf.tf[li], xg, sf.tp[li], sf.tp[li + 1], sf.ep[li],
+                                sf.ep[li + 1], lane, mask, da, db);
+        if (lane == 0) {
+          const T* e = sf.pv + 4 * li;
+          const T ra = e[0] - da, rb = e[1] - db;
+          T2 wo;
+          wo.x = on0 ? e[2] * ra : T(0);
+          wo.y = on1 ? e[3] * rb : T(0);
+          reinterpret_cast<T2*>(k.ww)[bf.v0 + li] = wo;
+          if (on0) r2a += static_cast<double>(ra) * static_cast<double>(ra);
+          if (on1) r2b += static_cast<double>(rb) * static_cast<double>(rb);
+        }
+      }
+      r2a = warp_sum(r2a);
+      r2b = warp_sum(r2b);
+      if (wl == 0) {
+        red[0][warp] = r2a;
+        red[1][warp] = r2b;
+      }
+      __syncthreads();
+      if (warp < 2) {
+        const double t = warp_sum(wl < NW ? red[warp][wl] : 0.0);
+        if (wl == 0) k.partial[warp * nct + blockIdx.x] = t;
+      }
+    }
+    RES_T(1)
+    grid_sync_flip(bar, phase);
+    RES_T(2)
+    // ---- ||r|| and the stop test (warp q: system q), identically in every CTA
+    if (warp < 2) {
+      const bool on = warp ? on1 : on0;
+      double t = 0.0;
+      for (int b = wl; b < nct; b += 32) t += __ldcg(k.partial + warp * nct + b);
+      t = warp_sum(t);
+      if (wl == 0) {
+        int gq = 0;
+        if (on) {
+          const double res = sqrt(t);
+          const bool stop = res <= k.tol * k.pnorm[warp];
+          gq = stop ? 0 : 1;
+          if (blockIdx.x == 0) {
+            k.history[warp * k.hstride + it] = res;
+            if (stop) {
+              k.state[4 * warp + 0] = 1;
+              k.state[4 * warp + 1] = it;
+            }
+          }
+        }
+        go[warp] = gq;
+      }
+    }
+    __syncthreads();
+    const bool u0 = go[0] != 0, u1 = go[1] != 0;
+    if (!u0 && !u1) break;  // both stopped (CTA 0 recorded it)
+    RES_T(3)
+    // ---- K2 phase over this CTA's columns: x += lambda col_inv (A^T w)
+    {
+      const int lane = threadIdx.x & (VSB - 1);
+      const unsigned mask = group_mask<VSB>();
+      for (int li = threadIdx.x / VSB; li < bb.v1 - bb.v0; li += kResThreads / VSB) {
+        const int g = bb.v0 + li;
+        T2 xo;
+        xo.x = xo.y = T(0);
+        if (lane == 0) xo = xg[g];
+        T ua, ub;
+        seg_dot2m_s<T, VSB, UF>(sb, sb.tf[li], wg, sb.tp[li], sb.tp[li + 1], sb.ep[li],
+                                sb.ep[li + 1], lane, mask, ua, ub);
+        if (lane == 0) {
+          const T* ci = sb.pv + 2 * li;
+          if (u0) xo.x = upd(xo.x, k.relax, ua, ci[0]);
+          if (u1) xo.y = upd(xo.y, k.relax, ub, ci[1]);
+          reinterpret_cast<T2*>(k.xx)[g] = xo;
+          if (u0 && !isfinite(static_cast<double>(xo.x))) atomicCAS(&k.state[2], 0, it + 1);
+          if (u1 && !isfinite(static_cast<double>(xo.y))) atomicCAS(&k.state[4 + 2], 0, it + 1);
+        }
+      }
+    }
+    RES_T(4)
+    grid_sync_flip(bar, phase);
+    RES_T(5)
   }
 }
 
@@ -4187,6 +4348,110 @@ void setup_cluster(Plan& P) {
   }
 }
 
+// the stream-resident kernel of a paired plan's shape, or nullptr
+template <class T>
+PersistFn<T> resident_kernel(int vsf, int vsb) {
+#define SSB_RESIDENT(F, B) \
+  if (vsf == F && vsb == B) return sart_resident_pair_kernel<T, F, B, 2>;
+  SSB_RESIDENT(8, 4) SSB_RESIDENT(8, 8) SSB_RESIDENT(8, 16)
+  SSB_RESIDENT(16, 4) SSB_RESIDENT(16, 8) SSB_RESIDENT(16, 16)
+  SSB_RESIDENT(32, 4) SSB_RESIDENT(32, 8) SSB_RESIDENT(32, 16)
+#undef SSB_RESIDENT
+  return nullptr;
+}
+
+// Stream-resident persistent loop of a paired plan (see
+// sart_resident_pair_kernel): one CTA per SM, every CTA's share of both
+// streams must fit kResSmemMax and the grid must be co-resident; otherwise the
+// plan keeps resident = false.
+template <class T>
+void setup_resident(Plan& P) {
+  P.resident = false;
+  PersistFn<T> fn = resident_kernel<T>(P.vs_fwd, P.vs_back);
+  if (!fn || !P.mir_f || !P.mir_b || !P.c16f || !P.c16b || P.stream_cs) return;
+  const int nr = static_cast<int>(P.rows[0]), nc = static_cast<int>(P.cols[0]);
+  std::vector<int> tpf(nr + 1), tff(nr + 1), epf(nr + 1, 0), tpb(nc + 1), tfb(nc + 1),
+      epb(nc + 1, 0);
+  P.ctx->copy(tpf.data(), P.tptr_f.get(), (nr + 1) * sizeof(int));
+  P.ctx->copy(tff.data(), P.tfirst_f.get(), (nr + 1) * sizeof(int));
+  P.ctx->copy(tpb.data(), P.tptr_b.get(), (nc + 1) * sizeof(int));
+  P.ctx->copy(tfb.data(), P.tfirst_b.get(), (nc + 1) * sizeof(int));
+  if (P.eptr_f.get()) P.ctx->copy(epf.data(), P.eptr_f.get(), (nr + 1) * sizeof(int));
+  if (P.eptr_b.get()) P.ctx->copy(epb.data(), P.eptr_b.get(), (nc + 1) * sizeof(int));
+  const auto blk = [](const std::vector<int>& tp, const std::vector<int>& tf,
+                      const std::vector<int>& ep, int n, int per, int b) {
+    CBlock c;
+    c.v0 = std::min(b * per, n);
+    c.v1 = std::min(c.v0 + per, n);
+    c.e0 = tp[c.v0];
+    c.e1 = tp[c.v1];
+    c.t0 = tf[c.v0];
+    c.t1 = tf[c.v1];
+    c.x0 = ep[c.v0];
+    c.x1 = ep[c.v1];
+    return c;
+  };
+  const int g = P.ctx->sm_count;
+  const int pf = (nr + g - 1) / g, pb = (nc + g - 1) / g;
+  long long need = 0;
+  for (int b = 0; b < g; ++b) {
+    need = std::max(need, cstage_bytes<T>(blk(tpf, tff, epf, nr, pf, b), P.hs_f, 4) +
+                              cstage_bytes<T>(blk(tpb, tfb, epb, nc, pb, b), P.hs_b, 2));
+  }
+  if (need > kResSmemMax) return;
+  const int smem = static_cast<int>(need);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kResThreads, smem) !=
+          cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return;
+  }
+  P.pgrid = g;
+  P.csmem = smem;
+  P.gbar.alloc(2);
+  SSB_CUDA(cudaMemsetAsync(P.gbar.get(), 0, 2 * sizeof(unsigned), P.ctx->stream));
+  if (static_cast<std::size_t>(g) * 2 > P.partial.size()) P.partial.alloc(2 * g);
+  P.ctx->sync();
+  P.resident = P.persistent = true;
+}
+
+template <class T>
+void launch_resident(Plan& P, const SartK<T>& k, int first, int count) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.pgrid);
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = P.csmem;
+  cfg.stream = P.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, resident_kernel<T>(P.vs_fwd, P.vs_back), k, first, count,
+                              P.gbar.get()));
+  P.ctx->check_launch("sart_resident_pair_kernel");
+#ifdef SSB_RES_TIMING
+  {
+    cudaStreamCaptureStatus cs;
+    cudaStreamIsCapturing(P.ctx->stream, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      unsigned long long h[8];
+      cudaStreamSynchronize(P.ctx->stream);
+      cudaMemcpyFromSymbol(h, res_ticks, sizeof h);
+      std::fprintf(stderr, "[res ticks] head %llu K1 %llu sync1 %llu norm %llu K2 %llu sync2 %llu (count %d)\n",
+                   h[0], h[1], h[2], h[3], h[4], h[5], count);
+      unsigned long long z[8] = {};
+      cudaMemcpyToSymbol(res_ticks, z, sizeof z);
+    }
+  }
+#endif
+}
+
 // one cooperative launch runs passes [first, first + count) (all CTAs resident)
 template <class T>
 void launch_persistent(Plan& P, const SartK<T>& k, int first, int count) {
@@ -4208,6 +4473,10 @@ void do_iterations(Plan& P, int first, int count) {
   const SartK<T> k = make_args<T>(P);
   if (P.cluster) {
     launch_cluster<T>(P, k, first, count);
+    return;
+  }
+  if (P.resident) {
+    launch_resident<T>(P, k, first, count);
     return;
   }
   if (P.persistent) {
@@ -4776,6 +5045,9 @@ std::string Plan::describe() const {
   std::string pk = cluster ? "sart_cluster_pair_kernel<" + std::string(t) + ", " +
                                  std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
                                  ", 2>"
+                   : resident ? "sart_resident_pair_kernel<" + std::string(t) + ", " +
+                                    std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
+                                    ", 2>"
                    : persistent ? "sart_persistent_pair_kernel<" + std::string(t) + ", " +
                                       std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
                                       ", 2, 4>"
@@ -5536,7 +5808,13 @@ Plan* make_plan(Context* ctx, Matrix* a1, Matrix* a2, const ss_solve_options& o,
     if (!P->cluster) {
       const int want = env_int("SSB_PERSIST", -1);
       const bool small = static_cast<std::size_t>(fb + bb) * 2 <= ctx->l2_bytes;
-      if (want != 0 && want != 2 && (want == 1 || small)) {
+      // streams that fit the shared memory of the whole GPU stay resident
+      // there (3: whenever the shape allows; 1: the L2-streamed grid kernel)
+      if (want == 3 || (want == -1 && small)) {
+        if (o.dtype == SS_F32) setup_resident<float>(*P);
+        else setup_resident<double>(*P);
+      }
+      if (!P->resident && want != 0 && want != 2 && (want == 1 || want == 3 || small)) {
         if (o.dtype == SS_F32) setup_persistent<float>(*P);
         else setup_persistent<double>(*P);
       }
@@ -5932,6 +6210,7 @@ Plan* make_sharded_pair_plan_local(Context* ctx, Matrix* a1, Matrix* a2, std::in
   P->own = l1.release();
   P->own2 = l2.release();
   P->persistent = false;  // the exchange kernels run the loop
+  P->resident = false;
   P->cluster = false;
   P->ccluster = 0;
   P->sharded = true;
