@@ -106,3 +106,51 @@ def test_resident_matches_oracle_and_repeats():
     assert first.tobytes() == again.tobytes()
     got = P.recombine_solution(res.solution(0), res.solution(1))
     assert rel_err(got, want) <= 1e-4
+
+
+def plan_with(sp, opts, persist, p1=None, p2=None):
+    old = os.environ.get("SSB_PERSIST")
+    os.environ["SSB_PERSIST"] = str(persist)
+    try:
+        plan = P.SartPlan(sp.a1, sp.a2, opts)
+    finally:
+        if old is None:
+            os.environ.pop("SSB_PERSIST", None)
+        else:
+            os.environ["SSB_PERSIST"] = old
+    plan.set_rhs(0, sp.p1 if p1 is None else p1)
+    plan.set_rhs(1, sp.p2 if p2 is None else p2)
+    return plan
+
+
+def test_resident_one_system_stops_first():
+    """system 2 gets a zero right-hand side: ||r|| = 0 <= tol * 0 stops it at
+    iteration 0 while system 1 runs on (independent stop state per system)"""
+    w, sp, csr, p = folded(2)
+    opts = P.SolveOptions(max_iters=40, tol=1e-3, relaxation=w.relaxation, dtype="f32")
+    z = np.zeros_like(np.asarray(sp.p2))
+    res, ref = plan_with(sp, opts, 3, p2=z), plan_with(sp, opts, 0, p2=z)
+    assert res.describe()["persistent_kernel"].startswith("sart_resident_pair_kernel")
+    r1, r0 = res.run(), ref.run()
+    assert r1.iterations == r0.iterations > 1
+    assert len(res.history(1)) == 1
+    for which in (0, 1):
+        assert res.solution(which).tobytes() == ref.solution(which).tobytes()
+        assert len(res.history(which)) == len(ref.history(which))
+
+
+def test_resident_divergence_reported_like_two_launch_loop():
+    """a non-finite update seen by one CTA turns that system off in every CTA
+    (its -1 partial in the next pass's exchange); the report names the same
+    iteration as the two-launch loop's"""
+    w, sp, csr, p = folded(2)
+    opts = P.SolveOptions(max_iters=10, tol=0.0, relaxation=w.relaxation, dtype="f32")
+    bad = np.array(sp.p1, dtype=np.float64)
+    bad[7] = np.nan
+    msgs = []
+    for persist in (3, 0):
+        plan = plan_with(sp, opts, persist, p1=bad)
+        with pytest.raises(P.Error) as e:
+            plan.run()
+        msgs.append(str(e.value))
+    assert msgs[0] == msgs[1] and "diverged (non-finite iterate at iteration" in msgs[0], msgs
