@@ -113,6 +113,7 @@ struct Plan {
   // stream-resident persistent loop (sart_resident_pair_kernel): one CTA per
   // SM, both streams staged in shared memory once per launch (csmem bytes)
   bool resident = false;
+  bool res_back = true;  // K2's stream staged too (false: only K1's fits)
   // cluster-persistent loop (sart_cluster_pair_kernel): the grid is one
   // thread-block cluster of ccluster CTAs, hardware cluster barriers
   bool cluster = false;

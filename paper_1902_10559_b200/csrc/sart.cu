@@ -1593,7 +1593,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 
 // ------------------------------------------------------------ stream-resident persistent loop
 // Folded pairs whose mirror-coded streams fit the GPU's shared memory
-// (config 2 fp32: 23 MB over 148 SMs = 160 KB per CTA) but not one cluster:
+// (config 2 fp32: 23 MB over 148 SMs = 160 KB per CTA; fp64: K1's stream only,
+// SB = false, K2 then streams from L2 as in the grid kernel) but not one cluster:
 // the grid is one CTA per SM, every CTA owns a contiguous block of rows (K1)
 // and of columns (K2) and copies its share of both streams (offsets, values,
 // tile headers, exception lists, bounds, {p, rinv}, cinv) into shared memory
@@ -1611,7 +1612,7 @@ __device__ unsigned long long res_ticks[8];
 #define RES_T(i)
 #endif
 
-template <class T, int VSF, int VSB, int UF>
+template <class T, int VSF, int VSB, int UF, bool SB>
 __global__ void __launch_bounds__(kResThreads, 1)
     sart_resident_pair_kernel(SartK<T> k, int first, int count, unsigned* bar) {
   using T2 = typename Vec2<T>::type;
@@ -1630,8 +1631,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
   CStage<T> sf, sb;
   const long long used = cstage_load<T>(rs_smem, bf, HWF, 4, k.tof, k.rv2, k.thf, k.tpf, k.tff,
                                         k.epf, k.eif, k.evf, k.pe, sf);
-  cstage_load<T>(rs_smem + used, bb, HWB, 2, k.tob, k.cv2, k.thb, k.tpb, k.tfb, k.epb, k.eib,
-                 k.evb, k.cc, sb);
+  if constexpr (SB) {  // (SB = false: only K1's stream fits; K2 streams from L2)
+    cstage_load<T>(rs_smem + used, bb, HWB, 2, k.tob, k.cv2, k.thb, k.tpb, k.tfb, k.epb, k.eib,
+                   k.evb, k.cc, sb);
+  }
   __syncthreads();
   const T2* xg = reinterpret_cast<const T2*>(k.xx);
   const T2* wg = reinterpret_cast<const T2*>(k.ww);
@@ -1716,12 +1719,29 @@ __global__ void __launch_bounds__(kResThreads, 1)
         xo.x = xo.y = T(0);
         if (lane == 0) xo = xg[g];
         T ua, ub;
-        seg_dot2m_s<T, VSB, UF>(sb, sb.tf[li], wg, sb.tp[li], sb.tp[li + 1], sb.ep[li],
-                                sb.ep[li + 1], lane, mask, ua, ub);
+        T2 ci;
+        ci.x = ci.y = T(0);
+        if constexpr (SB) {
+          seg_dot2m_s<T, VSB, UF>(sb, sb.tf[li], wg, sb.tp[li], sb.tp[li + 1], sb.ep[li],
+                                  sb.ep[li + 1], lane, mask, ua, ub);
+          if (lane == 0) {
+            ci.x = sb.pv[2 * li];
+            ci.y = sb.pv[2 * li + 1];
+          }
+        } else {
+          const int beg = __ldg(k.tpb + g), end = __ldg(k.tpb + g + 1), tf = __ldg(k.tfb + g);
+          int eb = 0, ee = 0;
+          if (k.epb) {
+            eb = __ldg(k.epb + g);
+            ee = __ldg(k.epb + g + 1);
+          }
+          if (lane == 0) ci = __ldg(reinterpret_cast<const T2*>(k.cc) + g);
+          seg_dot2m<T, VSB, UF, false, true, false>(k.tob, k.tib, k.thb, tf, k.cv2, wg, beg, end,
+                                                    eb, ee, k.eib, k.evb, lane, mask, ua, ub);
+        }
         if (lane == 0) {
-          const T* ci = sb.pv + 2 * li;
-          if (u0) xo.x = upd(xo.x, k.relax, ua, ci[0]);
-          if (u1) xo.y = upd(xo.y, k.relax, ub, ci[1]);
+          if (u0) xo.x = upd(xo.x, k.relax, ua, ci.x);
+          if (u1) xo.y = upd(xo.y, k.relax, ub, ci.y);
           reinterpret_cast<T2*>(k.xx)[g] = xo;
           if (u0 && !isfinite(static_cast<double>(xo.x))) atomicCAS(&k.state[2], 0, it + 1);
           if (u1 && !isfinite(static_cast<double>(xo.y))) atomicCAS(&k.state[4 + 2], 0, it + 1);
@@ -4382,9 +4402,12 @@ void setup_cluster(Plan& P) {
 
 // the stream-resident kernel of a paired plan's shape, or nullptr
 template <class T>
-PersistFn<T> resident_kernel(int vsf, int vsb) {
-#define SSB_RESIDENT(F, B) \
-  if (vsf == F && vsb == B) return sart_resident_pair_kernel<T, F, B, 2>;
+PersistFn<T> resident_kernel(int vsf, int vsb, bool sb) {
+#define SSB_RESIDENT(F, B)                                                    \
+  if (vsf == F && vsb == B) {                                                 \
+    return sb ? sart_resident_pair_kernel<T, F, B, 2, true>                   \
+              : sart_resident_pair_kernel<T, F, B, 2, false>;                 \
+  }
   SSB_RESIDENT(8, 4) SSB_RESIDENT(8, 8) SSB_RESIDENT(8, 16)
   SSB_RESIDENT(16, 4) SSB_RESIDENT(16, 8) SSB_RESIDENT(16, 16)
   SSB_RESIDENT(32, 4) SSB_RESIDENT(32, 8) SSB_RESIDENT(32, 16)
@@ -4399,8 +4422,10 @@ PersistFn<T> resident_kernel(int vsf, int vsb) {
 template <class T>
 void setup_resident(Plan& P) {
   P.resident = false;
-  PersistFn<T> fn = resident_kernel<T>(P.vs_fwd, P.vs_back);
-  if (!fn || !P.mir_f || !P.mir_b || !P.c16f || !P.c16b || P.stream_cs) return;
+  if (!resident_kernel<T>(P.vs_fwd, P.vs_back, true) || !P.mir_f || !P.mir_b || !P.c16f ||
+      !P.c16b || P.stream_cs) {
+    return;
+  }
   const int nr = static_cast<int>(P.rows[0]), nc = static_cast<int>(P.cols[0]);
   std::vector<int> tpf(nr + 1), tff(nr + 1), epf(nr + 1, 0), tpb(nc + 1), tfb(nc + 1),
       epb(nc + 1, 0);
@@ -4425,12 +4450,17 @@ void setup_resident(Plan& P) {
   };
   const int g = P.ctx->sm_count;
   const int pf = (nr + g - 1) / g, pb = (nc + g - 1) / g;
-  long long need = 0;
+  long long need = 0, need_f = 0;
   for (int b = 0; b < g; ++b) {
-    need = std::max(need, cstage_bytes<T>(blk(tpf, tff, epf, nr, pf, b), P.hs_f, 4) +
-                              cstage_bytes<T>(blk(tpb, tfb, epb, nc, pb, b), P.hs_b, 2));
+    const long long f = cstage_bytes<T>(blk(tpf, tff, epf, nr, pf, b), P.hs_f, 4);
+    need_f = std::max(need_f, f);
+    need = std::max(need, f + cstage_bytes<T>(blk(tpb, tfb, epb, nc, pb, b), P.hs_b, 2));
   }
+  // both streams resident, else K1's only (config 2 fp64: K2 streams from L2)
+  P.res_back = need <= kResSmemMax;
+  if (!P.res_back) need = need_f;
   if (need > kResSmemMax) return;
+  PersistFn<T> fn = resident_kernel<T>(P.vs_fwd, P.vs_back, P.res_back);
   const int smem = static_cast<int>(need);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess) {
@@ -4464,8 +4494,8 @@ void launch_resident(Plan& P, const SartK<T>& k, int first, int count) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SSB_CUDA(cudaLaunchKernelEx(&cfg, resident_kernel<T>(P.vs_fwd, P.vs_back), k, first, count,
-                              P.gbar.get()));
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, resident_kernel<T>(P.vs_fwd, P.vs_back, P.res_back), k, first,
+                              count, P.gbar.get()));
   P.ctx->check_launch("sart_resident_pair_kernel");
 #ifdef SSB_RES_TIMING
   {
@@ -5079,7 +5109,7 @@ std::string Plan::describe() const {
                                  ", 2>"
                    : resident ? "sart_resident_pair_kernel<" + std::string(t) + ", " +
                                     std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
-                                    ", 2>"
+                                    (res_back ? ", 2, true>" : ", 2, false>")
                    : persistent ? "sart_persistent_pair_kernel<" + std::string(t) + ", " +
                                       std::to_string(vs_fwd) + ", " + std::to_string(vs_back) +
                                       ", 2, 4>"

@@ -47,7 +47,8 @@ def run_plan(sp, opts, persist, **env):
 
 
 @pytest.mark.parametrize("idx,dtype,env", [
-    (1, "f64", {}), (1, "f32", {}), (2, "f32", {}),
+    (1, "f64", {}), (1, "f32", {}), (2, "f32", {}), (2, "f64", {}),
+    (2, "f64", {"SSB_VS_FWD": 16, "SSB_VS_BACK": 8}),
     (2, "f32", {"SSB_VS_FWD": 16, "SSB_VS_BACK": 8}),
     (2, "f32", {"SSB_VS_FWD": 32, "SSB_VS_BACK": 16}),
 ])
@@ -65,21 +66,22 @@ def test_resident_equals_two_launch_loop(idx, dtype, env):
         assert np.allclose(res.history(which), ref.history(which), rtol=1e-13, atol=0)
 
 
-def test_resident_is_the_default_for_config2_f32():
-    """auto selection: config 2 fp32 fits the GPU's shared memory (the fp64
-    streams do not and keep the L2-streamed grid kernel)"""
+def test_resident_is_the_default_for_config2():
+    """auto selection: config 2's fp32 streams fit the GPU's shared memory
+    (both staged); of the fp64 streams only K1's fits (K2 streams from L2)"""
     w, sp, csr, p = folded(2)
-    for dtype, name in (("f32", "sart_resident_pair_kernel"), ("f64", "sart_persistent_pair_kernel")):
+    for dtype, tail in (("f32", ", 2, true>"), ("f64", ", 2, false>")):
         opts = P.SolveOptions(max_iters=5, tol=0.0, relaxation=w.relaxation, dtype=dtype)
         plan, _ = run_plan(sp, opts, -1)
-        assert plan.describe()["persistent_kernel"].startswith(name), plan.describe()
+        name = plan.describe()["persistent_kernel"]
+        assert name.startswith("sart_resident_pair_kernel") and name.endswith(tail), name
 
 
-@pytest.mark.parametrize("tol", [0.3, 0.05])
-def test_resident_tolerance_stop(tol):
+@pytest.mark.parametrize("tol,dtype", [(0.3, "f32"), (0.05, "f32"), (0.05, "f64")])
+def test_resident_tolerance_stop(tol, dtype):
     """the stop test runs inside the kernel: same iteration, same iterate"""
     w, sp, csr, p = folded(2)
-    opts = P.SolveOptions(max_iters=300, tol=tol, relaxation=w.relaxation, dtype="f32")
+    opts = P.SolveOptions(max_iters=300, tol=tol, relaxation=w.relaxation, dtype=dtype)
     ref, rref = run_plan(sp, opts, 0)
     res, rres = run_plan(sp, opts, 3)
     assert res.describe()["persistent_kernel"].startswith("sart_resident_pair_kernel")
