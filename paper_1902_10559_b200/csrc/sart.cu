@@ -244,6 +244,15 @@ __device__ __forceinline__ bool sys_on(const int* state, int idx) {
   return s[0] == 0 && s[2] == 0;
 }
 
+// One system's run flag from one 16-byte L2 load (sys_on's two dependent
+// volatile loads in one): for kernels that read the state once at their start,
+// after the grid dependency. Every thread of every CTA reads the same line, so
+// the number of dependent round trips is what the start of a pass waits for.
+__device__ __forceinline__ bool sys_on_cg(const int* state, int idx) {
+  const int4 s = __ldcg(reinterpret_cast<const int4*>(state) + idx);
+  return s.x == 0 && s.z == 0;
+}
+
 // Both systems' run flags of a paired plan for a whole CTA: threads 0 / 1 load
 // one system's state words each (one 16-byte L2 load) and broadcast through
 // shared memory. Every thread evaluating sys_on sent 4,736 warps x up to 4
@@ -1815,7 +1824,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_fwd_tiled_ker
   const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
   int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
   double r2 = 0.0;
-  if (sys_on(k.state, 0)) {
+  if (sys_on_cg(k.state, 0)) {
     int beg = 0, end = 0, tf = 0;
     if (g < n) {
       beg = __ldg(k.tpf + g);
@@ -1875,7 +1884,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks) sart_back_tiled_ke
   const int n = static_cast<int>(k.cols0);
   const int gstep = static_cast<int>((long long)gridDim.x * kThreads / VS);
   int g = static_cast<int>((blockIdx.x * (long long)kThreads + threadIdx.x) / VS);
-  if (!sys_on(k.state, 0)) return;
+  if (!sys_on_cg(k.state, 0)) return;
   int beg = 0, end = 0, tf = 0;
   if (g < n) {
     beg = __ldg(k.tpb + g);
@@ -3196,7 +3205,7 @@ template <class T, int VS, int UF, bool U16>
 __global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
     sart_back_xchg_kernel(SartK<T> k, XK<T> x, int it) {
   cudaGridDependencySynchronize();
-  if (!sys_on(k.state, 0)) return;
+  if (!sys_on_cg(k.state, 0)) return;
   const SysK<T>& S = k.s[0];
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -3448,7 +3457,7 @@ __global__ void __launch_bounds__(kThreads, kDirectMinBlocks)
     sart_back_xchg_pair_kernel(SartK<T> k, XK<T> x, int it) {
   using T2 = typename Vec2<T>::type;
   cudaGridDependencySynchronize();
-  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  const bool on0 = sys_on_cg(k.state, 0), on1 = sys_on_cg(k.state, 1);
   if (!on0 && !on1) return;
   const int lane = threadIdx.x & (VS - 1);
   const unsigned mask = group_mask<VS>();
@@ -3485,7 +3494,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) xchg_reduce_pair_kernel(SartK<T> k, XK<T> x, int it) {
   using T2 = typename Vec2<T>::type;
   cudaGridDependencySynchronize();
-  const bool on0 = sys_on(k.state, 0), on1 = sys_on(k.state, 1);
+  const bool on0 = sys_on_cg(k.state, 0), on1 = sys_on_cg(k.state, 1);
   if (!on0 && !on1) return;
   __shared__ int go;
   const long long e = x.local[0] + it;
